@@ -1,0 +1,177 @@
+/*
+ * eucalc.h — C ABI of the B200-native exact Euler-characteristic, Radon and
+ * hybrid transforms of weighted cubical complexes (arxiv 2405.02256).
+ *
+ * Citation keys: P:n = PAPER.md line n (the paper); S:n = SPEC.md line n.
+ *
+ * Conventions shared by every call
+ * --------------------------------
+ *  - Images are C-order (row-major, last axis fastest), axis i of the image
+ *    <-> coordinate xi_i of a direction.
+ *  - Directions are int32 [D][ndim], every coordinate nonzero (genericity,
+ *    P:105). They may live on the host or the device.
+ *  - Heights are integer LATTICE heights H = sum_i xi_i * (L/(M_i-1)) * p_i,
+ *    p the vertex index, M_i the number of vertices on axis i, L the lcm of
+ *    the (M_i - 1) > 0. The paper's normalised height (vertices evenly spaced
+ *    in [-0.5,0.5]^n) is t = (2H - L*csum) / (2L) with csum the sum of
+ *    xi_i over axes with M_i > 1: a strictly increasing map, so every order, tie
+ *    and value is the paper's (E10). eucalc_height_map() returns L and csum.
+ *  - Jumps use the TRUE right-minus-left sign J = chi(lower star) - chi(upper
+ *    star) = -Delta^ord of P:87 (E1).
+ *  - Pointers: every buffer argument may be host memory (pageable or pinned)
+ *    or device memory; the library detects which with cudaPointerGetAttributes
+ *    and copies as needed. All work is enqueued on `stream` (a cudaStream_t,
+ *    NULL = legacy default stream). Calls that return host-visible results
+ *    synchronise that stream, as documented per call.
+ *  - Errors: no C++ exception crosses the ABI. On failure nothing is written
+ *    to the outputs unless stated; eucalc_last_error() describes the failure
+ *    (thread-local).
+ */
+#ifndef EUCALC_H
+#define EUCALC_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum eucalc_status {
+    EUCALC_OK = 0,
+    EUCALC_E_ARG = 1,        /* bad dtype / ndim / shape / kernel / precision / NULL */
+    EUCALC_E_NOMEM = 2,      /* device or host allocation failed */
+    EUCALC_E_CUDA = 3,       /* a CUDA runtime error (see eucalc_last_error) */
+    EUCALC_E_NONGENERIC = 4, /* a direction has a zero coordinate; see eucalc_last_bad_index */
+    EUCALC_E_CAPACITY = 5,   /* an output buffer is too small; the required size is reported */
+    EUCALC_E_RANGE = 6,      /* a height/value bound does not fit the requested element width */
+    EUCALC_E_STATE = 7       /* invalid handle */
+} eucalc_status;
+
+enum { EUCALC_U8 = 0, EUCALC_I16 = 1, EUCALC_I32 = 2 };        /* image dtypes */
+enum { EUCALC_VERTEX = 0, EUCALC_TOP = 1 };                    /* constructions */
+enum { EUCALC_K_GAUSS = 0, EUCALC_K_COS = 1, EUCALC_K_SIN = 2, EUCALC_K_EXP = 3 };
+enum { EUCALC_F32 = 0, EUCALC_F64 = 1 };
+
+typedef struct eucalc_complex eucalc_complex;
+typedef struct eucalc_critical eucalc_critical;
+
+/* A batch of exact step-function representations in CSR form.
+ * Segment s = image * D + direction holds entries [offsets[s], offsets[s+1]):
+ * heights ascending (int lattice heights, see above) and the values there.
+ * The value left of the first height is 0 (implicit leading E[0] = 0).
+ * offsets: int64 [batch*D + 1]; height/value: int32 or int64 [capacity]
+ * (elem_bytes 4 or 8). All three caller-owned. */
+typedef struct eucalc_steps {
+    int64_t *offsets;
+    void *height;
+    void *value;
+    int64_t capacity;   /* entries available in height[] and value[] */
+    int32_t elem_bytes; /* 4 or 8 */
+    int32_t reserved;   /* must be 0 */
+} eucalc_steps;
+
+/* ---- build (P:116 top-cell construction, P:140 dual/vertex construction) ----
+ * img: `batch` same-shape images, C-order, dtype EUCALC_U8/I16/I32, host or
+ * device. ndim 2 or 3; shape[ndim] >= 1. The image is copied (the caller may
+ * free it after the call); the handle is library-owned (eucalc_destroy_complex).
+ * Synchronises `stream` once (reads back max |weight|, used to pick record width).
+ * Errors: E_ARG (dtype/ndim/shape/batch, packed vertex coords need > 32 bits),
+ * E_NOMEM, E_CUDA. */
+eucalc_status eucalc_build_complex(const void *img, int dtype, int ndim, const int64_t *shape,
+                                   int64_t batch, int construction, void *stream,
+                                   eucalc_complex **out);
+eucalc_status eucalc_destroy_complex(eucalc_complex *cx);
+
+/* ---- critical points ----
+ * For every image, vertex x and sign vector eps: Delta^-(eps,x) =
+ * chi(phi|lwst), J(eps,x) = Delta^-(eps,x) - Delta^-(-eps,x) (E1; the
+ * upper star w.r.t. eps is the lower star w.r.t. -eps). Vertices with
+ * Delta^-(eps,x) != 0 or Delta^-(-eps,x) != 0 are kept, per antipodal pair
+ * {eps,-eps}, in a deterministic order. The handle keeps a reference to `cx`
+ * (destroy the critical handle first). Asynchronous. Errors: E_STATE, E_NOMEM, E_CUDA. */
+eucalc_status eucalc_critical_points(const eucalc_complex *cx, void *stream, eucalc_critical **out);
+eucalc_status eucalc_destroy_critical(eucalc_critical *cr);
+
+/* h_counts: host int64 [batch][2^ndim][2] = (N^-, N^ord) per image and orthant
+ * index e (bit i set iff eps_i = +1). Synchronises `stream`. */
+eucalc_status eucalc_critical_counts(const eucalc_critical *cr, int64_t *h_counts, void *stream);
+
+/* h_len: host int64 [batch][2^(ndim-1)] = length of each antipodal-pair list
+ * (pair q = orthant index with bit ndim-1 clear). Synchronises `stream`. */
+eucalc_status eucalc_critical_list_lengths(const eucalc_critical *cr, int64_t *h_len, void *stream);
+
+/* Export the critical list of (image, orthant e): every kept vertex of e's
+ * antipodal pair, with its row-major vertex id, Delta^-(e,x) and J(e,x).
+ * Records with both zero cannot occur; records with Delta^- = 0 (not classical
+ * for e) or J = 0 (not ordinary) can. Order: ascending vertex id.
+ * vertex/dminus/jump: caller-owned, host or device, `cap` entries; *n_out gets
+ * the list length. Synchronises `stream`. E_CAPACITY if cap < length (nothing written). */
+eucalc_status eucalc_critical_export(const eucalc_critical *cr, int64_t image, int orthant,
+                                     int64_t *vertex, int32_t *dminus, int32_t *jump,
+                                     int64_t cap, int64_t *n_out, void *stream);
+
+/* Upper bounds of the total number of entries of the ECT (= classical Radon)
+ * and ordinary Radon outputs for these directions: sum over (image, direction)
+ * of min(list length, height range R). Synchronises `stream` on first use. */
+eucalc_status eucalc_output_bound(const eucalc_critical *cr, const int32_t *dirs, int64_t D,
+                                  int64_t *bound_ect, int64_t *bound_ordinary, void *stream);
+
+/* ---- exact transforms (Lemma 2) ----
+ * For every (image, direction):
+ *   ect       : (T, E)     ECT(xi,t) = sum_{classical x} Delta^- 1[t >= h(x)]
+ *   ordinary  : (T_o, E')  heights where Radon(t+) != Radon(t-), value Radon(t+) (E1)
+ *   classical : (T_c, E_c) heights where Radon(t) != Radon(t-), value Radon(t)   (E7)
+ * Equal heights are merged and zero-net entries dropped (canonical form, E8).
+ * Any of ect/ordinary/classical may be NULL (not computed). A classical
+ * `height` pointer equal to the ect `height` pointer is written once (T_c = T).
+ * Capacity: each non-NULL output must hold eucalc_output_bound() entries
+ * (ect/classical: bound_ect, ordinary: bound_ordinary), else E_CAPACITY with
+ * *required_out (if non-NULL) = that bound and nothing written. Element width 4 is
+ * accepted when every height and value provably fits int32, else E_RANGE.
+ * The exact total of segment s is offsets[s+1] - offsets[s].
+ * Device outputs: asynchronous except the first bound query. Host outputs:
+ * computed into library scratch and copied back, then `stream` is synchronised.
+ * Errors: E_NONGENERIC (eucalc_last_bad_index() = first bad direction),
+ * E_CAPACITY, E_RANGE, E_ARG, E_NOMEM, E_CUDA. */
+eucalc_status eucalc_transforms(const eucalc_critical *cr, const int32_t *dirs, int64_t D,
+                                eucalc_steps *ect, eucalc_steps *ordinary, eucalc_steps *classical,
+                                int64_t *required_out, void *stream);
+eucalc_status eucalc_ect(const eucalc_critical *cr, const int32_t *dirs, int64_t D,
+                         eucalc_steps *ect, int64_t *required_out, void *stream);
+eucalc_status eucalc_radon(const eucalc_critical *cr, const int32_t *dirs, int64_t D,
+                           eucalc_steps *ordinary, eucalc_steps *classical,
+                           int64_t *required_out, void *stream);
+
+/* ---- hybrid transform (Lemma 2) ----
+ * HT(xi) = int kappa(t) Radon(xi,t) dt = -sum_{ordinary x} J(eps,x) kbar(t(x)),
+ * t the paper's normalised height. Kernels (kappa -> kbar):
+ *   GAUSS: exp(-t^2/(2 s^2)) -> s sqrt(pi/2) erf(t/(s sqrt 2)),  param = s > 0
+ *   COS  : cos(2 pi t / P)   -> P/(2 pi) sin(2 pi t / P),       param = P > 0
+ *   SIN  : sin t             -> -cos t,               param ignored
+ *   EXP  : exp t             -> exp t   (Appendix A),   param ignored
+ * out: [batch][D] float (F32) or double (F64), host or device, caller-owned.
+ * Deterministic: identical bits run to run (fixed-order combine).
+ * Errors: E_NONGENERIC, E_ARG, E_NOMEM, E_CUDA. */
+eucalc_status eucalc_hybrid(const eucalc_critical *cr, const int32_t *dirs, int64_t D, int kernel,
+                            double param, int precision, void *out, void *stream);
+
+/* ---- helpers ---- */
+/* L and csum of the height map t = (2H - L*csum)/(2L) for direction dir (host, [ndim]). */
+eucalc_status eucalc_height_map(const eucalc_complex *cx, const int32_t *dir, int64_t *L, int64_t *csum);
+/* Stage timing with CUDA events recorded on the launching stream around each
+ * kernel group: stages "build", "k1_critical", "k2_transforms", "k3_hybrid".
+ * eucalc_profile_enable(1) clears and starts recording on the calling thread,
+ * (0) stops. eucalc_profile_read synchronises the recorded events and returns
+ * the summed milliseconds and number of recorded launches of `stage`. */
+void eucalc_profile_enable(int on);
+int eucalc_profile_read(const char *stage, double *ms, int64_t *launches);
+/* Kernel launches issued by this library on the calling thread since the last reset. */
+int64_t eucalc_launch_count(int reset);
+const char *eucalc_status_string(eucalc_status s);
+const char *eucalc_last_error(void);
+int64_t eucalc_last_bad_index(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* EUCALC_H */

@@ -1,0 +1,309 @@
+"""eucalc-b200: exact ECT / Radon / hybrid transforms of weighted cubical complexes
+(arxiv 2405.02256) on one B200, behind the C ABI of include/eucalc.h.
+
+This module is a thin ctypes binding with the ABI's names: it marshals
+arguments (torch tensors or numpy arrays -> pointers, the current CUDA stream)
+and allocates outputs with torch. Every step of the path runs in the CUDA
+kernels of libeucalc.so; there is no CPU fallback — if the library is missing
+the import of the native layer raises.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libeucalc.so")
+
+OK, E_ARG, E_NOMEM, E_CUDA, E_NONGENERIC, E_CAPACITY, E_RANGE, E_STATE = range(8)
+DTYPES = {np.dtype(np.uint8): 0, np.dtype(np.int16): 1, np.dtype(np.int32): 2}
+CONSTRUCTIONS = {"vertex": 0, "top": 1}
+KERNELS = {"gauss": 0, "cos": 1, "sin": 2, "exp": 3}
+PRECISIONS = {"f32": 0, "f64": 1}
+
+
+class EucalcError(RuntimeError):
+    def __init__(self, status, msg, bad_index=-1, required=None):
+        super().__init__(f"eucalc status {status}: {msg}")
+        self.status = status
+        self.bad_index = bad_index
+        self.required = required
+
+
+class _Steps(ctypes.Structure):
+    _fields_ = [("offsets", ctypes.c_void_p), ("height", ctypes.c_void_p), ("value", ctypes.c_void_p),
+                ("capacity", ctypes.c_int64), ("elem_bytes", ctypes.c_int32), ("reserved", ctypes.c_int32)]
+
+
+_lib = None
+
+
+def lib():
+    """Load libeucalc.so (in-tree). Raises if it is missing: no fallback."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} not built; run `python -m paper_2405_02256_b200._build` "
+                              "(the CUDA extension is required, there is no CPU path)")
+        L = ctypes.CDLL(LIB_PATH)
+        P, I64, I32, St = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int, ctypes.c_int
+        L.eucalc_build_complex.argtypes = [P, I32, I32, P, I64, I32, P, ctypes.POINTER(P)]
+        L.eucalc_destroy_complex.argtypes = [P]
+        L.eucalc_critical_points.argtypes = [P, P, ctypes.POINTER(P)]
+        L.eucalc_destroy_critical.argtypes = [P]
+        L.eucalc_critical_counts.argtypes = [P, P, P]
+        L.eucalc_critical_list_lengths.argtypes = [P, P, P]
+        L.eucalc_critical_list_lengths.restype = St
+        L.eucalc_critical_export.argtypes = [P, I64, I32, P, P, P, I64, ctypes.POINTER(I64), P]
+        L.eucalc_output_bound.argtypes = [P, P, I64, ctypes.POINTER(I64), ctypes.POINTER(I64), P]
+        SP = ctypes.POINTER(_Steps)
+        L.eucalc_transforms.argtypes = [P, P, I64, SP, SP, SP, ctypes.POINTER(I64), P]
+        L.eucalc_ect.argtypes = [P, P, I64, SP, ctypes.POINTER(I64), P]
+        L.eucalc_radon.argtypes = [P, P, I64, SP, SP, ctypes.POINTER(I64), P]
+        L.eucalc_hybrid.argtypes = [P, P, I64, I32, ctypes.c_double, I32, P, P]
+        L.eucalc_height_map.argtypes = [P, P, ctypes.POINTER(I64), ctypes.POINTER(I64)]
+        L.eucalc_profile_enable.argtypes = [I32]
+        L.eucalc_profile_enable.restype = None
+        L.eucalc_profile_read.argtypes = [ctypes.c_char_p, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(I64)]
+        L.eucalc_launch_count.argtypes = [I32]
+        L.eucalc_launch_count.restype = I64
+        L.eucalc_status_string.restype = ctypes.c_char_p
+        L.eucalc_last_error.restype = ctypes.c_char_p
+        L.eucalc_last_bad_index.restype = I64
+        for f in ("eucalc_build_complex", "eucalc_destroy_complex", "eucalc_critical_points",
+                  "eucalc_destroy_critical", "eucalc_critical_counts", "eucalc_critical_export",
+                  "eucalc_output_bound", "eucalc_transforms", "eucalc_ect", "eucalc_radon",
+                  "eucalc_hybrid", "eucalc_height_map"):
+            getattr(L, f).restype = St
+        _lib = L
+    return _lib
+
+
+def _check(st, required=None):
+    if st != OK:
+        L = lib()
+        raise EucalcError(st, L.eucalc_last_error().decode(), L.eucalc_last_bad_index(), required)
+
+
+def _stream(stream):
+    import torch
+
+    if stream is None:
+        if torch.cuda.is_available():
+            return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+        return ctypes.c_void_p(0)
+    if hasattr(stream, "cuda_stream"):
+        return ctypes.c_void_p(stream.cuda_stream)
+    return ctypes.c_void_p(int(stream))
+
+
+def _ptr(x):
+    """(pointer, keepalive) for a torch tensor or numpy array (host or device)."""
+    if hasattr(x, "data_ptr"):
+        return ctypes.c_void_p(x.data_ptr()), x
+    a = np.ascontiguousarray(x)
+    return ctypes.c_void_p(a.ctypes.data), a
+
+
+def _dirs_i32(dirs):
+    if hasattr(dirs, "data_ptr"):
+        import torch
+
+        assert dirs.dtype == torch.int32 and dirs.is_contiguous() and dirs.dim() == 2
+        return dirs
+    return np.ascontiguousarray(np.asarray(dirs, dtype=np.int32).reshape(len(dirs), -1))
+
+
+class Complex:
+    """eucalc_build_complex handle: a batch of same-shape images (P:116 / P:140)."""
+
+    def __init__(self, images, construction="vertex", stream=None):
+        if hasattr(images, "data_ptr"):
+            import torch
+
+            tmap = {torch.uint8: 0, torch.int16: 1, torch.int32: 2}
+            dt = tmap[images.dtype]
+            images = images.contiguous()
+            shape = tuple(images.shape)
+        else:
+            images = np.ascontiguousarray(images)
+            dt = DTYPES[images.dtype]
+            shape = images.shape
+        self.batch = int(shape[0])
+        self.shape = tuple(int(s) for s in shape[1:])
+        self.ndim = len(self.shape)
+        self.construction = construction
+        self.stream = stream
+        p, keep = _ptr(images)
+        shp = (ctypes.c_int64 * self.ndim)(*self.shape)
+        h = ctypes.c_void_p()
+        _check(lib().eucalc_build_complex(p, dt, self.ndim, shp, self.batch, CONSTRUCTIONS[construction],
+                                          _stream(stream), ctypes.byref(h)))
+        self._h = h
+        del keep
+
+    def height_map(self, xi):
+        """(L, csum) with t = (2H - L*csum) / (2L) (paper's normalised height, E10)."""
+        d = (ctypes.c_int32 * self.ndim)(*[int(v) for v in xi])
+        L, cs = ctypes.c_int64(), ctypes.c_int64()
+        _check(lib().eucalc_height_map(self._h, d, ctypes.byref(L), ctypes.byref(cs)))
+        return L.value, cs.value
+
+    def __del__(self):
+        if getattr(self, "_h", None) and _lib is not None:
+            _lib.eucalc_destroy_complex(self._h)
+            self._h = None
+
+
+class Critical:
+    """eucalc_critical_points handle (K1: per-pair critical lists)."""
+
+    def __init__(self, cx: Complex, stream=None):
+        self.cx = cx
+        self.stream = stream
+        h = ctypes.c_void_p()
+        _check(lib().eucalc_critical_points(cx._h, _stream(stream), ctypes.byref(h)))
+        self._h = h
+
+    def counts(self):
+        """int64 [batch, 2^n, 2] = (N^-, N^ord) per orthant (syncs)."""
+        out = np.zeros((self.cx.batch, 1 << self.cx.ndim, 2), dtype=np.int64)
+        _check(lib().eucalc_critical_counts(self._h, ctypes.c_void_p(out.ctypes.data), _stream(self.stream)))
+        return out
+
+    def list_lengths(self):
+        """int64 [batch, 2^(n-1)] lengths of the antipodal-pair lists (syncs)."""
+        out = np.zeros((self.cx.batch, 1 << (self.cx.ndim - 1)), dtype=np.int64)
+        _check(lib().eucalc_critical_list_lengths(self._h, ctypes.c_void_p(out.ctypes.data), _stream(self.stream)))
+        return out
+
+    def export(self, image: int, orthant: int):
+        """(vertex ids, Delta^-, J) of (image, orthant), ascending vertex id (syncs)."""
+        n = ctypes.c_int64()
+        st = lib().eucalc_critical_export(self._h, image, orthant, None, None, None, 0, ctypes.byref(n),
+                                          _stream(self.stream))
+        if st not in (OK, E_CAPACITY):
+            _check(st)
+        k = n.value
+        v = np.empty(k, dtype=np.int64)
+        dm = np.empty(k, dtype=np.int32)
+        j = np.empty(k, dtype=np.int32)
+        _check(lib().eucalc_critical_export(self._h, image, orthant, ctypes.c_void_p(v.ctypes.data),
+                                            ctypes.c_void_p(dm.ctypes.data), ctypes.c_void_p(j.ctypes.data),
+                                            k, ctypes.byref(n), _stream(self.stream)))
+        return v, dm, j
+
+    def output_bound(self, dirs):
+        d = _dirs_i32(dirs)
+        p, keep = _ptr(d)
+        be, bo = ctypes.c_int64(), ctypes.c_int64()
+        _check(lib().eucalc_output_bound(self._h, p, int(d.shape[0]), ctypes.byref(be), ctypes.byref(bo),
+                                         _stream(self.stream)))
+        return be.value, bo.value
+
+    def __del__(self):
+        if getattr(self, "_h", None) and _lib is not None:
+            _lib.eucalc_destroy_critical(self._h)
+            self._h = None
+
+
+def build_complex(images, construction="vertex", stream=None) -> Complex:
+    return Complex(images, construction, stream)
+
+
+def critical_points(cx: Complex, stream=None) -> Critical:
+    return Critical(cx, stream)
+
+
+def _alloc_steps(torch, S, cap, elem_bytes, device, with_height=True):
+    dt = torch.int32 if elem_bytes == 4 else torch.int64
+    pin = device == "cpu" and torch.cuda.is_available()
+    mk = lambda n, t: torch.empty(n, dtype=t, device=device, pin_memory=pin)
+    off = mk(S + 1, torch.int64)
+    h = mk(max(cap, 1), dt) if with_height else None
+    v = mk(max(cap, 1), dt)
+    st = _Steps(off.data_ptr(), h.data_ptr() if h is not None else 0, v.data_ptr(), cap, elem_bytes, 0)
+    return dict(offsets=off, height=h, value=v), st
+
+
+def transforms(cr: Critical, dirs, ect=True, ordinary=True, classical=True, elem_bytes=8, device="cuda",
+               share_heights=False, stream=None):
+    """eucalc_transforms: canonical ECT (T,E) and Radon (T_o,E'), (T_c,E_c) for every
+    (image, direction), as CSR torch tensors on `device` ("cuda" or "cpu").
+
+    share_heights=True lets the classical stream reuse the ECT heights (T_c = T,
+    Lemma 6) instead of writing them twice; its "height" is then the ECT tensor."""
+    import torch
+
+    d = _dirs_i32(dirs)
+    D = int(d.shape[0])
+    S = cr.cx.batch * D
+    bound, _ = cr.output_bound(d)
+    res = {}
+    sts = [None, None, None]
+    for i, (name, want) in enumerate((("ect", ect), ("ordinary", ordinary), ("classical", classical))):
+        if not want:
+            continue
+        share = name == "classical" and share_heights and ect
+        res[name], sts[i] = _alloc_steps(torch, S, bound, elem_bytes, device, with_height=not share)
+        if share:
+            res[name]["height"] = res["ect"]["height"]
+            sts[i].height = sts[0].height
+    p, keep = _ptr(d)
+    req = ctypes.c_int64()
+    refs = [ctypes.byref(s) if s is not None else None for s in sts]
+    _check(lib().eucalc_transforms(cr._h, p, D, refs[0], refs[1], refs[2], ctypes.byref(req),
+                                   _stream(stream if stream is not None else cr.stream)), req.value)
+    return res
+
+
+def ect(cr: Critical, dirs, **kw):
+    return transforms(cr, dirs, ect=True, ordinary=False, classical=False, **kw)["ect"]
+
+
+def radon(cr: Critical, dirs, **kw):
+    r = transforms(cr, dirs, ect=False, ordinary=True, classical=True, **kw)
+    return r["ordinary"], r["classical"]
+
+
+def hybrid(cr: Critical, dirs, kernel="gauss", param=1.0, precision="f64", device="cuda", stream=None):
+    """eucalc_hybrid: HT(xi) = int kappa(t) Radon(xi,t) dt for every (image, direction)."""
+    import torch
+
+    d = _dirs_i32(dirs)
+    D = int(d.shape[0])
+    dt = torch.float32 if precision == "f32" else torch.float64
+    pin = device == "cpu" and torch.cuda.is_available()
+    out = torch.empty((cr.cx.batch, D), dtype=dt, device=device, pin_memory=pin)
+    p, keep = _ptr(d)
+    _check(lib().eucalc_hybrid(cr._h, p, D, KERNELS[kernel], float(param), PRECISIONS[precision],
+                               ctypes.c_void_p(out.data_ptr()),
+                               _stream(stream if stream is not None else cr.stream)))
+    return out
+
+
+def profile_enable(on=True):
+    """Record per-stage CUDA-event times on the launching stream (clears previous records)."""
+    lib().eucalc_profile_enable(1 if on else 0)
+
+
+def profile_read(stage=None):
+    """(milliseconds, launches) summed over recorded `stage` launches (None = all)."""
+    ms, n = ctypes.c_double(), ctypes.c_int64()
+    lib().eucalc_profile_read(stage.encode() if stage else None, ctypes.byref(ms), ctypes.byref(n))
+    return ms.value, n.value
+
+
+def launch_count(reset=False) -> int:
+    return int(lib().eucalc_launch_count(1 if reset else 0))
+
+
+def segment(steps, s):
+    """(heights, values) of CSR segment s as numpy (moves to host)."""
+    off = steps["offsets"]
+    a, b = int(off[s]), int(off[s + 1])
+    h = steps["height"][a:b].cpu().numpy().astype(np.int64)
+    v = steps["value"][a:b].cpu().numpy().astype(np.int64)
+    return h, v

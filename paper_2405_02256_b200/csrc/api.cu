@@ -1,0 +1,786 @@
+// eucalc C ABI — host runtime (handles, validation, capacity protocol, launches).
+// See include/eucalc.h for the contract of every entry point.
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <numeric>
+#include <string>
+#include <vector>
+
+#include "eucalc_internal.cuh"
+
+namespace eucalc {
+int k1_tile_vertices();
+int k3_chunk();
+
+namespace {
+thread_local std::string g_err;
+thread_local int64_t g_bad = -1;
+thread_local int64_t g_launches = 0;
+
+// ---- stage timing (eucalc_profile_*) ----
+struct ProfRec {
+    std::string stage;
+    cudaEvent_t a, b;
+    int64_t launches;
+};
+thread_local bool g_prof = false;
+thread_local std::vector<ProfRec> g_prof_recs;
+thread_local std::vector<cudaEvent_t> g_ev_pool;
+
+cudaEvent_t ev_get() {
+    if (!g_ev_pool.empty()) {
+        cudaEvent_t e = g_ev_pool.back();
+        g_ev_pool.pop_back();
+        return e;
+    }
+    cudaEvent_t e = nullptr;
+    cudaEventCreate(&e);
+    return e;
+}
+struct ProfScope {
+    bool on;
+    cudaStream_t st;
+    cudaEvent_t a = nullptr;
+    int64_t l0;
+    std::string stage;
+    ProfScope(const char *name, cudaStream_t s) : on(g_prof), st(s), l0(g_launches), stage(name) {
+        if (on) {
+            a = ev_get();
+            cudaEventRecord(a, st);
+        }
+    }
+    ~ProfScope() {
+        if (on) {
+            cudaEvent_t b = ev_get();
+            cudaEventRecord(b, st);
+            g_prof_recs.push_back(ProfRec{stage, a, b, g_launches - l0});
+        }
+    }
+};
+
+eucalc_status fail(eucalc_status s, const std::string &msg) {
+    g_err = msg;
+    return s;
+}
+eucalc_status cuda_fail(cudaError_t e, const char *where) {
+    g_err = std::string(where) + ": " + cudaGetErrorString(e);
+    return EUCALC_E_CUDA;
+}
+#define CK(expr)                                                 \
+    do {                                                         \
+        cudaError_t _e = (expr);                                 \
+        if (_e != cudaSuccess) return cuda_fail(_e, #expr);      \
+    } while (0)
+
+bool is_device_ptr(const void *p) {
+    if (!p) return false;
+    cudaPointerAttributes at;
+    cudaError_t e = cudaPointerGetAttributes(&at, p);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged;
+}
+
+int num_sms() {
+    static thread_local int n = 0;
+    if (!n) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+        if (n <= 0) n = 148;
+    }
+    return n;
+}
+
+int bits_for(int64_t v) {  // bits to hold 0..v
+    int b = 1;
+    while ((int64_t(1) << b) <= v) ++b;
+    return b;
+}
+
+template <typename T>
+__global__ void maxabs_kernel(const T *p, int64_t n, unsigned long long *out) {
+    unsigned long long m = 0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        long long v = (long long)p[i];
+        unsigned long long a = (unsigned long long)(v < 0 ? -v : v);
+        m = a > m ? a : m;
+    }
+    for (int d = 16; d; d >>= 1) {
+        unsigned long long o = __shfl_xor_sync(0xffffffffu, m, d);
+        m = o > m ? o : m;
+    }
+    if ((threadIdx.x & 31) == 0) atomicMax(out, m);
+}
+
+struct DirPlan {
+    std::vector<int32_t> host;  // [D][n]
+    std::vector<DirInfo> info;
+    std::vector<int32_t> csum;
+    std::vector<int> orthant;
+    int R_max = 0;
+};
+
+eucalc_status plan_dirs(const Complex *cx, const int32_t *dirs, int64_t D, cudaStream_t st, DirPlan &p) {
+    if (D < 0) return fail(EUCALC_E_ARG, "D < 0");
+    if (D > 0 && !dirs) return fail(EUCALC_E_ARG, "dirs is NULL");
+    const int n = cx->ndim;
+    p.host.resize((size_t)D * n);
+    if (D > 0) {
+        if (is_device_ptr(dirs)) {
+            CK(cudaMemcpyAsync(p.host.data(), dirs, sizeof(int32_t) * D * n, cudaMemcpyDeviceToHost, st));
+            CK(cudaStreamSynchronize(st));
+        } else {
+            memcpy(p.host.data(), dirs, sizeof(int32_t) * D * n);
+        }
+    }
+    p.info.resize(D);
+    p.csum.resize(D);
+    p.orthant.resize(D);
+    p.R_max = 1;
+    const int full = (1 << n) - 1;
+    for (int64_t d = 0; d < D; ++d) {
+        DirInfo di{};
+        int e = 0;
+        int64_t lo = 0, hi = 0, cs = 0;
+        for (int k = 0; k < n; ++k) {
+            const int64_t xi = p.host[d * n + k];
+            if (xi == 0) {
+                g_bad = d;
+                return fail(EUCALC_E_NONGENERIC, "direction " + std::to_string(d) + " has a zero coordinate (P:105)");
+            }
+            if (xi > 0) e |= 1 << k;
+            const int64_t xs = xi * cx->scale[k];
+            if (xs > INT32_MAX || xs < INT32_MIN) return fail(EUCALC_E_RANGE, "scaled direction overflows int32");
+            di.xs[k] = (int)xs;
+            const int64_t ext = xs * (cx->M[k] - 1);
+            if (ext < 0) lo += ext; else hi += ext;
+            if (cx->M[k] > 1) cs += xi;
+        }
+        if (lo < -(int64_t(1) << 30) || hi > (int64_t(1) << 30))
+            return fail(EUCALC_E_RANGE, "lattice heights exceed the int32 kernel range");
+        di.hlo = (int)lo;
+        di.R = (int)(hi - lo + 1);
+        const bool rep = ((e >> (n - 1)) & 1) == 0;
+        di.q = rep ? e : (e ^ full);
+        di.swap = rep ? 0 : 1;
+        p.info[d] = di;
+        p.csum[d] = (int32_t)cs;
+        p.orthant[d] = e;
+        p.R_max = std::max(p.R_max, di.R);
+    }
+    return EUCALC_OK;
+}
+
+eucalc_status sync_counts(Critical *cr, cudaStream_t st) {
+    if (cr->have_host) return EUCALC_OK;
+    const Complex *cx = cr->cx;
+    const int64_t nc = cx->batch * cr->Q;
+    const int64_t ns = cx->batch * (1 << cx->ndim) * 2 + nc;
+    std::vector<int32_t> c(nc);
+    cr->h_count = new (std::nothrow) int64_t[nc];
+    cr->h_stats = new (std::nothrow) int64_t[ns];
+    if (!cr->h_count || !cr->h_stats) return fail(EUCALC_E_NOMEM, "host alloc");
+    CK(cudaMemcpyAsync(c.data(), cr->d_count, sizeof(int32_t) * nc, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(cr->h_stats, cr->d_stats, sizeof(int64_t) * ns, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    cr->max_count = 0;
+    for (int64_t i = 0; i < nc; ++i) {
+        cr->h_count[i] = c[i];
+        cr->max_count = std::max<int64_t>(cr->max_count, c[i]);
+    }
+    cr->max_abs_sum = 0;
+    for (int64_t i = 0; i < nc; ++i)
+        cr->max_abs_sum = std::max<int64_t>(cr->max_abs_sum, cr->h_stats[cx->batch * (1 << cx->ndim) * 2 + i]);
+    cr->have_host = true;
+    return EUCALC_OK;
+}
+
+eucalc_status bounds(Critical *cr, const DirPlan &p, cudaStream_t st, int64_t &bound) {
+    eucalc_status s = sync_counts(cr, st);
+    if (s != EUCALC_OK) return s;
+    bound = 0;
+    const int64_t D = (int64_t)p.info.size();
+    for (int64_t b = 0; b < cr->cx->batch; ++b)
+        for (int64_t d = 0; d < D; ++d)
+            bound += std::min<int64_t>(cr->h_count[b * cr->Q + p.info[d].q], p.info[d].R);
+    return EUCALC_OK;
+}
+
+}  // namespace
+
+void count_launch(int n) { g_launches += n; }
+
+}  // namespace eucalc
+
+using namespace eucalc;
+
+struct eucalc_complex : Complex {};
+struct eucalc_critical : Critical {};
+
+extern "C" {
+
+const char *eucalc_status_string(eucalc_status s) {
+    switch (s) {
+    case EUCALC_OK: return "ok";
+    case EUCALC_E_ARG: return "invalid argument";
+    case EUCALC_E_NOMEM: return "out of memory";
+    case EUCALC_E_CUDA: return "CUDA error";
+    case EUCALC_E_NONGENERIC: return "non-generic direction (zero coordinate)";
+    case EUCALC_E_CAPACITY: return "output capacity too small";
+    case EUCALC_E_RANGE: return "value range exceeded";
+    case EUCALC_E_STATE: return "invalid handle";
+    }
+    return "unknown status";
+}
+const char *eucalc_last_error(void) { return g_err.c_str(); }
+
+void eucalc_profile_enable(int on) {
+    for (auto &r : g_prof_recs) {
+        cudaEventSynchronize(r.b);
+        g_ev_pool.push_back(r.a);
+        g_ev_pool.push_back(r.b);
+    }
+    g_prof_recs.clear();
+    g_prof = on != 0;
+}
+
+int eucalc_profile_read(const char *stage, double *ms, int64_t *launches) {
+    double t = 0;
+    int64_t n = 0;
+    for (auto &r : g_prof_recs) {
+        if (stage && r.stage != stage) continue;
+        cudaEventSynchronize(r.b);
+        float x = 0;
+        cudaEventElapsedTime(&x, r.a, r.b);
+        t += x;
+        n += r.launches;
+    }
+    if (ms) *ms = t;
+    if (launches) *launches = n;
+    return 0;
+}
+int64_t eucalc_last_bad_index(void) { return g_bad; }
+int64_t eucalc_launch_count(int reset) {
+    int64_t v = g_launches;
+    if (reset) g_launches = 0;
+    return v;
+}
+
+eucalc_status eucalc_build_complex(const void *img, int dtype, int ndim, const int64_t *shape, int64_t batch,
+                                   int construction, void *stream, eucalc_complex **out) {
+    if (!out) return fail(EUCALC_E_ARG, "out is NULL");
+    *out = nullptr;
+    if (!img || !shape) return fail(EUCALC_E_ARG, "img/shape is NULL");
+    if (dtype < EUCALC_U8 || dtype > EUCALC_I32) return fail(EUCALC_E_ARG, "bad dtype");
+    if (ndim != 2 && ndim != 3) return fail(EUCALC_E_ARG, "ndim must be 2 or 3");
+    if (batch < 1) return fail(EUCALC_E_ARG, "batch < 1");
+    if (construction != EUCALC_VERTEX && construction != EUCALC_TOP) return fail(EUCALC_E_ARG, "bad construction");
+    cudaStream_t st = (cudaStream_t)stream;
+    eucalc_complex *cx = new (std::nothrow) eucalc_complex();
+    if (!cx) return fail(EUCALC_E_NOMEM, "host alloc");
+    cx->ndim = ndim;
+    cx->dtype = dtype;
+    cx->construction = construction;
+    cx->batch = batch;
+    cx->npix = 1;
+    cx->nvert = 1;
+    for (int k = 0; k < ndim; ++k) {
+        if (shape[k] < 1 || shape[k] > (1 << 20)) {
+            delete cx;
+            return fail(EUCALC_E_ARG, "shape out of range");
+        }
+        cx->m[k] = shape[k];
+        cx->M[k] = construction == EUCALC_VERTEX ? shape[k] : shape[k] + 1;
+        cx->npix *= cx->m[k];
+        cx->nvert *= cx->M[k];
+    }
+    if (cx->nvert > INT32_MAX) {
+        delete cx;
+        return fail(EUCALC_E_ARG, "image too large");
+    }
+    // packed coordinates: axis n-1 in the low bits
+    int sh = 0;
+    for (int k = ndim - 1; k >= 0; --k) {
+        int bw = bits_for(cx->M[k] - 1);
+        cx->sh[k] = sh;
+        cx->msk[k] = (uint32_t)((1ull << bw) - 1);
+        sh += bw;
+    }
+    if (sh > 32) {
+        delete cx;
+        return fail(EUCALC_E_ARG, "packed vertex coordinates need more than 32 bits");
+    }
+    // height scale (E10): L = lcm of (M_i - 1) > 0
+    int64_t L = 1;
+    for (int k = 0; k < ndim; ++k)
+        if (cx->M[k] > 1) L = L / std::gcd(L, cx->M[k] - 1) * (cx->M[k] - 1);
+    cx->L = L;
+    for (int k = 0; k < ndim; ++k) cx->scale[k] = cx->M[k] > 1 ? L / (cx->M[k] - 1) : 0;
+    const size_t esz = dtype == EUCALC_U8 ? 1 : dtype == EUCALC_I16 ? 2 : 4;
+    const size_t bytes = esz * (size_t)(cx->npix * batch);
+    cudaError_t e = cudaMallocAsync(&cx->d_img, bytes, st);
+    if (e != cudaSuccess) {
+        delete cx;
+        return cuda_fail(e, "cudaMallocAsync(image)");
+    }
+    e = cudaMemcpyAsync(cx->d_img, img, bytes, is_device_ptr(img) ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st);
+    unsigned long long *d_max = nullptr;
+    if (e == cudaSuccess) e = cudaMallocAsync(&d_max, sizeof(unsigned long long), st);
+    if (e == cudaSuccess) e = cudaMemsetAsync(d_max, 0, sizeof(unsigned long long), st);
+    if (e == cudaSuccess) {
+        const int64_t n = cx->npix * batch;
+        ProfScope ps("build", st);
+        const unsigned g = (unsigned)std::min<int64_t>(4 * 148, (n + 255) / 256);
+        if (dtype == EUCALC_U8) maxabs_kernel<<<g, 256, 0, st>>>((const uint8_t *)cx->d_img, n, d_max);
+        else if (dtype == EUCALC_I16) maxabs_kernel<<<g, 256, 0, st>>>((const int16_t *)cx->d_img, n, d_max);
+        else maxabs_kernel<<<g, 256, 0, st>>>((const int32_t *)cx->d_img, n, d_max);
+        count_launch();
+        e = cudaGetLastError();
+    }
+    unsigned long long hmax = 0;
+    if (e == cudaSuccess) e = cudaMemcpyAsync(&hmax, d_max, sizeof(hmax), cudaMemcpyDeviceToHost, st);
+    if (d_max) cudaFreeAsync(d_max, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) {
+        cudaFreeAsync(cx->d_img, st);
+        delete cx;
+        return cuda_fail(e, "build_complex");
+    }
+    cx->max_abs_w = (int64_t)hmax;
+    cx->owner_stream = st;
+    *out = cx;
+    return EUCALC_OK;
+}
+
+eucalc_status eucalc_destroy_complex(eucalc_complex *cx) {
+    if (!cx) return fail(EUCALC_E_STATE, "NULL handle");
+    if (cx->d_img) cudaFree(cx->d_img);
+    delete cx;
+    return EUCALC_OK;
+}
+
+eucalc_status eucalc_critical_points(const eucalc_complex *cx, void *stream, eucalc_critical **out) {
+    if (!out) return fail(EUCALC_E_ARG, "out is NULL");
+    *out = nullptr;
+    if (!cx || !cx->d_img) return fail(EUCALC_E_STATE, "invalid complex");
+    cudaStream_t st = (cudaStream_t)stream;
+    eucalc_critical *cr = new (std::nothrow) eucalc_critical();
+    if (!cr) return fail(EUCALC_E_NOMEM, "host alloc");
+    const int n = cx->ndim;
+    cr->cx = cx;
+    cr->Q = 1 << (n - 1);
+    // |Delta^-| <= 2^n max|w| must fit the record's int16 halves, J = a - b is formed in int32
+    cr->wide = ((int64_t(1) << n) * cx->max_abs_w) > 32767;
+    cr->vcap = cx->nvert;
+    const size_t rsz = cr->wide ? sizeof(Rec32) : sizeof(Rec16);
+    const int64_t nlist = cx->batch * cr->Q;
+    const int64_t nstats = cx->batch * (1 << n) * 2 + nlist;
+    // tile shape: full rows when they fit (row-major list order)
+    const int TV = k1_tile_vertices();
+    const int MX = (int)cx->M[n - 1], MY = (int)cx->M[n - 2];
+    int TX = std::min(MX, TV);
+    int TY = std::max(1, std::min(MY, TV / TX));
+    const int tiles_x = (MX + TX - 1) / TX, tiles_y = (MY + TY - 1) / TY;
+    const int tiles_z = n == 3 ? (int)cx->M[0] : 1;
+    const int64_t ntiles = cx->batch * (int64_t)tiles_x * tiles_y * tiles_z;
+    unsigned long long *flags = nullptr;
+    unsigned int *ticket = nullptr;
+    cudaError_t e = cudaMallocAsync(&cr->d_rec, rsz * nlist * cr->vcap, st);
+    if (e == cudaSuccess) e = cudaMallocAsync(&cr->d_count, sizeof(int32_t) * nlist, st);
+    if (e == cudaSuccess) e = cudaMallocAsync(&cr->d_stats, sizeof(int64_t) * nstats, st);
+    if (e == cudaSuccess) e = cudaMallocAsync(&flags, sizeof(unsigned long long) * ntiles * cr->Q, st);
+    if (e == cudaSuccess) e = cudaMallocAsync(&ticket, sizeof(unsigned int), st);
+    if (e == cudaSuccess) e = cudaMemsetAsync(cr->d_stats, 0, sizeof(int64_t) * nstats, st);
+    if (e == cudaSuccess) e = cudaMemsetAsync(flags, 0, sizeof(unsigned long long) * ntiles * cr->Q, st);
+    if (e == cudaSuccess) e = cudaMemsetAsync(ticket, 0, sizeof(unsigned int), st);
+    if (e == cudaSuccess) {
+        K1Args a{};
+        a.img = cx->d_img;
+        a.dtype = cx->dtype;
+        a.construction = cx->construction;
+        a.ndim = n;
+        a.batch = cx->batch;
+        a.npix = cx->npix;
+        a.vcap = cr->vcap;
+        for (int k = 0; k < n; ++k) {
+            a.m[k] = (int)cx->m[k];
+            a.M[k] = (int)cx->M[k];
+            a.sh[k] = cx->sh[k];
+        }
+        a.TX = TX;
+        a.TY = TY;
+        a.tiles_x = tiles_x;
+        a.tiles_y = tiles_y;
+        a.tiles_z = tiles_z;
+        a.rec = cr->d_rec;
+        a.wide = cr->wide;
+        a.count = cr->d_count;
+        a.flags = flags;
+        a.ticket = ticket;
+        a.stats = cr->d_stats;
+        a.abs_sum = cr->d_stats + cx->batch * (1 << n) * 2;
+        ProfScope ps("k1_critical", st);
+        e = launch_k1(a, st);
+    }
+    if (flags) cudaFreeAsync(flags, st);
+    if (ticket) cudaFreeAsync(ticket, st);
+    if (e != cudaSuccess) {
+        if (cr->d_rec) cudaFreeAsync(cr->d_rec, st);
+        if (cr->d_count) cudaFreeAsync(cr->d_count, st);
+        if (cr->d_stats) cudaFreeAsync(cr->d_stats, st);
+        delete cr;
+        return cuda_fail(e, "critical_points");
+    }
+    *out = cr;
+    return EUCALC_OK;
+}
+
+eucalc_status eucalc_destroy_critical(eucalc_critical *cr) {
+    if (!cr) return fail(EUCALC_E_STATE, "NULL handle");
+    cudaFree(cr->d_rec);
+    cudaFree(cr->d_count);
+    cudaFree(cr->d_stats);
+    delete[] cr->h_count;
+    delete[] cr->h_stats;
+    delete cr;
+    return EUCALC_OK;
+}
+
+eucalc_status eucalc_critical_counts(const eucalc_critical *ccr, int64_t *h_counts, void *stream) {
+    if (!ccr || !h_counts) return fail(EUCALC_E_ARG, "NULL argument");
+    eucalc_critical *cr = const_cast<eucalc_critical *>(ccr);
+    eucalc_status s = sync_counts(cr, (cudaStream_t)stream);
+    if (s != EUCALC_OK) return s;
+    memcpy(h_counts, cr->h_stats, sizeof(int64_t) * cr->cx->batch * (1 << cr->cx->ndim) * 2);
+    return EUCALC_OK;
+}
+
+eucalc_status eucalc_critical_list_lengths(const eucalc_critical *ccr, int64_t *h_len, void *stream) {
+    if (!ccr || !h_len) return fail(EUCALC_E_ARG, "NULL argument");
+    eucalc_critical *cr = const_cast<eucalc_critical *>(ccr);
+    eucalc_status s = sync_counts(cr, (cudaStream_t)stream);
+    if (s != EUCALC_OK) return s;
+    memcpy(h_len, cr->h_count, sizeof(int64_t) * cr->cx->batch * cr->Q);
+    return EUCALC_OK;
+}
+
+eucalc_status eucalc_critical_export(const eucalc_critical *ccr, int64_t image, int orthant, int64_t *vertex,
+                                     int32_t *dminus, int32_t *jump, int64_t cap, int64_t *n_out, void *stream) {
+    if (!ccr || !n_out) return fail(EUCALC_E_ARG, "NULL argument");
+    eucalc_critical *cr = const_cast<eucalc_critical *>(ccr);
+    const Complex *cx = cr->cx;
+    const int n = cx->ndim, full = (1 << n) - 1;
+    if (image < 0 || image >= cx->batch || orthant < 0 || orthant > full) return fail(EUCALC_E_ARG, "bad image/orthant");
+    cudaStream_t st = (cudaStream_t)stream;
+    eucalc_status s = sync_counts(cr, st);
+    if (s != EUCALC_OK) return s;
+    const bool rep = ((orthant >> (n - 1)) & 1) == 0;
+    const int q = rep ? orthant : (orthant ^ full);
+    const int64_t len = cr->h_count[image * cr->Q + q];
+    *n_out = len;
+    if (cap < len) return fail(EUCALC_E_CAPACITY, "export capacity");
+    const size_t rsz = cr->wide ? sizeof(Rec32) : sizeof(Rec16);
+    std::vector<unsigned char> raw(rsz * len);
+    if (len) {
+        CK(cudaMemcpyAsync(raw.data(), (const unsigned char *)cr->d_rec + rsz * (image * cr->Q + q) * cr->vcap,
+                           rsz * len, cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+    }
+    struct Row { int64_t v; int32_t dm, j; };
+    std::vector<Row> rows(len);
+    for (int64_t i = 0; i < len; ++i) {
+        uint32_t c;
+        int32_t a, b;
+        if (cr->wide) {
+            const Rec32 *r = (const Rec32 *)raw.data() + i;
+            c = r->c; a = r->a; b = r->b;
+        } else {
+            const Rec16 *r = (const Rec16 *)raw.data() + i;
+            c = r->c; a = r->a; b = r->b;
+        }
+        int64_t vid = 0;
+        for (int k = 0; k < n; ++k) vid = vid * cx->M[k] + ((c >> cx->sh[k]) & cx->msk[k]);
+        const int32_t dm = rep ? a : b, other = rep ? b : a;
+        rows[i] = Row{vid, dm, dm - other};
+    }
+    std::sort(rows.begin(), rows.end(), [](const Row &x, const Row &y) { return x.v < y.v; });
+    std::vector<int64_t> hv(len);
+    std::vector<int32_t> hd(len), hj(len);
+    for (int64_t i = 0; i < len; ++i) { hv[i] = rows[i].v; hd[i] = rows[i].dm; hj[i] = rows[i].j; }
+    auto put = [&](void *dst, const void *src, size_t bytes) -> cudaError_t {
+        if (!dst || !bytes) return cudaSuccess;
+        if (is_device_ptr(dst)) return cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, st);
+        memcpy(dst, src, bytes);
+        return cudaSuccess;
+    };
+    CK(put(vertex, hv.data(), sizeof(int64_t) * len));
+    CK(put(dminus, hd.data(), sizeof(int32_t) * len));
+    CK(put(jump, hj.data(), sizeof(int32_t) * len));
+    CK(cudaStreamSynchronize(st));
+    return EUCALC_OK;
+}
+
+eucalc_status eucalc_output_bound(const eucalc_critical *ccr, const int32_t *dirs, int64_t D, int64_t *bound_ect,
+                                  int64_t *bound_ordinary, void *stream) {
+    if (!ccr) return fail(EUCALC_E_STATE, "NULL handle");
+    eucalc_critical *cr = const_cast<eucalc_critical *>(ccr);
+    DirPlan p;
+    eucalc_status s = plan_dirs(cr->cx, dirs, D, (cudaStream_t)stream, p);
+    if (s != EUCALC_OK) return s;
+    int64_t bnd = 0;
+    s = bounds(cr, p, (cudaStream_t)stream, bnd);
+    if (s != EUCALC_OK) return s;
+    if (bound_ect) *bound_ect = bnd;
+    if (bound_ordinary) *bound_ordinary = bnd;
+    return EUCALC_OK;
+}
+
+eucalc_status eucalc_transforms(const eucalc_critical *ccr, const int32_t *dirs, int64_t D, eucalc_steps *ect,
+                                eucalc_steps *ordinary, eucalc_steps *classical, int64_t *required_out,
+                                void *stream) {
+    if (!ccr) return fail(EUCALC_E_STATE, "NULL handle");
+    eucalc_critical *cr = const_cast<eucalc_critical *>(ccr);
+    const Complex *cx = cr->cx;
+    cudaStream_t st = (cudaStream_t)stream;
+    DirPlan p;
+    eucalc_status s = plan_dirs(cx, dirs, D, st, p);
+    if (s != EUCALC_OK) return s;
+    int64_t bnd = 0;
+    s = bounds(cr, p, st, bnd);
+    if (s != EUCALC_OK) return s;
+    if (required_out) *required_out = bnd;
+    eucalc_steps *outs[3] = {ect, ordinary, classical};
+    int eb = 0;
+    for (eucalc_steps *o : outs) {
+        if (!o) continue;
+        if (!o->offsets || (!o->height && o != classical) || !o->value) return fail(EUCALC_E_ARG, "NULL output array");
+        if (o->elem_bytes != 4 && o->elem_bytes != 8) return fail(EUCALC_E_ARG, "elem_bytes must be 4 or 8");
+        if (eb && o->elem_bytes != eb) return fail(EUCALC_E_ARG, "all outputs must share elem_bytes");
+        eb = o->elem_bytes;
+        if (o->capacity < bnd) return fail(EUCALC_E_CAPACITY, "capacity " + std::to_string(o->capacity) + " < required bound " + std::to_string(bnd));
+    }
+    if (!eb) return EUCALC_OK;  // nothing requested
+    // value bounds: every bin sum, ECT and Radon value is bounded by the list's sum |a|+|b|
+    if (cr->max_abs_sum >= (int64_t(1) << 31)) return fail(EUCALC_E_RANGE, "total |weight| of a critical list exceeds 2^31");
+    if (bnd >= (int64_t(1) << 31)) return fail(EUCALC_E_RANGE, "more than 2^31 output entries in one call");
+    const int64_t S = cx->batch * D;
+    if (S == 0) return EUCALC_OK;
+    const bool cls_alias = classical && ect && (classical->height == ect->height || !classical->height);
+    if (classical && !classical->height && !ect) return fail(EUCALC_E_ARG, "classical height is NULL");
+    // host outputs -> device scratch
+    bool host_out = false;
+    for (eucalc_steps *o : outs)
+        if (o && !is_device_ptr(o->value)) host_out = true;
+    const size_t esz = (size_t)eb;
+    std::vector<void *> scratch;
+    auto dalloc = [&](size_t bytes) -> void * {
+        void *q = nullptr;
+        if (cudaMallocAsync(&q, bytes, st) != cudaSuccess) return nullptr;
+        scratch.push_back(q);
+        return q;
+    };
+    auto free_scratch = [&]() { for (void *q : scratch) cudaFreeAsync(q, st); };
+    K2Args a{};
+    StepsOut dev[3] = {};
+    for (int i = 0; i < 3; ++i) {
+        eucalc_steps *o = outs[i];
+        if (!o) continue;
+        if (host_out) {
+            dev[i].off = (int64_t *)dalloc(sizeof(int64_t) * (S + 1));
+            dev[i].v = dalloc(esz * std::max<int64_t>(bnd, 1));
+            dev[i].h = (i == 2 && cls_alias) ? dev[0].h : dalloc(esz * std::max<int64_t>(bnd, 1));
+            if (!dev[i].off || !dev[i].v || !dev[i].h) {
+                free_scratch();
+                return fail(EUCALC_E_NOMEM, "device scratch for host outputs");
+            }
+        } else {
+            dev[i].off = o->offsets;
+            dev[i].h = (i == 2 && cls_alias) ? nullptr : o->height;
+            dev[i].v = o->value;
+        }
+    }
+    DirInfo *d_info = (DirInfo *)dalloc(sizeof(DirInfo) * D);
+    unsigned long long *flags = (unsigned long long *)dalloc(sizeof(unsigned long long) * S);
+    unsigned int *ticket = (unsigned int *)dalloc(sizeof(unsigned int));
+    if (!d_info || !flags || !ticket) {
+        free_scratch();
+        return fail(EUCALC_E_NOMEM, "scratch");
+    }
+    cudaError_t e = cudaMemcpyAsync(d_info, p.info.data(), sizeof(DirInfo) * D, cudaMemcpyHostToDevice, st);
+    if (e == cudaSuccess) e = cudaMemsetAsync(flags, 0, sizeof(unsigned long long) * S, st);
+    if (e == cudaSuccess) e = cudaMemsetAsync(ticket, 0, sizeof(unsigned int), st);
+    if (e == cudaSuccess) {
+        a.rec = cr->d_rec;
+        a.wide = cr->wide;
+        a.vcap = cr->vcap;
+        a.count = cr->d_count;
+        a.Q = cr->Q;
+        a.ndim = cx->ndim;
+        for (int k = 0; k < cx->ndim; ++k) {
+            a.sh[k] = cx->sh[k];
+            a.msk[k] = cx->msk[k];
+        }
+        a.dirs = d_info;
+        a.D = D;
+        a.batch = cx->batch;
+        a.R_max = p.R_max;
+        a.max_count = cr->max_count;
+        a.elem_bytes = eb;
+        a.do_ect = ect != nullptr;
+        a.do_ord = ordinary != nullptr;
+        a.do_cls = classical != nullptr;
+        a.cls_alias = cls_alias;
+        a.ect = dev[0];
+        a.ord = dev[1];
+        a.cls = dev[2];
+        a.flags = flags;
+        a.ticket = ticket;
+        ProfScope ps("k2_transforms", st);
+        e = launch_k2(a, st, num_sms());
+    }
+    if (e == cudaSuccess && host_out) {
+        // copy back: offsets first (to learn the exact totals), then the used entries
+        for (int i = 0; i < 3 && e == cudaSuccess; ++i) {
+            eucalc_steps *o = outs[i];
+            if (!o) continue;
+            e = cudaMemcpyAsync(o->offsets, dev[i].off, sizeof(int64_t) * (S + 1), cudaMemcpyDeviceToHost, st);
+        }
+        if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+        for (int i = 0; i < 3 && e == cudaSuccess; ++i) {
+            eucalc_steps *o = outs[i];
+            if (!o) continue;
+            const size_t nbytes = esz * (size_t)o->offsets[S];
+            if (nbytes == 0) continue;
+            e = cudaMemcpyAsync(o->value, dev[i].v, nbytes, cudaMemcpyDeviceToHost, st);
+            if (e == cudaSuccess && o->height && !(i == 2 && cls_alias))
+                e = cudaMemcpyAsync(o->height, dev[i].h, nbytes, cudaMemcpyDeviceToHost, st);
+        }
+    }
+    free_scratch();
+    if (e == cudaSuccess && host_out) e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) return cuda_fail(e, "transforms");
+    return EUCALC_OK;
+}
+
+eucalc_status eucalc_ect(const eucalc_critical *cr, const int32_t *dirs, int64_t D, eucalc_steps *ect,
+                         int64_t *required_out, void *stream) {
+    if (!ect) return fail(EUCALC_E_ARG, "ect is NULL");
+    return eucalc_transforms(cr, dirs, D, ect, nullptr, nullptr, required_out, stream);
+}
+
+eucalc_status eucalc_radon(const eucalc_critical *cr, const int32_t *dirs, int64_t D, eucalc_steps *ordinary,
+                           eucalc_steps *classical, int64_t *required_out, void *stream) {
+    if (!ordinary || !classical) return fail(EUCALC_E_ARG, "ordinary/classical is NULL");
+    if (!classical->height) return fail(EUCALC_E_ARG, "classical height is NULL");
+    return eucalc_transforms(cr, dirs, D, nullptr, ordinary, classical, required_out, stream);
+}
+
+eucalc_status eucalc_hybrid(const eucalc_critical *ccr, const int32_t *dirs, int64_t D, int kernel, double param,
+                            int precision, void *out, void *stream) {
+    if (!ccr) return fail(EUCALC_E_STATE, "NULL handle");
+    if (kernel < EUCALC_K_GAUSS || kernel > EUCALC_K_EXP) return fail(EUCALC_E_ARG, "bad kernel");
+    if (precision != EUCALC_F32 && precision != EUCALC_F64) return fail(EUCALC_E_ARG, "bad precision");
+    if ((kernel == EUCALC_K_GAUSS || kernel == EUCALC_K_COS) && !(param > 0)) return fail(EUCALC_E_ARG, "param must be > 0");
+    if (D > 0 && !out) return fail(EUCALC_E_ARG, "out is NULL");
+    eucalc_critical *cr = const_cast<eucalc_critical *>(ccr);
+    const Complex *cx = cr->cx;
+    cudaStream_t st = (cudaStream_t)stream;
+    DirPlan p;
+    eucalc_status s = plan_dirs(cx, dirs, D, st, p);
+    if (s != EUCALC_OK) return s;
+    s = sync_counts(cr, st);
+    if (s != EUCALC_OK) return s;
+    if (D == 0) return EUCALC_OK;
+    // group directions by orthant (Lemma 3) into tiles of <= 256
+    std::vector<int32_t> order(D);
+    std::iota(order.begin(), order.end(), 0);
+    std::stable_sort(order.begin(), order.end(), [&](int32_t x, int32_t y) { return p.orthant[x] < p.orthant[y]; });
+    std::vector<int32_t> tstart, tlen;
+    for (int64_t i = 0; i < D;) {
+        int64_t j = i;
+        while (j < D && p.orthant[order[j]] == p.orthant[order[i]] && j - i < 256) ++j;
+        tstart.push_back((int32_t)i);
+        tlen.push_back((int32_t)(j - i));
+        i = j;
+    }
+    const int chunk = k3_chunk();
+    const int nchunks = (int)std::max<int64_t>(1, (cr->max_count + chunk - 1) / chunk);
+    const size_t osz = precision == EUCALC_F32 ? 4 : 8;
+    const bool host_out = !is_device_ptr(out);
+    std::vector<void *> scratch;
+    auto dalloc = [&](size_t bytes) -> void * {
+        void *q = nullptr;
+        if (cudaMallocAsync(&q, bytes, st) != cudaSuccess) return nullptr;
+        scratch.push_back(q);
+        return q;
+    };
+    auto free_scratch = [&]() { for (void *q : scratch) cudaFreeAsync(q, st); };
+    DirInfo *d_info = (DirInfo *)dalloc(sizeof(DirInfo) * D);
+    int32_t *d_order = (int32_t *)dalloc(sizeof(int32_t) * D);
+    int32_t *d_ts = (int32_t *)dalloc(sizeof(int32_t) * tstart.size());
+    int32_t *d_tl = (int32_t *)dalloc(sizeof(int32_t) * tlen.size());
+    int32_t *d_cs = (int32_t *)dalloc(sizeof(int32_t) * D);
+    double *d_part = (double *)dalloc(sizeof(double) * cx->batch * nchunks * D);
+    void *d_out = host_out ? dalloc(osz * cx->batch * D) : out;
+    if (!d_info || !d_order || !d_ts || !d_tl || !d_cs || !d_part || !d_out) {
+        free_scratch();
+        return fail(EUCALC_E_NOMEM, "scratch");
+    }
+    cudaError_t e = cudaMemcpyAsync(d_info, p.info.data(), sizeof(DirInfo) * D, cudaMemcpyHostToDevice, st);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(d_order, order.data(), sizeof(int32_t) * D, cudaMemcpyHostToDevice, st);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(d_ts, tstart.data(), sizeof(int32_t) * tstart.size(), cudaMemcpyHostToDevice, st);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(d_tl, tlen.data(), sizeof(int32_t) * tlen.size(), cudaMemcpyHostToDevice, st);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(d_cs, p.csum.data(), sizeof(int32_t) * D, cudaMemcpyHostToDevice, st);
+    if (e == cudaSuccess) {
+        K3Args a{};
+        a.rec = cr->d_rec;
+        a.wide = cr->wide;
+        a.vcap = cr->vcap;
+        a.count = cr->d_count;
+        a.Q = cr->Q;
+        a.ndim = cx->ndim;
+        for (int k = 0; k < cx->ndim; ++k) {
+            a.sh[k] = cx->sh[k];
+            a.msk[k] = cx->msk[k];
+        }
+        a.dirs = d_info;
+        a.order = d_order;
+        a.tile_start = d_ts;
+        a.tile_len = d_tl;
+        a.ntiles = (int)tstart.size();
+        a.D = D;
+        a.batch = cx->batch;
+        a.kernel = kernel;
+        a.precision = precision;
+        a.param = param;
+        a.L = cx->L;
+        a.csum = d_cs;
+        a.nchunks = nchunks;
+        a.partial = d_part;
+        a.out = d_out;
+        ProfScope ps("k3_hybrid", st);
+        e = launch_k3(a, st);
+    }
+    if (e == cudaSuccess && host_out) e = cudaMemcpyAsync(out, d_out, osz * cx->batch * D, cudaMemcpyDeviceToHost, st);
+    free_scratch();
+    if (e == cudaSuccess && host_out) e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) return cuda_fail(e, "hybrid");
+    return EUCALC_OK;
+}
+
+eucalc_status eucalc_height_map(const eucalc_complex *cx, const int32_t *dir, int64_t *L, int64_t *csum) {
+    if (!cx || !dir) return fail(EUCALC_E_ARG, "NULL argument");
+    int64_t cs = 0;
+    for (int k = 0; k < cx->ndim; ++k)
+        if (cx->M[k] > 1) cs += dir[k];
+    if (L) *L = cx->L;
+    if (csum) *csum = cs;
+    return EUCALC_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,138 @@
+// Internal declarations shared by the eucalc CUDA translation units.
+// Product code only: nothing here is shared with oracle/ (test infrastructure).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+
+#include "../../include/eucalc.h"
+
+namespace eucalc {
+
+constexpr int kMaxN = 3;
+
+// One record of a critical list: packed vertex coordinates + Delta^- for the
+// pair's representative orthant (a) and for its antipode (b). SURVEY 8(a) A2.
+struct __align__(8) Rec16 {
+    uint32_t c;
+    int16_t a, b;
+};
+struct Rec32 {
+    uint32_t c;
+    int32_t a, b;
+};
+
+// ---- host-side handles -----------------------------------------------------
+struct Complex {
+    int ndim = 0, dtype = 0, construction = 0;
+    int64_t batch = 0;
+    int64_t m[kMaxN] = {1, 1, 1};  // image extents (pixels)
+    int64_t M[kMaxN] = {1, 1, 1};  // vertex extents
+    int64_t npix = 0, nvert = 0;   // per image
+    void *d_img = nullptr;         // device copy, batch * npix elements
+    int64_t max_abs_w = 0;
+    int sh[kMaxN] = {0, 0, 0};     // packed coordinate shifts
+    uint32_t msk[kMaxN] = {0, 0, 0};
+    int64_t L = 1;                 // lcm of (M_i - 1) > 0
+    int64_t scale[kMaxN] = {0, 0, 0};
+    cudaStream_t owner_stream = nullptr;
+};
+
+struct Critical {
+    const Complex *cx = nullptr;
+    int Q = 0;          // antipodal pairs = 2^(n-1)
+    bool wide = false;  // Rec32 instead of Rec16
+    int64_t vcap = 0;   // records capacity per (image, pair) list = nvert
+    void *d_rec = nullptr;       // [batch][Q][vcap]
+    int32_t *d_count = nullptr;  // [batch][Q]
+    int64_t *d_stats = nullptr;  // [batch][2^n][2] (N^-, N^ord) then [batch][Q] sum(|a|+|b|)
+    // host cache (filled by sync_counts)
+    bool have_host = false;
+    int64_t *h_count = nullptr;  // [batch][Q]
+    int64_t *h_stats = nullptr;
+    int64_t max_count = 0;
+    int64_t max_abs_sum = 0;
+};
+
+// ---- launchers (implemented in the .cu files) -------------------------------
+struct K1Args {
+    const void *img;
+    int dtype, construction, ndim;
+    int64_t batch, npix, vcap;
+    int m[kMaxN], M[kMaxN];
+    int TX, TY, tiles_x, tiles_y, tiles_z;
+    int sh[kMaxN];
+    void *rec;
+    bool wide;
+    int32_t *count;
+    unsigned long long *flags;
+    unsigned int *ticket;
+    int64_t *stats;
+    int64_t *abs_sum;
+};
+cudaError_t launch_k1(const K1Args &a, cudaStream_t s);
+
+// Per-direction info for K2/K3 (host-computed, copied to device).
+struct DirInfo {
+    int xs[kMaxN];  // axis-scaled direction xi_i * L/(M_i-1)
+    int hlo;        // lowest lattice height
+    int R;          // number of lattice heights
+    int q;          // antipodal pair of the orthant
+    int swap;       // 1 if the orthant is the pair's non-representative
+};
+
+struct StepsOut {
+    int64_t *off;
+    void *h;
+    void *v;
+};
+
+struct K2Args {
+    const void *rec;
+    bool wide;
+    int64_t vcap;
+    const int32_t *count;
+    int Q, ndim;
+    int sh[kMaxN];
+    uint32_t msk[kMaxN];
+    const DirInfo *dirs;
+    int64_t D, batch;
+    int R_max;
+    int64_t max_count;
+    int elem_bytes;
+    bool do_ect, do_ord, do_cls, cls_alias;
+    StepsOut ect, ord, cls;
+    unsigned long long *flags;  // [batch*D]
+    unsigned int *ticket;
+};
+cudaError_t launch_k2(const K2Args &a, cudaStream_t s, int num_sms);
+
+struct K3Args {
+    const void *rec;
+    bool wide;
+    int64_t vcap;
+    const int32_t *count;
+    int Q, ndim;
+    int sh[kMaxN];
+    uint32_t msk[kMaxN];
+    const DirInfo *dirs;       // per direction (original order)
+    const int32_t *order;      // sorted direction index list (grouped by orthant)
+    const int32_t *tile_start; // [ntiles] start into order; tile = same-orthant run of <= 256
+    const int32_t *tile_len;
+    int ntiles;
+    int64_t D, batch;
+    int kernel, precision;
+    double param;
+    int64_t L;
+    const int32_t *csum;       // [D] sum of xi_i over axes with M_i > 1
+    int nchunks;
+    double *partial;           // [batch][nchunks][D]
+    void *out;                 // [batch][D]
+};
+cudaError_t launch_k3(const K3Args &a, cudaStream_t s);
+
+// thread-local launch counter (eucalc_launch_count)
+void count_launch(int n = 1);
+
+}  // namespace eucalc

@@ -1,0 +1,371 @@
+// K1 — critical points (SURVEY 8(a) A1 stencil + A2 ordered compaction).
+//
+// For every vertex x of every image and every sign vector eps:
+//   Delta^-(eps, x) = chi(phi | lwst(eps, x))
+// where the lower star is the set of cells at doubled coordinates 2x - delta o eps,
+// delta in {0,1}^n, restricted to existing cells (E16). One CTA owns a
+// tile of vertices (full rows when they fit, so lists come out in row-major
+// vertex order); the image tile plus a one-vertex halo is staged in shared
+// memory as int32 with a sentinel for out-of-range positions:
+//   VERTEX: phi(cell) = min of its vertices; out-of-range vertex = INT_MIN,
+//                   so a cell touching it has phi = INT_MIN = "does not exist".
+//   TOP: phi(cell) = min over its top cofaces (pixels); out-of-range
+//                   pixel = INT_MAX, so a cell whose fixed pixel index is out of
+//                   range has phi = INT_MAX = "does not exist", while an in-range
+//                   face at the image border takes the min of its real cofaces.
+// Per vertex all 3^n star-cell values are formed in registers (separable mins),
+// masked to 0 where the cell does not exist, and the 2^n lower-star sums come
+// from an in-register inclusion-exclusion transform (38 adds in 3-D).
+//
+// Compaction: per antipodal pair {eps, -eps} (eps the representative with
+// eps_{n-1} = -1) a vertex is kept iff Delta^-(eps) != 0 or Delta^-(-eps) != 0
+// (this covers the classical points of both orthants and every ordinary point,
+// since J(eps) = Delta^-(eps) - Delta^-(-eps)). Warp ballot/popc + block scan
+// give the in-tile order; a decoupled look-back over the image's tiles (dynamic
+// ticket order) gives each tile's global offset, so the list order is
+// deterministic (tile-major, row-major within a tile) with a single pass.
+#include <climits>
+
+#include "eucalc_internal.cuh"
+
+namespace eucalc {
+namespace {
+
+constexpr int kThreads = 256;
+constexpr int kTileV = 2048;  // vertices per tile (max)
+
+__host__ __device__ constexpr int pow3(int k) { return k == 0 ? 1 : 3 * pow3(k - 1); }
+
+template <typename T>
+__device__ __forceinline__ int load_img(const T *p, int64_t i) { return (int)__ldg(p + i); }
+
+__device__ __forceinline__ unsigned long long ld_relaxed(const unsigned long long *p) {
+    unsigned long long v;
+    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_relaxed(unsigned long long *p, unsigned long long v) {
+    asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+// Flag word for the tile look-back: status in bits 62..63 (1 = aggregate,
+// 2 = inclusive prefix), count in the low 62 bits.
+constexpr unsigned long long kAgg = 1ull << 62, kIncl = 2ull << 62, kValMask = (1ull << 62) - 1;
+
+// Warp-wide decoupled look-back. Returns the exclusive prefix of tile `t`
+// (t >= 1) given flags for tiles [0, t) of this (image, pair); `stride` between
+// consecutive tiles' flag words.
+__device__ long long lookback(unsigned long long *flag_t, int t, int stride, long long agg) {
+    const int lane = threadIdx.x & 31;
+    if (lane == 0) st_relaxed(flag_t, kAgg | (unsigned long long)agg);
+    long long excl = 0;
+    int j = t - 1;
+    while (true) {
+        int idx = j - lane;
+        unsigned long long f = kIncl;  // virtual inclusive 0 before tile 0
+        if (idx >= 0) {
+            const unsigned long long *p = flag_t - (long long)(t - idx) * stride;
+            do { f = ld_relaxed(p); } while ((f >> 62) == 0);
+        }
+        unsigned incl = __ballot_sync(0xffffffffu, (f >> 62) == 2);
+        int first = incl ? __ffs(incl) - 1 : 31;
+        long long v = (lane <= first) ? (long long)(f & kValMask) : 0;
+        for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        excl += v;
+        if (incl) break;
+        j -= 32;
+    }
+    if (lane == 0) st_relaxed(flag_t, kIncl | (unsigned long long)(excl + agg));
+    return excl;
+}
+
+template <int N, int CONS>
+__device__ __forceinline__ void vertex_dminus(const int *s, int sz, int sy, int base, int (&dm)[1 << N]) {
+    constexpr int P3 = pow3(N);
+    int val[P3];
+    if (CONS == EUCALC_VERTEX) {
+        // point values of the 3^n neighbourhood, then separable box mins
+#pragma unroll
+        for (int idx = 0; idx < P3; ++idx) {
+            int off = 0, r = idx;
+#pragma unroll
+            for (int k = N - 1; k >= 0; --k) {
+                int o = r % 3 - 1;
+                r /= 3;
+                int stride = (k == N - 1) ? 1 : ((k == N - 2) ? sy : sz);
+                off += o * stride;
+            }
+            val[idx] = s[base + off];
+        }
+#pragma unroll
+        for (int k = 0; k < N; ++k) {
+            const int st = pow3(N - 1 - k);
+#pragma unroll
+            for (int idx = 0; idx < P3; ++idx) {
+                const int ok = (idx / st) % 3;
+                if (ok != 1) val[idx] = min(val[idx], val[idx + (1 - ok) * st]);
+            }
+        }
+#pragma unroll
+        for (int idx = 0; idx < P3; ++idx) val[idx] = (val[idx] == INT_MIN) ? 0 : val[idx];
+    } else {
+        // 2^n pixels around the vertex (pixel x + c, c in {-1,0}^n); base <-> c = 0
+        constexpr int P2 = 1 << N;
+        int pix[P2];
+#pragma unroll
+        for (int c = 0; c < P2; ++c) {
+            int off = 0;
+#pragma unroll
+            for (int k = 0; k < N; ++k) {
+                int stride = (k == N - 1) ? 1 : ((k == N - 2) ? sy : sz);
+                if (!((c >> k) & 1)) off -= stride;  // bit 0 -> c_k = -1
+            }
+            pix[c] = s[base + off];
+        }
+#pragma unroll
+        for (int idx = 0; idx < P3; ++idx) {
+            int mval = INT_MAX;
+#pragma unroll
+            for (int c = 0; c < P2; ++c) {
+                bool ok = true;
+#pragma unroll
+                for (int k = 0; k < N; ++k) {
+                    const int o = (idx / pow3(N - 1 - k)) % 3 - 1;
+                    const int cb = (c >> k) & 1;
+                    if (o == -1 && cb != 0) ok = false;  // cell extends to x-1: pixel x-1 only
+                    if (o == 1 && cb != 1) ok = false;   // cell extends to x+1: pixel x only
+                }
+                if (ok) mval = min(mval, pix[c]);
+            }
+            val[idx] = (mval == INT_MAX) ? 0 : mval;
+        }
+    }
+    // inclusion-exclusion: along axis k, slot +1 <- z(0) - z(-1) (eps_k=+1), slot -1 <- z(0) - z(+1)
+#pragma unroll
+    for (int k = 0; k < N; ++k) {
+        const int st = pow3(N - 1 - k);
+#pragma unroll
+        for (int idx = 0; idx < P3; ++idx) {
+            if ((idx / st) % 3 == 1) {
+                const int a = val[idx - st], c = val[idx], b = val[idx + st];
+                val[idx + st] = c - a;
+                val[idx - st] = c - b;
+            }
+        }
+    }
+#pragma unroll
+    for (int e = 0; e < (1 << N); ++e) {
+        int idx = 0;
+#pragma unroll
+        for (int k = 0; k < N; ++k) idx += (((e >> k) & 1) ? 2 : 0) * pow3(N - 1 - k);
+        dm[e] = val[idx];
+    }
+}
+
+template <int N, int CONS, typename TIn, typename RecT>
+__global__ void __launch_bounds__(kThreads) k1_kernel(K1Args a) {
+    constexpr int Q = 1 << (N - 1);
+    constexpr int FULL = (1 << N) - 1;
+    extern __shared__ __align__(16) unsigned char smem[];
+    RecT *stage = reinterpret_cast<RecT *>(smem);                 // [Q][kTileV]
+    int *reg = reinterpret_cast<int *>(stage + Q * kTileV);        // input region
+    __shared__ int s_warp[kThreads / 32][Q];
+    __shared__ int s_run[Q];
+    __shared__ long long s_excl[Q];
+    __shared__ unsigned s_ticket;
+    __shared__ int s_ostat[1 << N][2];
+
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    if (tid == 0) s_ticket = atomicAdd(a.ticket, 1u);
+    if (tid < Q) s_run[tid] = 0;
+    if (tid < (1 << N) * 2) (&s_ostat[0][0])[tid] = 0;
+    __syncthreads();
+    const unsigned ticket = s_ticket;
+    const int tiles_per_img = a.tiles_x * a.tiles_y * a.tiles_z;
+    const int64_t b = ticket / tiles_per_img;
+    const int t = ticket % tiles_per_img;
+    const int tx = t % a.tiles_x, ty = (t / a.tiles_x) % a.tiles_y, tz = t / (a.tiles_x * a.tiles_y);
+
+    // vertex-lattice extents along (z, y, x) view
+    const int MX = a.M[N - 1];
+    const int MY = (N >= 2) ? a.M[N - 2] : 1;
+    const int mX = a.m[N - 1];
+    const int mY = (N >= 2) ? a.m[N - 2] : 1;
+    const int mZ = (N == 3) ? a.m[0] : 1;
+    const int x0 = tx * a.TX, y0 = ty * a.TY, z = tz;
+    const int TXe = min(a.TX, MX - x0), TYe = min(a.TY, MY - y0);
+    const int RX = TXe + 2, RY = TYe + 2;
+    const int planes = (N == 3) ? 3 : 1;
+
+    // ---- stage input region rows y0-1 .. y0+TYe, cols x0-1 .. x0+TXe (image index = vertex idx for
+    // VERTEX, pixel idx for TOP), planes z-1..z+1
+    const TIn *img = reinterpret_cast<const TIn *>(a.img) + b * a.npix;
+    const int SENT = (CONS == EUCALC_VERTEX) ? INT_MIN : INT_MAX;
+    const int nreg = planes * RY * RX;
+    for (int i = tid; i < nreg; i += kThreads) {
+        int rx = i % RX, ry = (i / RX) % RY, pz = i / (RX * RY);
+        int gx = x0 - 1 + rx, gy = y0 - 1 + ry, gz = z - 1 + pz;
+        if (N == 2) gz = 0;
+        bool in = gx >= 0 && gx < mX && gy >= 0 && gy < mY && gz >= 0 && gz < mZ;
+        int64_t gi = ((int64_t)gz * mY + gy) * mX + gx;
+        reg[i] = in ? load_img(img, gi) : SENT;
+    }
+    __syncthreads();
+
+    // ---- per vertex stencil + compaction into shared staging
+    const int sy = RX, sz = RX * RY;
+    const int TV = TXe * TYe;
+    int cnt_o[1 << N][2];
+#pragma unroll
+    for (int e = 0; e < (1 << N); ++e) cnt_o[e][0] = cnt_o[e][1] = 0;
+    long long abs_sum[Q];
+#pragma unroll
+    for (int q = 0; q < Q; ++q) abs_sum[q] = 0;
+
+    for (int c0 = 0; c0 < TV; c0 += kThreads) {
+        const int li = c0 + tid;
+        const bool valid = li < TV;
+        int dm[1 << N];
+        int ly = 0, lx = 0;
+        if (valid) {
+            ly = li / TXe;
+            lx = li - ly * TXe;
+            const int base = ((N == 3) ? sz : 0) + (ly + 1) * sy + (lx + 1);
+            vertex_dminus<N, CONS>(reg, sz, sy, base, dm);
+        } else {
+#pragma unroll
+            for (int e = 0; e < (1 << N); ++e) dm[e] = 0;
+        }
+#pragma unroll
+        for (int e = 0; e < (1 << N); ++e) {
+            cnt_o[e][0] += dm[e] != 0;
+            cnt_o[e][1] += dm[e] != dm[e ^ FULL];
+        }
+        uint32_t coord = 0;
+        if (valid) {
+            const int gx = x0 + lx, gy = y0 + ly;
+            coord = ((uint32_t)gx << a.sh[N - 1]);
+            if (N >= 2) coord |= ((uint32_t)gy << a.sh[N - 2]);
+            if (N == 3) coord |= ((uint32_t)z << a.sh[0]);
+        }
+        bool keep[Q];
+        unsigned bal[Q];
+#pragma unroll
+        for (int q = 0; q < Q; ++q) {
+            keep[q] = dm[q] != 0 || dm[q ^ FULL] != 0;
+            bal[q] = __ballot_sync(0xffffffffu, keep[q]);
+            if (lane == 0) s_warp[warp][q] = __popc(bal[q]);
+            abs_sum[q] += abs(dm[q]) + abs(dm[q ^ FULL]);
+        }
+        __syncthreads();
+#pragma unroll
+        for (int q = 0; q < Q; ++q) {
+            if (keep[q]) {
+                int pos = s_run[q] + __popc(bal[q] & ((1u << lane) - 1));
+                for (int w = 0; w < warp; ++w) pos += s_warp[w][q];
+                RecT r;
+                r.c = coord;
+                r.a = dm[q];
+                r.b = dm[q ^ FULL];
+                stage[q * kTileV + pos] = r;
+            }
+        }
+        __syncthreads();
+        if (tid < Q) {
+            int tot = 0;
+            for (int w = 0; w < kThreads / 32; ++w) tot += s_warp[w][tid];
+            s_run[tid] += tot;
+        }
+        __syncthreads();
+    }
+
+    // ---- per-image statistics (order-independent integer sums: deterministic)
+#pragma unroll
+    for (int e = 0; e < (1 << N); ++e) {
+        int c = cnt_o[e][0], o = cnt_o[e][1];
+        for (int d = 16; d; d >>= 1) {
+            c += __shfl_xor_sync(0xffffffffu, c, d);
+            o += __shfl_xor_sync(0xffffffffu, o, d);
+        }
+        if (lane == 0) {
+            atomicAdd(&s_ostat[e][0], c);
+            atomicAdd(&s_ostat[e][1], o);
+        }
+    }
+#pragma unroll
+    for (int q = 0; q < Q; ++q) {
+        long long v = abs_sum[q];
+        for (int d = 16; d; d >>= 1) v += __shfl_xor_sync(0xffffffffu, v, d);
+        if (lane == 0 && v) atomicAdd((unsigned long long *)&a.abs_sum[b * Q + q], (unsigned long long)v);
+    }
+    __syncthreads();
+    if (tid < (1 << N) * 2) {
+        int v = (&s_ostat[0][0])[tid];
+        if (v) atomicAdd((unsigned long long *)&a.stats[b * (1 << N) * 2 + tid], (unsigned long long)v);
+    }
+
+    // ---- look-back per pair (warp q), then ordered copy-out
+    if (warp < Q) {
+        const int q = warp;
+        const long long agg = s_run[q];
+        unsigned long long *flag_t = a.flags + ((int64_t)b * tiles_per_img + t) * Q + q;
+        long long excl;
+        if (t == 0) {
+            if (lane == 0) st_relaxed(flag_t, kIncl | (unsigned long long)agg);
+            excl = 0;
+        } else {
+            excl = lookback(flag_t, t, Q, agg);
+        }
+        if (lane == 0) {
+            s_excl[q] = excl;
+            if (t == tiles_per_img - 1) a.count[b * Q + q] = (int32_t)(excl + agg);
+        }
+    }
+    __syncthreads();
+    RecT *out = reinterpret_cast<RecT *>(a.rec);
+#pragma unroll
+    for (int q = 0; q < Q; ++q) {
+        RecT *dst = out + (b * Q + q) * a.vcap + s_excl[q];
+        const RecT *src = stage + q * kTileV;
+        for (int i = tid; i < s_run[q]; i += kThreads) dst[i] = src[i];
+    }
+}
+
+template <int N, int CONS, typename TIn, typename RecT>
+cudaError_t launch_t(const K1Args &a, cudaStream_t s) {
+    constexpr int Q = 1 << (N - 1);
+    const int planes = (N == 3) ? 3 : 1;
+    size_t smem = sizeof(RecT) * Q * kTileV + sizeof(int) * planes * (a.TY + 2) * (a.TX + 2);
+    auto kern = k1_kernel<N, CONS, TIn, RecT>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    int64_t nblocks = a.batch * (int64_t)a.tiles_x * a.tiles_y * a.tiles_z;
+    kern<<<(unsigned)nblocks, kThreads, smem, s>>>(a);
+    count_launch();
+    return cudaGetLastError();
+}
+
+template <int N, int CONS, typename TIn>
+cudaError_t launch_r(const K1Args &a, cudaStream_t s) {
+    return a.wide ? launch_t<N, CONS, TIn, Rec32>(a, s) : launch_t<N, CONS, TIn, Rec16>(a, s);
+}
+template <int N, int CONS>
+cudaError_t launch_d(const K1Args &a, cudaStream_t s) {
+    switch (a.dtype) {
+    case EUCALC_U8: return launch_r<N, CONS, uint8_t>(a, s);
+    case EUCALC_I16: return launch_r<N, CONS, int16_t>(a, s);
+    default: return launch_r<N, CONS, int32_t>(a, s);
+    }
+}
+
+}  // namespace
+
+cudaError_t launch_k1(const K1Args &a, cudaStream_t s) {
+    if (a.ndim == 2)
+        return a.construction == EUCALC_VERTEX ? launch_d<2, EUCALC_VERTEX>(a, s) : launch_d<2, EUCALC_TOP>(a, s);
+    return a.construction == EUCALC_VERTEX ? launch_d<3, EUCALC_VERTEX>(a, s) : launch_d<3, EUCALC_TOP>(a, s);
+}
+
+int k1_tile_vertices() { return kTileV; }
+
+}  // namespace eucalc

@@ -1,0 +1,247 @@
+// K3 — hybrid transform.
+//
+// HT(xi) = int kappa(t) Radon(xi,t) dt = - sum_{ordinary x} J(eps,x) kbar(t(x))
+// (Lemma 2, ordinary sign corrected E1; "we sum, over all
+// ordinary critical points, the evaluation of the kernel kbar on the dot
+// products"), t(x) the paper's normalised height:
+//   t = (2H - L*csum) / (2L),  H = sum_i xs_i p_i an exact integer (E10, E11).
+// The additive constant of kbar cancels because sum J = 0.
+//
+// Work decomposition: directions are grouped by orthant on the host (Lemma 3,
+// same sign vector -> same critical list) into tiles of <= 256; a CTA
+// owns (image, tile, chunk of kChunk records) with one direction per thread in
+// registers and the chunk staged in shared memory (broadcast reads). Per term:
+// 3 FMA for the height, 1 FMA for the kernel argument, kbar (erf / sinpi /
+// cos / exp on the FMA + MUFU pipes), 1 FMUL and a compensated (Kahan) fp32
+// add — or the same in fp64. Chunk partials are combined in a fixed order by
+// a second kernel, so results are bit-identical run to run.
+#include <cmath>
+
+#include "eucalc_internal.cuh"
+
+namespace eucalc {
+namespace {
+
+constexpr int kThreads = 256;
+constexpr int kChunk = 4096;
+constexpr int kStage = 1024;
+
+template <typename RecT>
+__device__ __forceinline__ void rec_coords(const RecT &r, const K3Args &a, int &p0, int &p1, int &p2) {
+    p0 = (int)((r.c >> a.sh[0]) & a.msk[0]);
+    p1 = (int)((r.c >> a.sh[1]) & a.msk[1]);
+    p2 = (a.ndim == 3) ? (int)((r.c >> a.sh[2]) & a.msk[2]) : 0;
+}
+
+struct Kahan32 {
+    float s = 0.f, c = 0.f;
+    __device__ __forceinline__ void add(float x) {
+        float y = x - c;
+        float t = s + y;
+        c = (t - s) - y;
+        s = t;
+    }
+};
+
+template <typename RecT>
+__global__ void __launch_bounds__(kThreads) k3_f32(K3Args a) {
+    __shared__ float4 sm[kStage];
+    const int c = blockIdx.x, tile = blockIdx.y;
+    const long long b = blockIdx.z;
+    const int tlen = a.tile_len[tile];
+    const int myd = threadIdx.x < tlen ? a.order[a.tile_start[tile] + threadIdx.x]
+                                       : a.order[a.tile_start[tile]];
+    const DirInfo di = a.dirs[myd];
+    const int d0 = a.order[a.tile_start[tile]];
+    const DirInfo di0 = a.dirs[d0];  // orthant shared by the tile
+    const int n = a.count[b * a.Q + di0.q];
+    const RecT *list = reinterpret_cast<const RecT *>(a.rec) + (b * a.Q + di0.q) * a.vcap;
+    const int beg = c * kChunk, end = min(n, beg + kChunk);
+    // per-direction constants
+    const float x0 = (float)di.xs[0], x1 = (float)di.xs[1], x2 = (a.ndim == 3) ? (float)di.xs[2] : 0.f;
+    const double L = (double)a.L;
+    const double cs = (double)a.csum[myd];
+    float c1 = 0.f, c0 = 0.f;
+    float per = 0.f, inv_per = 0.f, inv_half = 0.f;
+    bool int_period = false;
+    if (a.kernel == EUCALC_K_GAUSS) {
+        const double k = 1.0 / (a.param * sqrt(2.0));
+        c1 = (float)(k / L);
+        c0 = (float)(-0.5 * cs * k);
+    } else if (a.kernel == EUCALC_K_COS) {
+        // sin(2 pi t / P) = sinpi(u / (L P)), u = 2H - L csum; period of u is 2LP
+        const double lp = L * a.param;
+        int_period = (a.param == rint(a.param)) && lp < 4.0e6;
+        per = (float)(2.0 * lp);
+        inv_per = (float)(1.0 / (2.0 * lp));
+        inv_half = (float)(1.0 / lp);
+        c0 = (float)(-L * cs);  // u = 2h + c0 (exact integer in fp32)
+        c1 = (float)(2.0 * M_PI / a.param / (2.0 * L));  // fallback: angle = u * c1
+    } else {
+        c1 = (float)(1.0 / L);
+        c0 = (float)(-0.5 * cs);
+    }
+    Kahan32 acc0, acc1;
+    const int sw = di.swap;
+    for (int s0 = beg; s0 < end; s0 += kStage) {
+        const int cnt = min(kStage, end - s0);
+        __syncthreads();
+        for (int i = threadIdx.x; i < cnt; i += kThreads) {
+            const RecT r = list[s0 + i];
+            int p0, p1, p2;
+            rec_coords(r, a, p0, p1, p2);
+            const int j = sw ? (r.b - r.a) : (r.a - r.b);
+            sm[i] = make_float4((float)p0, (float)p1, (float)p2, (float)j);
+        }
+        __syncthreads();
+        if (threadIdx.x < tlen) {
+#pragma unroll 2
+            for (int i = 0; i < cnt; ++i) {
+                const float4 r = sm[i];
+                const float h = fmaf(r.x, x0, fmaf(r.y, x1, r.z * x2));  // exact integer
+                float kb;
+                if (a.kernel == EUCALC_K_GAUSS) {
+                    kb = erff(fmaf(h, c1, c0));
+                } else if (a.kernel == EUCALC_K_COS) {
+                    const float u = fmaf(2.f, h, c0);
+                    if (int_period) {
+                        const float q = rintf(u * inv_per);
+                        const float rr = fmaf(-q, per, u);  // exact: integers < 2^24
+                        kb = sinpif(rr * inv_half);
+                    } else {
+                        kb = sinf(u * c1);
+                    }
+                } else if (a.kernel == EUCALC_K_SIN) {
+                    kb = cosf(fmaf(h, c1, c0));
+                } else {
+                    kb = expf(fmaf(h, c1, c0));
+                }
+                if (i & 1) acc1.add(r.w * kb);
+                else acc0.add(r.w * kb);
+            }
+        }
+    }
+    if (threadIdx.x < tlen) {
+        const double tot = ((double)acc0.s - (double)acc0.c) + ((double)acc1.s - (double)acc1.c);
+        a.partial[(b * a.nchunks + c) * a.D + myd] = tot;
+    }
+}
+
+template <typename RecT>
+__global__ void __launch_bounds__(kThreads) k3_f64(K3Args a) {
+    __shared__ int4 sm[kStage];
+    const int c = blockIdx.x, tile = blockIdx.y;
+    const long long b = blockIdx.z;
+    const int tlen = a.tile_len[tile];
+    const int myd = threadIdx.x < tlen ? a.order[a.tile_start[tile] + threadIdx.x]
+                                       : a.order[a.tile_start[tile]];
+    const DirInfo di = a.dirs[myd];
+    const DirInfo di0 = a.dirs[a.order[a.tile_start[tile]]];
+    const int n = a.count[b * a.Q + di0.q];
+    const RecT *list = reinterpret_cast<const RecT *>(a.rec) + (b * a.Q + di0.q) * a.vcap;
+    const int beg = c * kChunk, end = min(n, beg + kChunk);
+    const int x0 = di.xs[0], x1 = di.xs[1], x2 = (a.ndim == 3) ? di.xs[2] : 0;
+    const double L = (double)a.L;
+    const double cs = (double)a.csum[myd];
+    double c1 = 0, c0 = 0, per = 0, inv_per = 0, inv_half = 0;
+    bool int_period = false;
+    if (a.kernel == EUCALC_K_GAUSS) {
+        const double k = 1.0 / (a.param * sqrt(2.0));
+        c1 = k / L;
+        c0 = -0.5 * cs * k;
+    } else if (a.kernel == EUCALC_K_COS) {
+        const double lp = L * a.param;
+        int_period = (a.param == rint(a.param)) && lp < 1.0e15;
+        per = 2.0 * lp;
+        inv_per = 1.0 / per;
+        inv_half = 1.0 / lp;
+        c0 = -L * cs;
+        c1 = 2.0 * M_PI / a.param / (2.0 * L);
+    } else {
+        c1 = 1.0 / L;
+        c0 = -0.5 * cs;
+    }
+    double acc0 = 0.0, acc1 = 0.0;
+    const int sw = di.swap;
+    for (int s0 = beg; s0 < end; s0 += kStage) {
+        const int cnt = min(kStage, end - s0);
+        __syncthreads();
+        for (int i = threadIdx.x; i < cnt; i += kThreads) {
+            const RecT r = list[s0 + i];
+            int p0, p1, p2;
+            rec_coords(r, a, p0, p1, p2);
+            sm[i] = make_int4(p0, p1, p2, sw ? (r.b - r.a) : (r.a - r.b));
+        }
+        __syncthreads();
+        if (threadIdx.x < tlen) {
+#pragma unroll 2
+            for (int i = 0; i < cnt; ++i) {
+                const int4 r = sm[i];
+                const double h = (double)(r.x * x0 + r.y * x1 + r.z * x2);  // exact integer
+                double kb;
+                if (a.kernel == EUCALC_K_GAUSS) {
+                    kb = erf(fma(h, c1, c0));
+                } else if (a.kernel == EUCALC_K_COS) {
+                    const double u = fma(2.0, h, c0);
+                    if (int_period) {
+                        const double q = rint(u * inv_per);
+                        kb = sinpi(fma(-q, per, u) * inv_half);
+                    } else {
+                        kb = sin(u * c1);
+                    }
+                } else if (a.kernel == EUCALC_K_SIN) {
+                    kb = cos(fma(h, c1, c0));
+                } else {
+                    kb = exp(fma(h, c1, c0));
+                }
+                if (i & 1) acc1 = fma((double)r.w, kb, acc1);
+                else acc0 = fma((double)r.w, kb, acc0);
+            }
+        }
+    }
+    if (threadIdx.x < tlen) a.partial[(b * a.nchunks + c) * a.D + myd] = acc0 + acc1;
+}
+
+// Fixed-order combine of the chunk partials; applies -scale of kbar.
+__global__ void k3_combine(const K3Args a, double scale) {
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= a.batch * a.D) return;
+    const long long b = i / a.D, d = i % a.D;
+    double s = 0.0;
+    for (int c = 0; c < a.nchunks; ++c) s += a.partial[(b * a.nchunks + c) * a.D + d];
+    const double v = scale * s;
+    if (a.precision == EUCALC_F32) reinterpret_cast<float *>(a.out)[i] = (float)v;
+    else reinterpret_cast<double *>(a.out)[i] = v;
+}
+
+}  // namespace
+
+int k3_chunk() { return kChunk; }
+
+cudaError_t launch_k3(const K3Args &a, cudaStream_t s) {
+    dim3 grid((unsigned)a.nchunks, (unsigned)a.ntiles, (unsigned)a.batch);
+    if (a.precision == EUCALC_F32) {
+        if (a.wide) k3_f32<Rec32><<<grid, kThreads, 0, s>>>(a);
+        else k3_f32<Rec16><<<grid, kThreads, 0, s>>>(a);
+    } else {
+        if (a.wide) k3_f64<Rec32><<<grid, kThreads, 0, s>>>(a);
+        else k3_f64<Rec16><<<grid, kThreads, 0, s>>>(a);
+    }
+    count_launch();
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    // HT = -sum J kbar; kbar = scale_k * f
+    double scale;
+    switch (a.kernel) {
+    case EUCALC_K_GAUSS: scale = -a.param * sqrt(M_PI / 2.0); break;
+    case EUCALC_K_COS: scale = -a.param / (2.0 * M_PI); break;
+    case EUCALC_K_SIN: scale = 1.0; break;  // kbar = -cos
+    default: scale = -1.0; break;           // kbar = exp
+    }
+    const long long tot = a.batch * a.D;
+    k3_combine<<<(unsigned)((tot + 255) / 256), 256, 0, s>>>(a, scale);
+    count_launch();
+    return cudaGetLastError();
+}
+
+}  // namespace eucalc

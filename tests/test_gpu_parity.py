@@ -1,0 +1,307 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle.
+
+ECT/Radon representations and critical tables must be bit-exact (integers,
+SURVEY 8(c) E18); HT within 1e-9 (fp64) / 1e-4 (fp32) relative to max(|ref|,1)
+(BASELINE.json north_star). Inputs are the seeded generators of synth/.
+"""
+import math
+
+import numpy as np
+import pytest
+
+import oracle
+import synth
+from tests.helpers import orthant
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("needs a GPU", allow_module_level=True)
+
+import paper_2405_02256_b200 as eu  # noqa: E402
+
+HT_TOL = {"f64": 1e-9, "f32": 1e-4}
+
+
+def to_np(steps):
+    if steps is None:
+        return None
+    return {k: (v.cpu().numpy().astype(np.int64) if v is not None else None) for k, v in steps.items()}
+
+
+def seg(st, s):
+    a, b = st["offsets"][s], st["offsets"][s + 1]
+    return st["height"][a:b], st["value"][a:b]
+
+
+def run_gpu(images, dirs, construction, elem_bytes=8, share=False):
+    cx = eu.build_complex(np.ascontiguousarray(images), construction)
+    cr = eu.critical_points(cx)
+    r = eu.transforms(cr, dirs, elem_bytes=elem_bytes, share_heights=share)
+    torch.cuda.synchronize()
+    return cx, cr, {k: to_np(v) for k, v in r.items()}
+
+
+def check_transforms(images, dirs, construction, res, pairs=None):
+    D = len(dirs)
+    ref = oracle.transforms_batch(images, dirs, construction, pairs=pairs)
+    for (b, d), want in ref.items():
+        s = b * D + d
+        T, E = seg(res["ect"], s)
+        np.testing.assert_array_equal(T, want["T"], err_msg=f"ECT T b={b} d={d}")
+        np.testing.assert_array_equal(E, want["E"], err_msg=f"ECT E b={b} d={d}")
+        To, Eo = seg(res["ordinary"], s)
+        np.testing.assert_array_equal(To, want["To"], err_msg=f"Radon T_o b={b} d={d}")
+        np.testing.assert_array_equal(Eo, want["Eo"], err_msg=f"Radon E' b={b} d={d}")
+        Tc, Ec = seg(res["classical"], s)
+        np.testing.assert_array_equal(Tc, want["Tc"], err_msg=f"Radon T_c b={b} d={d}")
+        np.testing.assert_array_equal(Ec, want["Ec"], err_msg=f"Radon E_c b={b} d={d}")
+
+
+def check_critical(images, construction, cr, imgs_to_check=None):
+    n = images.ndim - 1
+    for b in (imgs_to_check if imgs_to_check is not None else range(images.shape[0])):
+        g = oracle.Grid(images[b], construction)
+        for e in range(1 << n):
+            v, dm, j = cr.export(b, e)
+            odm, oep = g.critical(e)
+            oj = odm - oep
+            keep = np.nonzero((odm != 0) | (oep != 0))[0]
+            np.testing.assert_array_equal(v, keep, err_msg=f"kept vertices b={b} e={e}")
+            np.testing.assert_array_equal(dm, odm[keep], err_msg=f"Delta^- b={b} e={e}")
+            np.testing.assert_array_equal(j, oj[keep], err_msg=f"J b={b} e={e}")
+
+
+def check_ht(images, dirs, construction, cr, kernel, param, precision, pairs=None):
+    out = eu.hybrid(cr, dirs, kernel, param, precision).cpu().numpy()
+    ref = oracle.ht_batch(images, dirs, construction, kernel, param, pairs=pairs)
+    tol = HT_TOL[precision]
+    for (b, d), want in ref.items():
+        got = float(out[b, d])
+        assert abs(got - want) <= tol * max(abs(want), 1.0), (kernel, precision, b, d, got, want)
+
+
+# ----------------------------------------------------------------------------- golden
+
+def test_ex4_golden_gpu():
+    img = synth.EX4[None].astype(np.uint8)
+    cx, cr, res = run_gpu(img, np.array([[2, 2]], np.int32), "vertex")
+    T, E = seg(res["ect"], 0)
+    assert E.tolist() == [1, 3, 2] and T.tolist() == [0, 4, 6]
+    To, Eo = seg(res["ordinary"], 0)
+    assert Eo.tolist() == [2, 1, 0] and To.tolist() == [4, 8, 10]
+    Tc, Ec = seg(res["classical"], 0)
+    assert Ec.tolist() == [1, 2, 1]
+    ht = eu.hybrid(cr, np.array([[2, 2]], np.int32), "exp", 1.0, "f64").item()
+    assert abs(ht - (math.exp(2 / 3) + math.exp(4 / 3) - 2 * math.exp(-2 / 3))) < 1e-12
+    check_critical(img, "vertex", cr)
+    assert cx.height_map([2, 2]) == (3, 4)
+
+
+# ----------------------------------------------------------------------------- random small, both regimes
+
+CASES = [
+    # (shape, batch, construction, levels, dir range, ndirs)
+    ((9, 13), 5, "vertex", 256, 8, 17),
+    ((9, 13), 5, "top", 256, 8, 17),
+    ((70, 100), 2, "vertex", 4, 6, 9),       # 4 K1 tiles, ragged last
+    ((70, 100), 2, "top", 7, 6, 9),
+    ((3, 2100), 1, "vertex", 256, 3, 5),     # x-split tiles
+    ((6, 7, 5), 4, "vertex", 256, 5, 11),
+    ((6, 7, 5), 4, "top", 3, 5, 11),
+    ((10, 12, 50), 1, "vertex", 256, 4, 7),  # 10 planes -> 10 tiles
+    ((1, 9), 3, "vertex", 5, 4, 6),          # degenerate axis
+    ((1, 1), 2, "top", 5, 4, 3),
+    ((1, 5, 1), 2, "top", 9, 3, 4),
+]
+
+
+@pytest.mark.parametrize("case", CASES, ids=lambda c: f"{c[0]}x{c[1]}-{c[2]}")
+def test_random_parity(case):
+    shape, batch, construction, levels, k, nd = case
+    rng = np.random.default_rng(hash(case) & 0xFFFF)
+    images = rng.integers(0, levels, size=(batch, *shape)).astype(np.uint8)
+    dirs = synth.random_directions(nd, len(shape), k, 99)
+    cx, cr, res = run_gpu(images, dirs, construction)
+    check_critical(images, construction, cr)
+    check_transforms(images, dirs, construction, res)
+    check_ht(images, dirs, construction, cr, "gauss", 1.0, "f64")
+    check_ht(images, dirs, construction, cr, "cos", 64.0, "f32")
+
+
+def test_block_regime_multiwindow():
+    """Large height range -> one CTA per segment, several 26624-bin windows."""
+    img = synth.grf_image(160, 5)[None]
+    dirs = np.concatenate([synth.random_directions(6, 2, 90, 5), np.array([[90, -89], [-90, 90]], np.int32)])
+    cx, cr, res = run_gpu(img, dirs, "vertex")
+    check_transforms(img, dirs, "vertex", res)
+
+
+def test_negative_and_int32_weights():
+    rng = np.random.default_rng(3)
+    images = rng.integers(-40000, 40000, size=(2, 12, 11)).astype(np.int32)
+    dirs = synth.random_directions(5, 2, 5, 8)
+    for construction in ("vertex", "top"):
+        cx, cr, res = run_gpu(images, dirs, construction)
+        check_critical(images, construction, cr)
+        check_transforms(images, dirs, construction, res)
+        check_ht(images, dirs, construction, cr, "sin", 1.0, "f64")
+
+
+@pytest.mark.parametrize("precision", ["f32", "f64"])
+@pytest.mark.parametrize("kernel,param", [("gauss", 1.0), ("cos", 64.0), ("sin", 1.0), ("exp", 1.0), ("cos", 7.5)])
+def test_ht_kernels(kernel, param, precision):
+    vols = np.stack([synth.smooth_volume(12, 1500 + j) for j in range(2)])
+    dirs, _ = synth.fibonacci_directions(40, 8.0)
+    cx = eu.build_complex(vols, "vertex")
+    cr = eu.critical_points(cx)
+    check_ht(vols, dirs, "vertex", cr, kernel, param, precision)
+
+
+# ----------------------------------------------------------------------------- ABI behaviour
+
+def test_output_widths_and_shared_heights():
+    images = synth.blob_images(6, 28, 1)
+    dirs = synth.random_directions(20, 2, 16, 3)
+    _, _, r8 = run_gpu(images, dirs, "vertex", elem_bytes=8)
+    _, _, r4 = run_gpu(images, dirs, "vertex", elem_bytes=4, share=True)
+    for k in ("ect", "ordinary", "classical"):
+        S = images.shape[0] * len(dirs)
+        np.testing.assert_array_equal(r8[k]["offsets"], r4[k]["offsets"])
+        n = r8[k]["offsets"][S]
+        np.testing.assert_array_equal(r8[k]["height"][:n], r4[k]["height"][:n])
+        np.testing.assert_array_equal(r8[k]["value"][:n], r4[k]["value"][:n])
+
+
+def test_host_buffers_match_device():
+    images = synth.blob_images(8, 28, 2)
+    dirs = synth.random_directions(16, 2, 16, 4)
+    cx = eu.build_complex(images, "vertex")
+    cr = eu.critical_points(cx)
+    dev = {k: to_np(v) for k, v in eu.transforms(cr, dirs, device="cuda").items()}
+    host = {k: to_np(v) for k, v in eu.transforms(cr, dirs, device="cpu").items()}
+    S = images.shape[0] * len(dirs)
+    for k in dev:
+        n = dev[k]["offsets"][S]
+        np.testing.assert_array_equal(dev[k]["offsets"], host[k]["offsets"])
+        np.testing.assert_array_equal(dev[k]["value"][:n], host[k]["value"][:n])
+        np.testing.assert_array_equal(dev[k]["height"][:n], host[k]["height"][:n])
+    hd = eu.hybrid(cr, dirs, "gauss", 1.0, "f64", device="cuda").cpu().numpy()
+    hh = eu.hybrid(cr, dirs, "gauss", 1.0, "f64", device="cpu").numpy()
+    np.testing.assert_array_equal(hd, hh)
+
+
+def test_determinism():
+    vols = np.stack([synth.smooth_volume(20, 7 + j) for j in range(2)])
+    dirs, _ = synth.fibonacci_directions(64, 8.0)
+    outs = []
+    for _ in range(2):
+        cx = eu.build_complex(vols, "vertex")
+        cr = eu.critical_points(cx)
+        r = {k: to_np(v) for k, v in eu.transforms(cr, dirs).items()}
+        h = eu.hybrid(cr, dirs, "cos", 64.0, "f32").cpu().numpy()
+        outs.append((r, h))
+    (r1, h1), (r2, h2) = outs
+    for k in r1:
+        for kk in ("offsets", "height", "value"):
+            n = r1[k]["offsets"][-1]
+            np.testing.assert_array_equal(r1[k][kk][:n] if kk != "offsets" else r1[k][kk],
+                                          r2[k][kk][:n] if kk != "offsets" else r2[k][kk])
+    assert h1.tobytes() == h2.tobytes()
+
+
+def test_errors():
+    images = synth.blob_images(2, 28, 3)
+    cx = eu.build_complex(images, "vertex")
+    cr = eu.critical_points(cx)
+    bad = np.array([[1, 2], [3, 0], [0, 1]], np.int32)
+    with pytest.raises(eu.EucalcError) as ei:
+        eu.transforms(cr, bad)
+    assert ei.value.status == eu.E_NONGENERIC and ei.value.bad_index == 1
+    with pytest.raises(eu.EucalcError) as ei:
+        eu.hybrid(cr, bad)
+    assert ei.value.status == eu.E_NONGENERIC
+    # capacity: hand the ABI a too-small buffer
+    import ctypes
+    dirs = np.array([[1, 2], [3, -1]], np.int32)
+    off = torch.zeros(5, dtype=torch.int64, device="cuda")
+    h = torch.zeros(4, dtype=torch.int64, device="cuda")
+    v = torch.zeros(4, dtype=torch.int64, device="cuda")
+    st = eu._Steps(off.data_ptr(), h.data_ptr(), v.data_ptr(), 4, 8, 0)
+    req = ctypes.c_int64()
+    rc = eu.lib().eucalc_ect(cr._h, dirs.ctypes.data_as(ctypes.c_void_p), 2, ctypes.byref(st), ctypes.byref(req),
+                             ctypes.c_void_p(torch.cuda.current_stream().cuda_stream))
+    assert rc == eu.E_CAPACITY and req.value == cr.output_bound(dirs)[0] > 4
+    with pytest.raises(eu.EucalcError) as ei:
+        eu.build_complex(np.zeros((1, 4, 4, 4, 4), np.uint8))
+    assert ei.value.status == eu.E_ARG
+
+
+def test_counts_match_oracle():
+    images = synth.blob_images(4, 28, 9)
+    cx = eu.build_complex(images, "vertex")
+    cr = eu.critical_points(cx)
+    cnt = cr.counts()
+    for b in range(4):
+        g = oracle.Grid(images[b], "vertex")
+        for e in range(4):
+            c, _, o, _ = g.critical_table(e)
+            assert tuple(cnt[b, e]) == (len(c), len(o))
+
+
+# ----------------------------------------------------------------------------- BASELINE configs
+
+def test_config1_full():
+    c = synth.config_inputs(1)
+    _, cr, res = run_gpu(c["images"], c["dirs"], c["construction"])
+    check_critical(c["images"], c["construction"], cr)
+    check_transforms(c["images"], c["dirs"], c["construction"], res)
+
+
+@pytest.mark.parametrize("variant", ["gray", "binary"])
+@pytest.mark.parametrize("construction", ["vertex", "top"])
+def test_config2_small_full(variant, construction):
+    c = synth.config_inputs(2, variant, small=True)
+    imgs, dirs = c["images"][:16], c["dirs"]
+    _, cr, res = run_gpu(imgs, dirs, construction)
+    check_transforms(imgs, dirs, construction, res)
+    check_critical(imgs, construction, cr, imgs_to_check=range(4))
+
+
+def test_config2_full_size_sampled():
+    """Full config 2 (1024 images x 256 directions) in the bench's launch
+    configuration; a seeded sample of (image, direction) segments vs the oracle."""
+    c = synth.config_inputs(2, "gray")
+    imgs, dirs = c["images"], c["dirs"]
+    _, cr, res = run_gpu(imgs, dirs, "vertex", elem_bytes=4, share=True)
+    rng = np.random.default_rng(0)
+    pairs = [(int(b), int(d)) for b, d in zip(rng.integers(0, 1024, 300), rng.integers(0, 256, 300))]
+    pairs += [(0, 0), (1023, 255)]
+    check_transforms(imgs, dirs, "vertex", res, pairs=pairs)
+
+
+def test_config3_sampled():
+    c = synth.config_inputs(3)
+    img, dirs = c["images"], c["dirs"][:64]
+    _, cr, res = run_gpu(img, dirs, "vertex")
+    check_transforms(img, dirs, "vertex", res, pairs=[(0, d) for d in (0, 17, 63)])
+    check_critical(img, "vertex", cr)
+
+
+def test_config4_sampled():
+    c = synth.config_inputs(4)
+    img, dirs = c["images"], c["dirs"][:48]
+    _, cr, res = run_gpu(img, dirs, "vertex")
+    check_transforms(img, dirs, "vertex", res, pairs=[(0, 0), (0, 31)])
+
+
+def test_config5_sampled():
+    c = synth.config_inputs(5)
+    vols, dirs = c["images"][:2], c["dirs"]
+    cx = eu.build_complex(vols, "vertex")
+    cr = eu.critical_points(cx)
+    pairs = [(0, 0), (1, 4999), (0, 9999)]
+    for kernel, param in (("gauss", 1.0), ("cos", 64.0)):
+        for precision in ("f64", "f32"):
+            check_ht(vols, dirs, "vertex", cr, kernel, param, precision, pairs=pairs)
