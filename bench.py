@@ -113,7 +113,7 @@ def run_step(eu, torch, imgs_dev, dirs, record=None):
     for img in imgs_dev:
         cx = eu.build_complex(img, "vertex")
         cr = eu.critical_points(cx)
-        r = eu.transforms(cr, dirs, elem_bytes=4, share_heights=True)
+        r = eu.transforms(cr, dirs, elem_bytes="auto", share_heights=True)
         ht = eu.hybrid(cr, dirs, HT_KERNEL, 1.0, "f64")
         out.append((cx, cr, r, ht))
     return out
@@ -127,11 +127,12 @@ def run_step_e2e(eu, torch, imgs_host, dirs):
         cx = eu.build_complex(img, "vertex")  # H2D inside the ABI
         h2d += img.numel() * img.element_size()
         cr = eu.critical_points(cx)
-        r = eu.transforms(cr, dirs, elem_bytes=4, share_heights=True, device="cpu")  # D2H inside the ABI
+        r = eu.transforms(cr, dirs, elem_bytes="auto", share_heights=True, device="cpu")  # D2H inside the ABI
         ht = eu.hybrid(cr, dirs, HT_KERNEL, 1.0, "f64", device="cpu")
         for k, st in r.items():
             n = int(st["offsets"][-1])
-            d2h += st["offsets"].numel() * 8 + n * 4 + (n * 4 if (k != "classical") else 0)
+            eb = st["value"].element_size()
+            d2h += st["offsets"].numel() * 8 + n * eb + (n * eb if (k != "classical") else 0)
         d2h += ht.numel() * 8
         h2d += dirs.nbytes
     return h2d, d2h
@@ -203,8 +204,10 @@ def gpu_arm(args):
         S = cx.batch * NDIRS
         ne = int(r["ect"]["offsets"][S])
         no = int(r["ordinary"]["offsets"][S])
+        eb = r["ect"]["value"].element_size()
         lists = list_bytes(cr, dirs)
-        k2_bytes += lists + ne * 8 + no * 8 + ne * 4 + 3 * (S + 1) * 8
+        # ECT (h,v) + ordinary (h,v) + classical (v; heights shared) + 3 offset arrays
+        k2_bytes += lists + ne * 2 * eb + no * 2 * eb + ne * eb + 3 * (S + 1) * 8
     k2_bytes /= 2  # per launch (two variants per step)
     peak, peak_src = peaks()
     achieved = k2_bytes / (k2_launch_ms / 1e3) / 1e9
@@ -335,7 +338,7 @@ def main(argv=None):
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--cpu-sample", type=int, default=16, help="images per variant in the oracle sample")
+    ap.add_argument("--cpu-sample", type=int, default=96, help="images per variant in the oracle sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args(argv)
     if args.warmup < 3:

@@ -218,7 +218,7 @@ def critical_points(cx: Complex, stream=None) -> Critical:
 
 
 def _alloc_steps(torch, S, cap, elem_bytes, device, with_height=True):
-    dt = torch.int32 if elem_bytes == 4 else torch.int64
+    dt = {2: torch.int16, 4: torch.int32, 8: torch.int64}[elem_bytes]
     pin = device == "cpu" and torch.cuda.is_available()
     mk = lambda n, t: torch.empty(n, dtype=t, device=device, pin_memory=pin)
     off = mk(S + 1, torch.int64)
@@ -233,8 +233,18 @@ def transforms(cr: Critical, dirs, ect=True, ordinary=True, classical=True, elem
     """eucalc_transforms: canonical ECT (T,E) and Radon (T_o,E'), (T_c,E_c) for every
     (image, direction), as CSR torch tensors on `device` ("cuda" or "cpu").
 
+    elem_bytes: 2, 4 or 8 (int16/int32/int64 heights and values), or "auto" for
+    the narrowest width the library accepts (E_RANGE -> next width).
     share_heights=True lets the classical stream reuse the ECT heights (T_c = T,
     Lemma 6) instead of writing them twice; its "height" is then the ECT tensor."""
+    if elem_bytes == "auto":
+        for eb in (2, 4):
+            try:
+                return transforms(cr, dirs, ect, ordinary, classical, eb, device, share_heights, stream)
+            except EucalcError as e:
+                if e.status != E_RANGE:
+                    raise
+        elem_bytes = 8
     import torch
 
     d = _dirs_i32(dirs)

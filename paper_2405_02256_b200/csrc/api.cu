@@ -180,7 +180,7 @@ eucalc_status sync_counts(Critical *cr, cudaStream_t st) {
     if (cr->have_host) return EUCALC_OK;
     const Complex *cx = cr->cx;
     const int64_t nc = cx->batch * cr->Q;
-    const int64_t ns = cx->batch * (1 << cx->ndim) * 2 + nc;
+    const int64_t ns = cx->batch * (1 << cx->ndim) * 2 + 2 * nc;
     std::vector<int32_t> c(nc);
     cr->h_count = new (std::nothrow) int64_t[nc];
     cr->h_stats = new (std::nothrow) int64_t[ns];
@@ -194,21 +194,50 @@ eucalc_status sync_counts(Critical *cr, cudaStream_t st) {
         cr->max_count = std::max<int64_t>(cr->max_count, c[i]);
     }
     cr->max_abs_sum = 0;
-    for (int64_t i = 0; i < nc; ++i)
-        cr->max_abs_sum = std::max<int64_t>(cr->max_abs_sum, cr->h_stats[cx->batch * (1 << cx->ndim) * 2 + i]);
+    cr->max_rec = 0;
+    const int64_t *abs_sum = cr->h_stats + cx->batch * (1 << cx->ndim) * 2;
+    for (int64_t i = 0; i < nc; ++i) {
+        cr->max_abs_sum = std::max<int64_t>(cr->max_abs_sum, abs_sum[i]);
+        cr->max_rec = std::max<int64_t>(cr->max_rec, abs_sum[nc + i]);
+    }
     cr->have_host = true;
     return EUCALC_OK;
 }
 
+// sum over (image, direction) of min(list length, R_d), in O(batch * Q * log D):
+// per pair, the directions' R sorted with prefix sums.
 eucalc_status bounds(Critical *cr, const DirPlan &p, cudaStream_t st, int64_t &bound) {
     eucalc_status s = sync_counts(cr, st);
     if (s != EUCALC_OK) return s;
     bound = 0;
     const int64_t D = (int64_t)p.info.size();
-    for (int64_t b = 0; b < cr->cx->batch; ++b)
+    for (int q = 0; q < cr->Q; ++q) {
+        std::vector<int64_t> R;
         for (int64_t d = 0; d < D; ++d)
-            bound += std::min<int64_t>(cr->h_count[b * cr->Q + p.info[d].q], p.info[d].R);
+            if (p.info[d].q == q) R.push_back(p.info[d].R);
+        if (R.empty()) continue;
+        std::sort(R.begin(), R.end());
+        std::vector<int64_t> pre(R.size() + 1, 0);
+        for (size_t i = 0; i < R.size(); ++i) pre[i + 1] = pre[i] + R[i];
+        for (int64_t b = 0; b < cr->cx->batch; ++b) {
+            const int64_t c = cr->h_count[b * cr->Q + q];
+            const size_t k = std::upper_bound(R.begin(), R.end(), c) - R.begin();  // R[<k] <= c
+            bound += pre[k] + (int64_t)(R.size() - k) * c;
+        }
+    }
     return EUCALC_OK;
+}
+
+// Every record at one lattice height lies on a distinct line along any axis k
+// with M_k > 1 (the height is strictly monotone along it), so a bin holds at
+// most nvert / max_k M_k records; with |a|+|b| <= max_rec per record this
+// bounds every bin sum of Delta^- and of J.
+int64_t bin_sum_bound(const Critical *cr) {
+    const Complex *cx = cr->cx;
+    int64_t mmax = 1;
+    for (int k = 0; k < cx->ndim; ++k) mmax = std::max<int64_t>(mmax, cx->M[k]);
+    const int64_t per_bin = std::max<int64_t>(1, cx->nvert / mmax);
+    return std::min<int64_t>(cr->max_abs_sum, per_bin * cr->max_rec);
 }
 
 }  // namespace
@@ -379,7 +408,7 @@ eucalc_status eucalc_critical_points(const eucalc_complex *cx, void *stream, euc
     cr->vcap = cx->nvert;
     const size_t rsz = cr->wide ? sizeof(Rec32) : sizeof(Rec16);
     const int64_t nlist = cx->batch * cr->Q;
-    const int64_t nstats = cx->batch * (1 << n) * 2 + nlist;
+    const int64_t nstats = cx->batch * (1 << n) * 2 + 2 * nlist;
     // tile shape: full rows when they fit (row-major list order)
     const int TV = k1_tile_vertices();
     const int MX = (int)cx->M[n - 1], MY = (int)cx->M[n - 2];
@@ -424,6 +453,7 @@ eucalc_status eucalc_critical_points(const eucalc_complex *cx, void *stream, euc
         a.ticket = ticket;
         a.stats = cr->d_stats;
         a.abs_sum = cr->d_stats + cx->batch * (1 << n) * 2;
+        a.max_rec = a.abs_sum + nlist;
         ProfScope ps("k1_critical", st);
         e = launch_k1(a, st);
     }
@@ -559,7 +589,7 @@ eucalc_status eucalc_transforms(const eucalc_critical *ccr, const int32_t *dirs,
     for (eucalc_steps *o : outs) {
         if (!o) continue;
         if (!o->offsets || (!o->height && o != classical) || !o->value) return fail(EUCALC_E_ARG, "NULL output array");
-        if (o->elem_bytes != 4 && o->elem_bytes != 8) return fail(EUCALC_E_ARG, "elem_bytes must be 4 or 8");
+        if (o->elem_bytes != 2 && o->elem_bytes != 4 && o->elem_bytes != 8) return fail(EUCALC_E_ARG, "elem_bytes must be 2, 4 or 8");
         if (eb && o->elem_bytes != eb) return fail(EUCALC_E_ARG, "all outputs must share elem_bytes");
         eb = o->elem_bytes;
         if (o->capacity < bnd) return fail(EUCALC_E_CAPACITY, "capacity " + std::to_string(o->capacity) + " < required bound " + std::to_string(bnd));
@@ -568,6 +598,11 @@ eucalc_status eucalc_transforms(const eucalc_critical *ccr, const int32_t *dirs,
     // value bounds: every bin sum, ECT and Radon value is bounded by the list's sum |a|+|b|
     if (cr->max_abs_sum >= (int64_t(1) << 31)) return fail(EUCALC_E_RANGE, "total |weight| of a critical list exceeds 2^31");
     if (bnd >= (int64_t(1) << 31)) return fail(EUCALC_E_RANGE, "more than 2^31 output entries in one call");
+    if (eb == 2) {
+        bool fits = cr->max_abs_sum < 32768;
+        for (const DirInfo &di : p.info) fits = fits && di.hlo >= -32768 && (int64_t)di.hlo + di.R - 1 <= 32767;
+        if (!fits) return fail(EUCALC_E_RANGE, "heights or values do not fit int16 (elem_bytes 2)");
+    }
     const int64_t S = cx->batch * D;
     if (S == 0) return EUCALC_OK;
     const bool cls_alias = classical && ect && (classical->height == ect->height || !classical->height);
@@ -631,6 +666,7 @@ eucalc_status eucalc_transforms(const eucalc_critical *ccr, const int32_t *dirs,
         a.R_max = p.R_max;
         a.max_count = cr->max_count;
         a.elem_bytes = eb;
+        a.pack16 = bin_sum_bound(cr) < 32768;
         a.do_ect = ect != nullptr;
         a.do_ord = ordinary != nullptr;
         a.do_cls = classical != nullptr;

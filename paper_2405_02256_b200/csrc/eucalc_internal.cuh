@@ -46,13 +46,14 @@ struct Critical {
     int64_t vcap = 0;   // records capacity per (image, pair) list = nvert
     void *d_rec = nullptr;       // [batch][Q][vcap]
     int32_t *d_count = nullptr;  // [batch][Q]
-    int64_t *d_stats = nullptr;  // [batch][2^n][2] (N^-, N^ord) then [batch][Q] sum(|a|+|b|)
+    int64_t *d_stats = nullptr;  // [batch][2^n][2] (N^-, N^ord), [batch][Q] sum(|a|+|b|), [batch][Q] max(|a|+|b|)
     // host cache (filled by sync_counts)
     bool have_host = false;
     int64_t *h_count = nullptr;  // [batch][Q]
     int64_t *h_stats = nullptr;
     int64_t max_count = 0;
     int64_t max_abs_sum = 0;
+    int64_t max_rec = 0;
 };
 
 // ---- launchers (implemented in the .cu files) -------------------------------
@@ -70,6 +71,7 @@ struct K1Args {
     unsigned int *ticket;
     int64_t *stats;
     int64_t *abs_sum;
+    int64_t *max_rec;
 };
 cudaError_t launch_k1(const K1Args &a, cudaStream_t s);
 
@@ -101,6 +103,7 @@ struct K2Args {
     int R_max;
     int64_t max_count;
     int elem_bytes;
+    bool pack16;  // 16+16-bit packed histogram bins are exact (host-checked)
     bool do_ect, do_ord, do_cls, cls_alias;
     StepsOut ect, ord, cls;
     unsigned long long *flags;  // [batch*D]

@@ -219,8 +219,12 @@ __global__ void __launch_bounds__(kThreads) k1_kernel(K1Args a) {
 #pragma unroll
     for (int e = 0; e < (1 << N); ++e) cnt_o[e][0] = cnt_o[e][1] = 0;
     long long abs_sum[Q];
+    int max_rec[Q];
 #pragma unroll
-    for (int q = 0; q < Q; ++q) abs_sum[q] = 0;
+    for (int q = 0; q < Q; ++q) {
+        abs_sum[q] = 0;
+        max_rec[q] = 0;
+    }
 
     for (int c0 = 0; c0 < TV; c0 += kThreads) {
         const int li = c0 + tid;
@@ -256,6 +260,7 @@ __global__ void __launch_bounds__(kThreads) k1_kernel(K1Args a) {
             bal[q] = __ballot_sync(0xffffffffu, keep[q]);
             if (lane == 0) s_warp[warp][q] = __popc(bal[q]);
             abs_sum[q] += abs(dm[q]) + abs(dm[q ^ FULL]);
+            max_rec[q] = max(max_rec[q], abs(dm[q]) + abs(dm[q ^ FULL]));
         }
         __syncthreads();
 #pragma unroll
@@ -297,6 +302,9 @@ __global__ void __launch_bounds__(kThreads) k1_kernel(K1Args a) {
         long long v = abs_sum[q];
         for (int d = 16; d; d >>= 1) v += __shfl_xor_sync(0xffffffffu, v, d);
         if (lane == 0 && v) atomicAdd((unsigned long long *)&a.abs_sum[b * Q + q], (unsigned long long)v);
+        int mr = max_rec[q];
+        for (int d = 16; d; d >>= 1) mr = max(mr, __shfl_xor_sync(0xffffffffu, mr, d));
+        if (lane == 0 && mr) atomicMax((unsigned long long *)&a.max_rec[b * Q + q], (unsigned long long)mr);
     }
     __syncthreads();
     if (tid < (1 << N) * 2) {

@@ -99,56 +99,125 @@ __device__ __forceinline__ void decode(const RecT &r, const DirInfo &di, const K
     wj = di.swap ? (y - x) : (x - y);
 }
 
-__device__ __forceinline__ void unpack_bin(unsigned long long v, int &wc, int &wj) {
-    wc = (int)(unsigned)(v & 0xffffffffull);
-    wj = (int)((long long)(v - (unsigned long long)(long long)wc) >> 32);
-}
+// Height histogram in shared memory with native 32-bit atomics (ATOMS.ADD;
+// 64-bit shared atomics are a CAS loop on sm_100a).
+//   PACK : one u32 per bin holding wj * 2^16 + wc, a linear packing that is
+//          exact while every bin's |sum| < 2^15 (host-checked bound).
+//   SPLIT: two u32 arrays (sum Delta^-, sum J), int32 sums.
+template <bool PACK>
+struct Hist {
+    unsigned *c;
+    unsigned *j;
+    __device__ __forceinline__ void add(int bin, int wc, int wj) const {
+        if (PACK) {
+            if (wc | wj) atomicAdd(c + bin, (unsigned)(wj * 65536 + wc));
+        } else {
+            if (wc) atomicAdd(c + bin, (unsigned)wc);
+            if (wj) atomicAdd(j + bin, (unsigned)wj);
+        }
+    }
+    // bins b0..b0+3 (b0 % 4 == 0), optionally cleared
+    __device__ __forceinline__ void load4(int b0, int (&wc)[4], int (&wj)[4], bool clear) const {
+        if (PACK) {
+            uint4 v = *reinterpret_cast<const uint4 *>(c + b0);
+            if (clear) *reinterpret_cast<uint4 *>(c + b0) = make_uint4(0, 0, 0, 0);
+            const unsigned u[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+            for (int s = 0; s < 4; ++s) {
+                wc[s] = (int)(short)(u[s] & 0xffffu);
+                wj[s] = ((int)u[s] - wc[s]) >> 16;
+            }
+        } else {
+            uint4 v = *reinterpret_cast<const uint4 *>(c + b0);
+            uint4 w = *reinterpret_cast<const uint4 *>(j + b0);
+            if (clear) {
+                *reinterpret_cast<uint4 *>(c + b0) = make_uint4(0, 0, 0, 0);
+                *reinterpret_cast<uint4 *>(j + b0) = make_uint4(0, 0, 0, 0);
+            }
+            wc[0] = (int)v.x; wc[1] = (int)v.y; wc[2] = (int)v.z; wc[3] = (int)v.w;
+            wj[0] = (int)w.x; wj[1] = (int)w.y; wj[2] = (int)w.z; wj[3] = (int)w.w;
+        }
+    }
+};
 
 template <typename OutT>
-__device__ __forceinline__ void put(const StepsOut &o, long long pos, long long h, long long v) {
+__device__ __forceinline__ void put(const StepsOut &o, long long pos, int h, int v) {
     reinterpret_cast<OutT *>(o.h)[pos] = (OutT)h;
     reinterpret_cast<OutT *>(o.v)[pos] = (OutT)v;
 }
 template <typename OutT>
-__device__ __forceinline__ void put_v(const StepsOut &o, long long pos, long long v) {
+__device__ __forceinline__ void put_v(const StepsOut &o, long long pos, int v) {
     reinterpret_cast<OutT *>(o.v)[pos] = (OutT)v;
 }
 
-// Emit one 32-bin chunk held by a warp (lane <-> bin). Running totals and
-// counters are warp-uniform.
-template <typename OutT>
-__device__ __forceinline__ void emit_chunk(const K2Args &a, int hbase, int wc, int wj, long long &e_run,
-                                           long long &r_run, long long &pos_c, long long &pos_o) {
+__device__ __forceinline__ int warp_incl_scan(int v) {
     const int lane = threadIdx.x & 31;
-    int ic = wc, ij = wj;
 #pragma unroll
     for (int d = 1; d < 32; d <<= 1) {
-        int tc = __shfl_up_sync(0xffffffffu, ic, d);
-        int tj = __shfl_up_sync(0xffffffffu, ij, d);
-        if (lane >= d) {
-            ic += tc;
-            ij += tj;
+        const int t = __shfl_up_sync(0xffffffffu, v, d);
+        if (lane >= d) v += t;
+    }
+    return v;
+}
+
+// Count the nonzero bins of one 128-bin group (lane <-> 4 consecutive bins).
+template <bool PACK>
+__device__ __forceinline__ void count_group(const Hist<PACK> &hs, int base, int &c, int &o, bool clear) {
+    int wc[4], wj[4];
+    hs.load4(base + 4 * (threadIdx.x & 31), wc, wj, clear);
+#pragma unroll
+    for (int s = 0; s < 4; ++s) {
+        c += wc[s] != 0;
+        o += wj[s] != 0;
+    }
+}
+
+// Emit one 128-bin group held by a warp (lane <-> 4 consecutive bins) in height
+// order: local sums per lane, one warp scan of (counts, sum Delta^-, sum J),
+// then up to 4 entries per stream per lane. Running values are warp-uniform.
+template <typename OutT, bool PACK>
+__device__ __forceinline__ void emit_group(const K2Args &a, const Hist<PACK> &hs, int base, int h0, int &e_run,
+                                           int &r_run, long long &pc, long long &po) {
+    const int lane = threadIdx.x & 31;
+    int wc[4], wj[4];
+    hs.load4(base + 4 * lane, wc, wj, true);
+    int lc = 0, lo = 0, sc = 0, sj = 0;
+#pragma unroll
+    for (int s = 0; s < 4; ++s) {
+        lc += wc[s] != 0;
+        lo += wj[s] != 0;
+        sc += wc[s];
+        sj += wj[s];
+    }
+    const int cnt = lc | (lo << 16);
+    const int ic = warp_incl_scan(cnt), isc = warp_incl_scan(sc), isj = warp_incl_scan(sj);
+    const int ec = ic - cnt;
+    long long p_c = pc + (ec & 0xffff), p_o = po + (ec >> 16);
+    int e = e_run + (isc - sc), r = r_run + (isj - sj);
+    const int hb = h0 + base + 4 * lane;
+#pragma unroll
+    for (int s = 0; s < 4; ++s) {
+        const int rb = r;
+        e += wc[s];
+        r += wj[s];
+        if (wc[s]) {
+            if (a.do_ect) put<OutT>(a.ect, p_c, hb + s, e);
+            if (a.do_cls) {
+                if (a.cls_alias) put_v<OutT>(a.cls, p_c, rb + wc[s]);
+                else put<OutT>(a.cls, p_c, hb + s, rb + wc[s]);
+            }
+            ++p_c;
+        }
+        if (wj[s]) {
+            if (a.do_ord) put<OutT>(a.ord, p_o, hb + s, r);
+            ++p_o;
         }
     }
-    const unsigned mc = __ballot_sync(0xffffffffu, wc != 0);
-    const unsigned mo = __ballot_sync(0xffffffffu, wj != 0);
-    const unsigned lt = (1u << lane) - 1;
-    const long long e_incl = e_run + ic;
-    const long long r_incl = r_run + ij;
-    const long long h = (long long)hbase + lane;
-    if (wc != 0) {
-        const long long p = pos_c + __popc(mc & lt);
-        if (a.do_ect) put<OutT>(a.ect, p, h, e_incl);
-        if (a.do_cls) {
-            if (a.cls_alias) put_v<OutT>(a.cls, p, r_incl - wj + wc);
-            else put<OutT>(a.cls, p, h, r_incl - wj + wc);
-        }
-    }
-    if (wj != 0 && a.do_ord) put<OutT>(a.ord, pos_o + __popc(mo & lt), h, r_incl);
-    pos_c += __popc(mc);
-    pos_o += __popc(mo);
-    e_run = __shfl_sync(0xffffffffu, e_incl, 31);
-    r_run = __shfl_sync(0xffffffffu, r_incl, 31);
+    const int tc = __shfl_sync(0xffffffffu, ic, 31);
+    pc += tc & 0xffff;
+    po += tc >> 16;
+    e_run += __shfl_sync(0xffffffffu, isc, 31);
+    r_run += __shfl_sync(0xffffffffu, isj, 31);
 }
 
 __device__ __forceinline__ void write_offsets(const K2Args &a, long long s, long long exc_c, long long exc_o,
@@ -164,17 +233,27 @@ __device__ __forceinline__ void write_offsets(const K2Args &a, long long s, long
     }
 }
 
+__device__ __forceinline__ int warp_sum(int v) {
+#pragma unroll
+    for (int d = 16; d; d >>= 1) v += __shfl_xor_sync(0xffffffffu, v, d);
+    return v;
+}
+
 // ----------------------------------------------------------------------------- warp kernel
 constexpr int kWarpThreads = 256;
+constexpr int kGroup = 128;  // bins per warp step (4 per lane)
 
-template <typename RecT, typename OutT>
+template <typename RecT, typename OutT, bool PACK>
 __global__ void __launch_bounds__(kWarpThreads) k2_warp(K2Args a, int rcap, int warps, long long nblk_total,
                                                        int ndblk) {
-    extern __shared__ __align__(16) unsigned long long hist_all[];
+    extern __shared__ __align__(16) unsigned hist_all[];
     __shared__ long long s_ticket;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    unsigned long long *hist = hist_all + (size_t)warp * rcap;
-    for (int i = threadIdx.x; i < warps * rcap; i += blockDim.x) hist_all[i] = 0;
+    constexpr int words = PACK ? 1 : 2;
+    Hist<PACK> hs;
+    hs.c = hist_all + (size_t)warp * rcap * words;
+    hs.j = hs.c + rcap;
+    for (int i = threadIdx.x; i < warps * rcap * words; i += blockDim.x) hist_all[i] = 0;
     const RecT *recs = reinterpret_cast<const RecT *>(a.rec);
     while (true) {
         __syncthreads();
@@ -190,36 +269,24 @@ __global__ void __launch_bounds__(kWarpThreads) k2_warp(K2Args a, int rcap, int 
         const DirInfo di = a.dirs[d];
         const RecT *list = recs + (b * a.Q + di.q) * a.vcap;
         const int n = a.count[b * a.Q + di.q];
-        // A4: histogram (run-length merge by height)
+        // A4: histogram = run-length merge by height
         for (int i = lane; i < n; i += 32) {
             int bin, wc, wj;
             decode(list[i], di, a, bin, wc, wj);
-            const unsigned long long pk =
-                ((unsigned long long)(long long)wj << 32) + (unsigned long long)(long long)wc;
-            if (pk) atomicAdd(hist + bin, pk);
+            hs.add(bin, wc, wj);
         }
         __syncwarp();
-        // A5 pass 1: counts
-        long long nc = 0, no = 0;
-        for (int base = 0; base < di.R; base += 32) {
-            int wc = 0, wj = 0;
-            if (base + lane < di.R) unpack_bin(hist[base + lane], wc, wj);
-            nc += __popc(__ballot_sync(0xffffffffu, wc != 0));
-            no += __popc(__ballot_sync(0xffffffffu, wj != 0));
-        }
+        // A5 pass 1: counts of nonzero bins
+        int c = 0, o = 0;
+        for (int base = 0; base < di.R; base += kGroup) count_group(hs, base, c, o, false);
+        const long long nc = warp_sum(c), no = warp_sum(o);
         long long exc_c, exc_o;
         seg_lookback(a.flags, s, nc, no, exc_c, exc_o);
         if (lane == 0) write_offsets(a, s, exc_c, exc_o, nc, no);
-        // A5 pass 2: emit + clear
-        long long e_run = 0, r_run = 0, pos_c = exc_c, pos_o = exc_o;
-        for (int base = 0; base < di.R; base += 32) {
-            int wc = 0, wj = 0;
-            if (base + lane < di.R) {
-                unpack_bin(hist[base + lane], wc, wj);
-                hist[base + lane] = 0;
-            }
-            emit_chunk<OutT>(a, di.hlo + base, wc, wj, e_run, r_run, pos_c, pos_o);
-        }
+        // A5 pass 2: emit in height order + clear
+        int e_run = 0, r_run = 0;
+        long long pc = exc_c, po = exc_o;
+        for (int base = 0; base < di.R; base += kGroup) emit_group<OutT>(a, hs, base, di.hlo, e_run, r_run, pc, po);
         __syncwarp();
     }
 }
@@ -227,31 +294,31 @@ __global__ void __launch_bounds__(kWarpThreads) k2_warp(K2Args a, int rcap, int 
 // ----------------------------------------------------------------------------- block kernel
 constexpr int kBlockThreads = 512;
 constexpr int kBlockWarps = kBlockThreads / 32;
-constexpr int kWinBins = 26624;  // 208 KB of 64-bit bins
+constexpr size_t kBlockSmem = 208 * 1024;
 
-template <typename RecT>
+template <typename RecT, bool PACK>
 __device__ void fill_window(const K2Args &a, const RecT *list, int n, const DirInfo &di, int lo, int wbins,
-                            unsigned long long *hist) {
+                            const Hist<PACK> &hs) {
     for (int i = threadIdx.x; i < n; i += kBlockThreads) {
         int bin, wc, wj;
         decode(list[i], di, a, bin, wc, wj);
         bin -= lo;
-        if ((unsigned)bin < (unsigned)wbins) {
-            const unsigned long long pk =
-                ((unsigned long long)(long long)wj << 32) + (unsigned long long)(long long)wc;
-            if (pk) atomicAdd(hist + bin, pk);
-        }
+        if ((unsigned)bin < (unsigned)wbins) hs.add(bin, wc, wj);
     }
 }
 
-template <typename RecT, typename OutT>
-__global__ void __launch_bounds__(kBlockThreads, 1) k2_block(K2Args a, long long nseg) {
-    extern __shared__ __align__(16) unsigned long long hist[];
+template <typename RecT, typename OutT, bool PACK>
+__global__ void __launch_bounds__(kBlockThreads, 1) k2_block(K2Args a, long long nseg, int win) {
+    extern __shared__ __align__(16) unsigned hist[];
     __shared__ long long s_seg;
-    __shared__ long long s_wsum[kBlockWarps][4];  // per-warp (nc, no, sum wc, sum wj)
+    __shared__ int s_wsum[kBlockWarps][4];  // per-warp (nc, no, sum wc, sum wj)
     __shared__ long long s_exc[2];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    for (int i = threadIdx.x; i < kWinBins; i += kBlockThreads) hist[i] = 0;
+    constexpr int words = PACK ? 1 : 2;
+    Hist<PACK> hs;
+    hs.c = hist;
+    hs.j = hist + win;
+    for (int i = threadIdx.x; i < win * words; i += kBlockThreads) hist[i] = 0;
     const RecT *recs = reinterpret_cast<const RecT *>(a.rec);
     while (true) {
         __syncthreads();
@@ -263,25 +330,20 @@ __global__ void __launch_bounds__(kBlockThreads, 1) k2_block(K2Args a, long long
         const DirInfo di = a.dirs[d];
         const RecT *list = recs + (b * a.Q + di.q) * a.vcap;
         const int n = a.count[b * a.Q + di.q];
-        const int nwin = (di.R + kWinBins - 1) / kWinBins;
+        const int nwin = (di.R + win - 1) / win;
+        // each warp owns a contiguous, 128-aligned range of the window
+        const int per = ((win / kBlockWarps) + kGroup - 1) / kGroup * kGroup;
         // phase A: counts over all windows
         long long nc = 0, no = 0;
         for (int w = 0; w < nwin; ++w) {
-            const int lo = w * kWinBins, wb = min(kWinBins, di.R - lo);
-            fill_window(a, list, n, di, lo, wb, hist);
+            const int lo = w * win, wb = min(win, di.R - lo);
+            fill_window(a, list, n, di, lo, wb, hs);
             __syncthreads();
             int c = 0, o = 0;
-            for (int i = threadIdx.x; i < wb; i += kBlockThreads) {
-                int wc, wj;
-                unpack_bin(hist[i], wc, wj);
-                c += wc != 0;
-                o += wj != 0;
-                if (nwin > 1) hist[i] = 0;
-            }
-            for (int dd = 16; dd; dd >>= 1) {
-                c += __shfl_xor_sync(0xffffffffu, c, dd);
-                o += __shfl_xor_sync(0xffffffffu, o, dd);
-            }
+            const int b0 = min(wb, warp * per), b1 = min(wb, b0 + per);
+            for (int base = b0; base < b1; base += kGroup) count_group(hs, base, c, o, nwin > 1);
+            c = warp_sum(c);
+            o = warp_sum(o);
             if (lane == 0) {
                 s_wsum[warp][0] = c;
                 s_wsum[warp][1] = o;
@@ -303,30 +365,32 @@ __global__ void __launch_bounds__(kBlockThreads, 1) k2_block(K2Args a, long long
             }
         }
         __syncthreads();
-        // phase B: emit, window by window; warp k owns a contiguous bin range of the window
-        long long e_carry = 0, r_carry = 0, pc_carry = s_exc[0], po_carry = s_exc[1];
+        // phase B: emit window by window
+        long long pc_carry = s_exc[0], po_carry = s_exc[1];
+        int e_carry = 0, r_carry = 0;
         for (int w = 0; w < nwin; ++w) {
-            const int lo = w * kWinBins, wb = min(kWinBins, di.R - lo);
+            const int lo = w * win, wb = min(win, di.R - lo);
             if (nwin > 1) {
-                fill_window(a, list, n, di, lo, wb, hist);
+                fill_window(a, list, n, di, lo, wb, hs);
                 __syncthreads();
             }
-            const int per = ((wb + kBlockWarps - 1) / kBlockWarps + 31) & ~31;
             const int b0 = min(wb, warp * per), b1 = min(wb, b0 + per);
-            long long c = 0, o = 0, sc = 0, sj = 0;
-            for (int base = b0; base < b1; base += 32) {
-                int wc = 0, wj = 0;
-                if (base + lane < b1) unpack_bin(hist[base + lane], wc, wj);
-                c += __popc(__ballot_sync(0xffffffffu, wc != 0));
-                o += __popc(__ballot_sync(0xffffffffu, wj != 0));
-                long long x = wc, y = wj;
-                for (int dd = 16; dd; dd >>= 1) {
-                    x += __shfl_xor_sync(0xffffffffu, x, dd);
-                    y += __shfl_xor_sync(0xffffffffu, y, dd);
+            int c = 0, o = 0, sc = 0, sj = 0;
+            for (int base = b0; base < b1; base += kGroup) {
+                int wc[4], wj[4];
+                hs.load4(base + 4 * lane, wc, wj, false);
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    c += wc[q] != 0;
+                    o += wj[q] != 0;
+                    sc += wc[q];
+                    sj += wj[q];
                 }
-                sc += x;
-                sj += y;
             }
+            c = warp_sum(c);
+            o = warp_sum(o);
+            sc = warp_sum(sc);
+            sj = warp_sum(sj);
             if (lane == 0) {
                 s_wsum[warp][0] = c;
                 s_wsum[warp][1] = o;
@@ -334,8 +398,10 @@ __global__ void __launch_bounds__(kBlockThreads, 1) k2_block(K2Args a, long long
                 s_wsum[warp][3] = sj;
             }
             __syncthreads();
-            long long pc = pc_carry, po = po_carry, er = e_carry, rr = r_carry;
-            long long tc = 0, to = 0, tsc = 0, tsj = 0;
+            long long pc = pc_carry, po = po_carry;
+            int er = e_carry, rr = r_carry;
+            long long tc = 0, to = 0;
+            int tsc = 0, tsj = 0;
             for (int k = 0; k < kBlockWarps; ++k) {
                 if (k < warp) {
                     pc += s_wsum[k][0];
@@ -348,14 +414,7 @@ __global__ void __launch_bounds__(kBlockThreads, 1) k2_block(K2Args a, long long
                 tsc += s_wsum[k][2];
                 tsj += s_wsum[k][3];
             }
-            for (int base = b0; base < b1; base += 32) {
-                int wc = 0, wj = 0;
-                if (base + lane < b1) {
-                    unpack_bin(hist[base + lane], wc, wj);
-                    hist[base + lane] = 0;
-                }
-                emit_chunk<OutT>(a, di.hlo + lo + base, wc, wj, er, rr, pc, po);
-            }
+            for (int base = b0; base < b1; base += kGroup) emit_group<OutT>(a, hs, base, di.hlo + lo, er, rr, pc, po);
             pc_carry += tc;
             po_carry += to;
             e_carry += tsc;
@@ -365,18 +424,19 @@ __global__ void __launch_bounds__(kBlockThreads, 1) k2_block(K2Args a, long long
     }
 }
 
-template <typename RecT, typename OutT>
+template <typename RecT, typename OutT, bool PACK>
 cudaError_t launch_t(const K2Args &a, cudaStream_t s, int num_sms) {
     const long long nseg = a.batch * a.D;
+    constexpr int words = PACK ? 1 : 2;
     // warp regime: whole histogram per warp, small lists
-    const int rcap = (a.R_max + 31) & ~31;
-    const size_t per_warp = (size_t)rcap * 8;
+    const int rcap = (a.R_max + kGroup - 1) / kGroup * kGroup;
+    const size_t per_warp = (size_t)rcap * 4 * words;
     int warps = (int)std::min<size_t>(8, (200 * 1024) / per_warp);
     if (warps >= 2 && a.max_count <= 32768) {
         const int ndblk = (int)((a.D + warps - 1) / warps);
         const long long nblk = a.batch * ndblk;
         const size_t smem = per_warp * warps;
-        auto kern = k2_warp<RecT, OutT>;
+        auto kern = k2_warp<RecT, OutT, PACK>;
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
         int occ = 0;
@@ -386,21 +446,33 @@ cudaError_t launch_t(const K2Args &a, cudaStream_t s, int num_sms) {
         count_launch();
         return cudaGetLastError();
     }
-    const size_t smem = (size_t)kWinBins * 8;
-    auto kern = k2_block<RecT, OutT>;
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    const int win = (int)(kBlockSmem / (4 * words)) / kGroup * kGroup;
+    auto kern = k2_block<RecT, OutT, PACK>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kBlockSmem);
     if (e != cudaSuccess) return e;
     long long grid = std::min<long long>(nseg, num_sms);
-    kern<<<(unsigned)grid, kBlockThreads, smem, s>>>(a, nseg);
+    kern<<<(unsigned)grid, kBlockThreads, kBlockSmem, s>>>(a, nseg, win);
     count_launch();
     return cudaGetLastError();
+}
+
+template <typename RecT, typename OutT>
+cudaError_t launch_p(const K2Args &a, cudaStream_t s, int num_sms) {
+    return a.pack16 ? launch_t<RecT, OutT, true>(a, s, num_sms) : launch_t<RecT, OutT, false>(a, s, num_sms);
+}
+template <typename RecT>
+cudaError_t launch_o(const K2Args &a, cudaStream_t s, int num_sms) {
+    switch (a.elem_bytes) {
+    case 2: return launch_p<RecT, int16_t>(a, s, num_sms);
+    case 4: return launch_p<RecT, int32_t>(a, s, num_sms);
+    default: return launch_p<RecT, int64_t>(a, s, num_sms);
+    }
 }
 
 }  // namespace
 
 cudaError_t launch_k2(const K2Args &a, cudaStream_t s, int num_sms) {
-    if (a.wide) return a.elem_bytes == 4 ? launch_t<Rec32, int32_t>(a, s, num_sms) : launch_t<Rec32, int64_t>(a, s, num_sms);
-    return a.elem_bytes == 4 ? launch_t<Rec16, int32_t>(a, s, num_sms) : launch_t<Rec16, int64_t>(a, s, num_sms);
+    return a.wide ? launch_o<Rec32>(a, s, num_sms) : launch_o<Rec16>(a, s, num_sms);
 }
 
 }  // namespace eucalc

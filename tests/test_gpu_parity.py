@@ -165,13 +165,23 @@ def test_output_widths_and_shared_heights():
     images = synth.blob_images(6, 28, 1)
     dirs = synth.random_directions(20, 2, 16, 3)
     _, _, r8 = run_gpu(images, dirs, "vertex", elem_bytes=8)
-    _, _, r4 = run_gpu(images, dirs, "vertex", elem_bytes=4, share=True)
-    for k in ("ect", "ordinary", "classical"):
-        S = images.shape[0] * len(dirs)
-        np.testing.assert_array_equal(r8[k]["offsets"], r4[k]["offsets"])
-        n = r8[k]["offsets"][S]
-        np.testing.assert_array_equal(r8[k]["height"][:n], r4[k]["height"][:n])
-        np.testing.assert_array_equal(r8[k]["value"][:n], r4[k]["value"][:n])
+    for eb in (4, 2):
+        _, _, r4 = run_gpu(images, dirs, "vertex", elem_bytes=eb, share=True)
+        for k in ("ect", "ordinary", "classical"):
+            S = images.shape[0] * len(dirs)
+            np.testing.assert_array_equal(r8[k]["offsets"], r4[k]["offsets"])
+            n = r8[k]["offsets"][S]
+            np.testing.assert_array_equal(r8[k]["height"][:n], r4[k]["height"][:n])
+            np.testing.assert_array_equal(r8[k]["value"][:n], r4[k]["value"][:n])
+    # int16 must be refused when values cannot fit
+    big = (np.random.default_rng(1).integers(0, 30000, size=(2, 28, 28))).astype(np.int32)
+    cx = eu.build_complex(big, "vertex")
+    cr = eu.critical_points(cx)
+    with pytest.raises(eu.EucalcError) as ei:
+        eu.transforms(cr, dirs, elem_bytes=2)
+    assert ei.value.status == eu.E_RANGE
+    r = eu.transforms(cr, dirs, elem_bytes="auto")
+    assert r["ect"]["value"].element_size() == 4
 
 
 def test_host_buffers_match_device():
