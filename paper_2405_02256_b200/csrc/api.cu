@@ -3,6 +3,9 @@
 #include <algorithm>
 #include <cstdio>
 #include <cstring>
+#include <map>
+#include <memory>
+#include <mutex>
 #include <new>
 #include <numeric>
 #include <string>
@@ -123,6 +126,7 @@ struct DirPlan {
     std::vector<int32_t> csum;
     std::vector<int> orthant;
     int R_max = 0;
+    int dp = 0;  // all directions fit int8 and the complex is byte-aligned
 };
 
 eucalc_status plan_dirs(const Complex *cx, const int32_t *dirs, int64_t D, cudaStream_t st, DirPlan &p) {
@@ -172,22 +176,130 @@ eucalc_status plan_dirs(const Complex *cx, const int32_t *dirs, int64_t D, cudaS
         p.csum[d] = (int32_t)cs;
         p.orthant[d] = e;
         p.R_max = std::max(p.R_max, di.R);
+        bool fits8 = true;
+        uint32_t x8 = 0;
+        for (int k = 0; k < n; ++k) {
+            fits8 = fits8 && di.xs[k] >= -127 && di.xs[k] <= 127;
+            x8 |= (uint32_t)(di.xs[k] & 0xff) << (8 * (n - 1 - k));
+        }
+        p.info[d].xs8 = (int)x8;
+        if (d == 0) p.dp = cx->aligned;
+        if (!fits8) p.dp = 0;
     }
+    return EUCALC_OK;
+}
+
+// ---- direction plans, cached with their device copies ------------------------
+// A plan holds the host DirInfo and the device arrays K2/K3 read (DirInfo,
+// csum, orthant-grouped order and tiles). Re-using a direction set (the common
+// case: many batches, one set of directions) then costs no host->device copy
+// — a pageable cudaMemcpyAsync would synchronise the stream.
+struct PlanEntry {
+    std::vector<int32_t> key;
+    int ndim = 0, aligned = 0, dev = 0;
+    int64_t M[kMaxN] = {0, 0, 0}, scale[kMaxN] = {0, 0, 0};
+    DirPlan p;
+    std::vector<int32_t> order, tstart, tlen;
+    DirInfo *d_info = nullptr;
+    int32_t *d_csum = nullptr, *d_order = nullptr, *d_ts = nullptr, *d_tl = nullptr;
+    uint64_t stamp = 0;
+    ~PlanEntry() {
+        // cudaFree synchronises the device, so no in-flight kernel still reads these
+        cudaFree(d_info);
+        cudaFree(d_csum);
+        cudaFree(d_order);
+        cudaFree(d_ts);
+        cudaFree(d_tl);
+    }
+};
+std::mutex g_plan_mu;
+std::vector<std::shared_ptr<PlanEntry>> g_plans;
+uint64_t g_plan_clock = 0;
+constexpr size_t kMaxPlans = 16;
+
+eucalc_status get_plan(const Complex *cx, const int32_t *dirs, int64_t D, cudaStream_t st,
+                       std::shared_ptr<PlanEntry> &out) {
+    if (D < 0) return fail(EUCALC_E_ARG, "D < 0");
+    if (D > 0 && !dirs) return fail(EUCALC_E_ARG, "dirs is NULL");
+    const int n = cx->ndim;
+    std::vector<int32_t> h((size_t)D * n);
+    if (D > 0) {
+        if (is_device_ptr(dirs)) {
+            CK(cudaMemcpyAsync(h.data(), dirs, sizeof(int32_t) * D * n, cudaMemcpyDeviceToHost, st));
+            CK(cudaStreamSynchronize(st));
+        } else {
+            memcpy(h.data(), dirs, sizeof(int32_t) * D * n);
+        }
+    }
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lk(g_plan_mu);
+    for (auto &e : g_plans) {
+        if (e->ndim == n && e->dev == dev && e->aligned == cx->aligned && e->key == h &&
+            std::equal(e->M, e->M + n, cx->M) && std::equal(e->scale, e->scale + n, cx->scale)) {
+            e->stamp = ++g_plan_clock;
+            out = e;
+            return EUCALC_OK;
+        }
+    }
+    auto e = std::make_shared<PlanEntry>();
+    eucalc_status s = plan_dirs(cx, h.data(), D, st, e->p);
+    if (s != EUCALC_OK) return s;
+    e->key = std::move(h);
+    e->ndim = n;
+    e->dev = dev;
+    e->aligned = cx->aligned;
+    std::copy(cx->M, cx->M + n, e->M);
+    std::copy(cx->scale, cx->scale + n, e->scale);
+    // HT tiles: directions grouped by orthant (Lemma 3), <= 256 per tile
+    e->order.resize(D);
+    std::iota(e->order.begin(), e->order.end(), 0);
+    std::stable_sort(e->order.begin(), e->order.end(),
+                     [&](int32_t x, int32_t y) { return e->p.orthant[x] < e->p.orthant[y]; });
+    for (int64_t i = 0; i < D;) {
+        int64_t j = i;
+        while (j < D && e->p.orthant[e->order[j]] == e->p.orthant[e->order[i]] && j - i < 256) ++j;
+        e->tstart.push_back((int32_t)i);
+        e->tlen.push_back((int32_t)(j - i));
+        i = j;
+    }
+    if (D > 0) {
+        const size_t nt = e->tstart.size();
+        CK(cudaMalloc(&e->d_info, sizeof(DirInfo) * D));
+        CK(cudaMalloc(&e->d_csum, sizeof(int32_t) * D));
+        CK(cudaMalloc(&e->d_order, sizeof(int32_t) * D));
+        CK(cudaMalloc(&e->d_ts, sizeof(int32_t) * nt));
+        CK(cudaMalloc(&e->d_tl, sizeof(int32_t) * nt));
+        CK(cudaMemcpy(e->d_info, e->p.info.data(), sizeof(DirInfo) * D, cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(e->d_csum, e->p.csum.data(), sizeof(int32_t) * D, cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(e->d_order, e->order.data(), sizeof(int32_t) * D, cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(e->d_ts, e->tstart.data(), sizeof(int32_t) * nt, cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(e->d_tl, e->tlen.data(), sizeof(int32_t) * nt, cudaMemcpyHostToDevice));
+    }
+    e->stamp = ++g_plan_clock;
+    if (g_plans.size() >= kMaxPlans) {
+        auto it = std::min_element(g_plans.begin(), g_plans.end(),
+                                   [](const auto &x, const auto &y) { return x->stamp < y->stamp; });
+        g_plans.erase(it);
+    }
+    g_plans.push_back(e);
+    out = e;
     return EUCALC_OK;
 }
 
 eucalc_status sync_counts(Critical *cr, cudaStream_t st) {
     if (cr->have_host) return EUCALC_OK;
+    (void)st;
     const Complex *cx = cr->cx;
     const int64_t nc = cx->batch * cr->Q;
     const int64_t ns = cx->batch * (1 << cx->ndim) * 2 + 2 * nc;
-    std::vector<int32_t> c(nc);
     cr->h_count = new (std::nothrow) int64_t[nc];
     cr->h_stats = new (std::nothrow) int64_t[ns];
     if (!cr->h_count || !cr->h_stats) return fail(EUCALC_E_NOMEM, "host alloc");
-    CK(cudaMemcpyAsync(c.data(), cr->d_count, sizeof(int32_t) * nc, cudaMemcpyDeviceToHost, st));
-    CK(cudaMemcpyAsync(cr->h_stats, cr->d_stats, sizeof(int64_t) * ns, cudaMemcpyDeviceToHost, st));
-    CK(cudaStreamSynchronize(st));
+    // the read-back was enqueued right after K1 into pinned memory: wait for it only
+    CK(cudaEventSynchronize(cr->k1_done));
+    const int32_t *c = (const int32_t *)cr->pinned;
+    memcpy(cr->h_stats, (const unsigned char *)cr->pinned + cr->pinned_stats_off, sizeof(int64_t) * ns);
     cr->max_count = 0;
     for (int64_t i = 0; i < nc; ++i) {
         cr->h_count[i] = c[i];
@@ -243,6 +355,36 @@ int64_t bin_sum_bound(const Critical *cr) {
 }  // namespace
 
 void count_launch(int n) { g_launches += n; }
+
+namespace {
+std::mutex g_pin_mu;
+std::multimap<size_t, void *> g_pin_free;
+}  // namespace
+
+void *pinned_get(size_t bytes, size_t *cap) {
+    size_t c = 256;
+    while (c < bytes) c <<= 1;
+    {
+        std::lock_guard<std::mutex> lk(g_pin_mu);
+        auto it = g_pin_free.find(c);
+        if (it != g_pin_free.end()) {
+            void *p = it->second;
+            g_pin_free.erase(it);
+            *cap = c;
+            return p;
+        }
+    }
+    void *p = nullptr;
+    if (cudaHostAlloc(&p, c, cudaHostAllocDefault) != cudaSuccess) return nullptr;
+    *cap = c;
+    return p;
+}
+
+void pinned_put(void *p, size_t cap) {
+    if (!p) return;
+    std::lock_guard<std::mutex> lk(g_pin_mu);
+    g_pin_free.emplace(cap, p);
+}
 
 }  // namespace eucalc
 
@@ -332,10 +474,15 @@ eucalc_status eucalc_build_complex(const void *img, int dtype, int ndim, const i
         delete cx;
         return fail(EUCALC_E_ARG, "image too large");
     }
-    // packed coordinates: axis n-1 in the low bits
+    // packed coordinates: axis n-1 in the low bits. Byte-aligned fields (16-bit
+    // halves in 2-D, bytes in 3-D) when the extents allow, so the height is one
+    // dp2a / dp4a instruction against the direction's packed int8 coordinates.
     int sh = 0;
+    bool al2 = ndim == 2 && cx->M[0] <= 65536 && cx->M[1] <= 65536;
+    bool al3 = ndim == 3 && cx->M[0] <= 256 && cx->M[1] <= 256 && cx->M[2] <= 256;
+    cx->aligned = al2 ? 2 : al3 ? 3 : 0;
     for (int k = ndim - 1; k >= 0; --k) {
-        int bw = bits_for(cx->M[k] - 1);
+        int bw = al2 ? 16 : al3 ? 8 : bits_for(cx->M[k] - 1);
         cx->sh[k] = sh;
         cx->msk[k] = (uint32_t)((1ull << bw) - 1);
         sh += bw;
@@ -358,6 +505,18 @@ eucalc_status eucalc_build_complex(const void *img, int dtype, int ndim, const i
         return cuda_fail(e, "cudaMallocAsync(image)");
     }
     e = cudaMemcpyAsync(cx->d_img, img, bytes, is_device_ptr(img) ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st);
+    if (dtype == EUCALC_U8) {
+        // |w| <= 255 by type: no reduction, no host synchronisation
+        if (e != cudaSuccess) {
+            cudaFreeAsync(cx->d_img, st);
+            delete cx;
+            return cuda_fail(e, "build_complex");
+        }
+        cx->max_abs_w = 255;
+        cx->owner_stream = st;
+        *out = cx;
+        return EUCALC_OK;
+    }
     unsigned long long *d_max = nullptr;
     if (e == cudaSuccess) e = cudaMallocAsync(&d_max, sizeof(unsigned long long), st);
     if (e == cudaSuccess) e = cudaMemsetAsync(d_max, 0, sizeof(unsigned long long), st);
@@ -388,7 +547,8 @@ eucalc_status eucalc_build_complex(const void *img, int dtype, int ndim, const i
 
 eucalc_status eucalc_destroy_complex(eucalc_complex *cx) {
     if (!cx) return fail(EUCALC_E_STATE, "NULL handle");
-    if (cx->d_img) cudaFree(cx->d_img);
+    // stream-ordered release on the stream the handle was built on (no device sync)
+    if (cx->d_img) cudaFreeAsync(cx->d_img, cx->owner_stream);
     delete cx;
     return EUCALC_OK;
 }
@@ -402,6 +562,7 @@ eucalc_status eucalc_critical_points(const eucalc_complex *cx, void *stream, euc
     if (!cr) return fail(EUCALC_E_NOMEM, "host alloc");
     const int n = cx->ndim;
     cr->cx = cx;
+    cr->owner_stream = st;
     cr->Q = 1 << (n - 1);
     // |Delta^-| <= 2^n max|w| must fit the record's int16 halves, J = a - b is formed in int32
     cr->wide = ((int64_t(1) << n) * cx->max_abs_w) > 32767;
@@ -454,8 +615,23 @@ eucalc_status eucalc_critical_points(const eucalc_complex *cx, void *stream, euc
         a.stats = cr->d_stats;
         a.abs_sum = cr->d_stats + cx->batch * (1 << n) * 2;
         a.max_rec = a.abs_sum + nlist;
-        ProfScope ps("k1_critical", st);
-        e = launch_k1(a, st);
+        {
+            ProfScope ps("k1_critical", st);
+            e = launch_k1(a, st);
+        }
+        // asynchronous read-back of the list lengths and statistics into pinned
+        // memory; sync_counts() later waits on this event only
+        cr->pinned_stats_off = ((sizeof(int32_t) * nlist + 15) / 16) * 16;
+        const size_t need = cr->pinned_stats_off + sizeof(int64_t) * nstats;
+        cr->pinned = pinned_get(need, &cr->pinned_bytes);
+        if (e == cudaSuccess && !cr->pinned) e = cudaErrorMemoryAllocation;
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&cr->k1_done, cudaEventDisableTiming);
+        if (e == cudaSuccess)
+            e = cudaMemcpyAsync(cr->pinned, cr->d_count, sizeof(int32_t) * nlist, cudaMemcpyDeviceToHost, st);
+        if (e == cudaSuccess)
+            e = cudaMemcpyAsync((unsigned char *)cr->pinned + cr->pinned_stats_off, cr->d_stats,
+                                sizeof(int64_t) * nstats, cudaMemcpyDeviceToHost, st);
+        if (e == cudaSuccess) e = cudaEventRecord(cr->k1_done, st);
     }
     if (flags) cudaFreeAsync(flags, st);
     if (ticket) cudaFreeAsync(ticket, st);
@@ -463,6 +639,9 @@ eucalc_status eucalc_critical_points(const eucalc_complex *cx, void *stream, euc
         if (cr->d_rec) cudaFreeAsync(cr->d_rec, st);
         if (cr->d_count) cudaFreeAsync(cr->d_count, st);
         if (cr->d_stats) cudaFreeAsync(cr->d_stats, st);
+        if (cr->k1_done) cudaEventDestroy(cr->k1_done);
+        cudaStreamSynchronize(st);
+        pinned_put(cr->pinned, cr->pinned_bytes);
         delete cr;
         return cuda_fail(e, "critical_points");
     }
@@ -472,9 +651,14 @@ eucalc_status eucalc_critical_points(const eucalc_complex *cx, void *stream, euc
 
 eucalc_status eucalc_destroy_critical(eucalc_critical *cr) {
     if (!cr) return fail(EUCALC_E_STATE, "NULL handle");
-    cudaFree(cr->d_rec);
-    cudaFree(cr->d_count);
-    cudaFree(cr->d_stats);
+    cudaFreeAsync(cr->d_rec, cr->owner_stream);
+    cudaFreeAsync(cr->d_count, cr->owner_stream);
+    cudaFreeAsync(cr->d_stats, cr->owner_stream);
+    if (cr->k1_done) {
+        cudaEventSynchronize(cr->k1_done);  // the read-back into `pinned` has landed
+        cudaEventDestroy(cr->k1_done);
+    }
+    pinned_put(cr->pinned, cr->pinned_bytes);
     delete[] cr->h_count;
     delete[] cr->h_stats;
     delete cr;
@@ -559,11 +743,11 @@ eucalc_status eucalc_output_bound(const eucalc_critical *ccr, const int32_t *dir
                                   int64_t *bound_ordinary, void *stream) {
     if (!ccr) return fail(EUCALC_E_STATE, "NULL handle");
     eucalc_critical *cr = const_cast<eucalc_critical *>(ccr);
-    DirPlan p;
-    eucalc_status s = plan_dirs(cr->cx, dirs, D, (cudaStream_t)stream, p);
+    std::shared_ptr<PlanEntry> pe;
+    eucalc_status s = get_plan(cr->cx, dirs, D, (cudaStream_t)stream, pe);
     if (s != EUCALC_OK) return s;
     int64_t bnd = 0;
-    s = bounds(cr, p, (cudaStream_t)stream, bnd);
+    s = bounds(cr, pe->p, (cudaStream_t)stream, bnd);
     if (s != EUCALC_OK) return s;
     if (bound_ect) *bound_ect = bnd;
     if (bound_ordinary) *bound_ordinary = bnd;
@@ -577,9 +761,10 @@ eucalc_status eucalc_transforms(const eucalc_critical *ccr, const int32_t *dirs,
     eucalc_critical *cr = const_cast<eucalc_critical *>(ccr);
     const Complex *cx = cr->cx;
     cudaStream_t st = (cudaStream_t)stream;
-    DirPlan p;
-    eucalc_status s = plan_dirs(cx, dirs, D, st, p);
+    std::shared_ptr<PlanEntry> pe;
+    eucalc_status s = get_plan(cx, dirs, D, st, pe);
     if (s != EUCALC_OK) return s;
+    const DirPlan &p = pe->p;
     int64_t bnd = 0;
     s = bounds(cr, p, st, bnd);
     if (s != EUCALC_OK) return s;
@@ -639,16 +824,16 @@ eucalc_status eucalc_transforms(const eucalc_critical *ccr, const int32_t *dirs,
             dev[i].v = o->value;
         }
     }
-    DirInfo *d_info = (DirInfo *)dalloc(sizeof(DirInfo) * D);
+    const DirInfo *d_info = pe->d_info;
     unsigned long long *flags = (unsigned long long *)dalloc(sizeof(unsigned long long) * S);
-    unsigned int *ticket = (unsigned int *)dalloc(sizeof(unsigned int));
-    if (!d_info || !flags || !ticket) {
+    unsigned int *ticket = (unsigned int *)dalloc(sizeof(unsigned int) * 4);
+    int *cnts = (int *)dalloc(sizeof(int) * 2 * S);
+    if (!flags || !ticket || !cnts) {
         free_scratch();
         return fail(EUCALC_E_NOMEM, "scratch");
     }
-    cudaError_t e = cudaMemcpyAsync(d_info, p.info.data(), sizeof(DirInfo) * D, cudaMemcpyHostToDevice, st);
-    if (e == cudaSuccess) e = cudaMemsetAsync(flags, 0, sizeof(unsigned long long) * S, st);
-    if (e == cudaSuccess) e = cudaMemsetAsync(ticket, 0, sizeof(unsigned int), st);
+    cudaError_t e = cudaMemsetAsync(flags, 0, sizeof(unsigned long long) * S, st);
+    if (e == cudaSuccess) e = cudaMemsetAsync(ticket, 0, sizeof(unsigned int) * 4, st);
     if (e == cudaSuccess) {
         a.rec = cr->d_rec;
         a.wide = cr->wide;
@@ -667,6 +852,7 @@ eucalc_status eucalc_transforms(const eucalc_critical *ccr, const int32_t *dirs,
         a.max_count = cr->max_count;
         a.elem_bytes = eb;
         a.pack16 = bin_sum_bound(cr) < 32768;
+        a.dp = p.dp;
         a.do_ect = ect != nullptr;
         a.do_ord = ordinary != nullptr;
         a.do_cls = classical != nullptr;
@@ -676,6 +862,8 @@ eucalc_status eucalc_transforms(const eucalc_critical *ccr, const int32_t *dirs,
         a.cls = dev[2];
         a.flags = flags;
         a.ticket = ticket;
+        a.cnt_c = cnts;
+        a.cnt_o = cnts + S;
         ProfScope ps("k2_transforms", st);
         e = launch_k2(a, st, num_sms());
     }
@@ -726,24 +914,14 @@ eucalc_status eucalc_hybrid(const eucalc_critical *ccr, const int32_t *dirs, int
     eucalc_critical *cr = const_cast<eucalc_critical *>(ccr);
     const Complex *cx = cr->cx;
     cudaStream_t st = (cudaStream_t)stream;
-    DirPlan p;
-    eucalc_status s = plan_dirs(cx, dirs, D, st, p);
+    std::shared_ptr<PlanEntry> pe;
+    eucalc_status s = get_plan(cx, dirs, D, st, pe);
     if (s != EUCALC_OK) return s;
+    const DirPlan &p = pe->p;
     s = sync_counts(cr, st);
     if (s != EUCALC_OK) return s;
     if (D == 0) return EUCALC_OK;
-    // group directions by orthant (Lemma 3) into tiles of <= 256
-    std::vector<int32_t> order(D);
-    std::iota(order.begin(), order.end(), 0);
-    std::stable_sort(order.begin(), order.end(), [&](int32_t x, int32_t y) { return p.orthant[x] < p.orthant[y]; });
-    std::vector<int32_t> tstart, tlen;
-    for (int64_t i = 0; i < D;) {
-        int64_t j = i;
-        while (j < D && p.orthant[order[j]] == p.orthant[order[i]] && j - i < 256) ++j;
-        tstart.push_back((int32_t)i);
-        tlen.push_back((int32_t)(j - i));
-        i = j;
-    }
+    const std::vector<int32_t> &tstart = pe->tstart;
     const int chunk = k3_chunk();
     const int nchunks = (int)std::max<int64_t>(1, (cr->max_count + chunk - 1) / chunk);
     const size_t osz = precision == EUCALC_F32 ? 4 : 8;
@@ -756,22 +934,15 @@ eucalc_status eucalc_hybrid(const eucalc_critical *ccr, const int32_t *dirs, int
         return q;
     };
     auto free_scratch = [&]() { for (void *q : scratch) cudaFreeAsync(q, st); };
-    DirInfo *d_info = (DirInfo *)dalloc(sizeof(DirInfo) * D);
-    int32_t *d_order = (int32_t *)dalloc(sizeof(int32_t) * D);
-    int32_t *d_ts = (int32_t *)dalloc(sizeof(int32_t) * tstart.size());
-    int32_t *d_tl = (int32_t *)dalloc(sizeof(int32_t) * tlen.size());
-    int32_t *d_cs = (int32_t *)dalloc(sizeof(int32_t) * D);
+    const DirInfo *d_info = pe->d_info;
+    const int32_t *d_order = pe->d_order, *d_ts = pe->d_ts, *d_tl = pe->d_tl, *d_cs = pe->d_csum;
     double *d_part = (double *)dalloc(sizeof(double) * cx->batch * nchunks * D);
     void *d_out = host_out ? dalloc(osz * cx->batch * D) : out;
-    if (!d_info || !d_order || !d_ts || !d_tl || !d_cs || !d_part || !d_out) {
+    if (!d_part || !d_out) {
         free_scratch();
         return fail(EUCALC_E_NOMEM, "scratch");
     }
-    cudaError_t e = cudaMemcpyAsync(d_info, p.info.data(), sizeof(DirInfo) * D, cudaMemcpyHostToDevice, st);
-    if (e == cudaSuccess) e = cudaMemcpyAsync(d_order, order.data(), sizeof(int32_t) * D, cudaMemcpyHostToDevice, st);
-    if (e == cudaSuccess) e = cudaMemcpyAsync(d_ts, tstart.data(), sizeof(int32_t) * tstart.size(), cudaMemcpyHostToDevice, st);
-    if (e == cudaSuccess) e = cudaMemcpyAsync(d_tl, tlen.data(), sizeof(int32_t) * tlen.size(), cudaMemcpyHostToDevice, st);
-    if (e == cudaSuccess) e = cudaMemcpyAsync(d_cs, p.csum.data(), sizeof(int32_t) * D, cudaMemcpyHostToDevice, st);
+    cudaError_t e = cudaSuccess;
     if (e == cudaSuccess) {
         K3Args a{};
         a.rec = cr->d_rec;
@@ -796,6 +967,9 @@ eucalc_status eucalc_hybrid(const eucalc_critical *ccr, const int32_t *dirs, int
         a.param = param;
         a.L = cx->L;
         a.csum = d_cs;
+        a.dp = p.dp;
+        const int maxlen = *std::max_element(pe->tlen.begin(), pe->tlen.end());
+        a.threads = std::max(32, (maxlen + 31) / 32 * 32);
         a.nchunks = nchunks;
         a.partial = d_part;
         a.out = d_out;

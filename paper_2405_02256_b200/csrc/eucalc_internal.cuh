@@ -34,6 +34,7 @@ struct Complex {
     int64_t max_abs_w = 0;
     int sh[kMaxN] = {0, 0, 0};     // packed coordinate shifts
     uint32_t msk[kMaxN] = {0, 0, 0};
+    int aligned = 0;               // 2: 16-bit coordinate halves (dp2a), 3: bytes (dp4a), 0: generic
     int64_t L = 1;                 // lcm of (M_i - 1) > 0
     int64_t scale[kMaxN] = {0, 0, 0};
     cudaStream_t owner_stream = nullptr;
@@ -54,7 +55,15 @@ struct Critical {
     int64_t max_count = 0;
     int64_t max_abs_sum = 0;
     int64_t max_rec = 0;
+    cudaStream_t owner_stream = nullptr;
+    cudaEvent_t k1_done = nullptr;  // after the async read-back of counts/stats
+    void *pinned = nullptr;         // pinned host copy: int32 counts, then int64 stats
+    size_t pinned_bytes = 0, pinned_stats_off = 0;
 };
+
+// Pinned host memory pool (power-of-two size classes, reused; never unpinned).
+void *pinned_get(size_t bytes, size_t *cap);
+void pinned_put(void *p, size_t cap);
 
 // ---- launchers (implemented in the .cu files) -------------------------------
 struct K1Args {
@@ -82,6 +91,7 @@ struct DirInfo {
     int R;          // number of lattice heights
     int q;          // antipodal pair of the orthant
     int swap;       // 1 if the orthant is the pair's non-representative
+    int xs8;        // xs as packed int8 (byte j <-> axis n-1-j) when every |xs_i| <= 127
 };
 
 struct StepsOut {
@@ -103,11 +113,13 @@ struct K2Args {
     int R_max;
     int64_t max_count;
     int elem_bytes;
+    int dp;       // 2/3: heights by dp2a/dp4a on byte-aligned coordinates; 0: shifts and masks
     bool pack16;  // 16+16-bit packed histogram bins are exact (host-checked)
     bool do_ect, do_ord, do_cls, cls_alias;
     StepsOut ect, ord, cls;
-    unsigned long long *flags;  // [batch*D]
-    unsigned int *ticket;
+    unsigned long long *flags;  // [batch*D] look-back flags (zeroed)
+    unsigned int *ticket;       // [4] ticket counters (zeroed)
+    int *cnt_c, *cnt_o;         // [batch*D] per-segment counts (warp regime)
 };
 cudaError_t launch_k2(const K2Args &a, cudaStream_t s, int num_sms);
 
@@ -129,6 +141,8 @@ struct K3Args {
     double param;
     int64_t L;
     const int32_t *csum;       // [D] sum of xi_i over axes with M_i > 1
+    int dp;                    // as K2Args::dp
+    int threads;               // block size = longest tile rounded up to a warp
     int nchunks;
     double *partial;           // [batch][nchunks][D]
     void *out;                 // [batch][D]

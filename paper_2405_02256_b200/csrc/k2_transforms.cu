@@ -28,6 +28,7 @@
 //                 and only in-window records are accumulated (configs 3-4).
 #include <algorithm>
 #include <climits>
+#include <type_traits>
 
 #include "eucalc_internal.cuh"
 
@@ -90,10 +91,19 @@ template <typename RecT>
 __device__ __forceinline__ void decode(const RecT &r, const DirInfo &di, const K2Args &a, int &bin, int &wc,
                                        int &wj) {
     int h = 0;
+    if (a.dp == 2) {
+        // h = sum of 16-bit unsigned coordinate halves x signed int8 direction bytes
+        asm("dp2a.lo.u32.s32 %0, %1, %2, %3;" : "=r"(h) : "r"(r.c), "r"(di.xs8), "r"(-di.hlo));
+        bin = h;
+    } else if (a.dp == 3) {
+        asm("dp4a.u32.s32 %0, %1, %2, %3;" : "=r"(h) : "r"(r.c), "r"(di.xs8), "r"(-di.hlo));
+        bin = h;
+    } else {
 #pragma unroll
-    for (int k = 0; k < kMaxN; ++k)
-        if (k < a.ndim) h += di.xs[k] * (int)((r.c >> a.sh[k]) & a.msk[k]);
-    bin = h - di.hlo;
+        for (int k = 0; k < kMaxN; ++k)
+            if (k < a.ndim) h += di.xs[k] * (int)((r.c >> a.sh[k]) & a.msk[k]);
+        bin = h - di.hlo;
+    }
     const int x = r.a, y = r.b;
     wc = di.swap ? y : x;
     wj = di.swap ? (y - x) : (x - y);
@@ -150,12 +160,16 @@ __device__ __forceinline__ void put_v(const StepsOut &o, long long pos, int v) {
     reinterpret_cast<OutT *>(o.v)[pos] = (OutT)v;
 }
 
+// Inclusive warp scan; the shuffle's own in-range predicate guards the add
+// (2 instructions per step).
 __device__ __forceinline__ int warp_incl_scan(int v) {
-    const int lane = threadIdx.x & 31;
 #pragma unroll
     for (int d = 1; d < 32; d <<= 1) {
-        const int t = __shfl_up_sync(0xffffffffu, v, d);
-        if (lane >= d) v += t;
+        asm("{\n\t.reg .s32 t;\n\t.reg .pred p;\n\t"
+            "shfl.sync.up.b32 t|p, %0, %1, 0x0, 0xffffffff;\n\t"
+            "@p add.s32 %0, t, %0;\n\t}"
+            : "+r"(v)
+            : "r"(d));
     }
     return v;
 }
@@ -172,12 +186,50 @@ __device__ __forceinline__ void count_group(const Hist<PACK> &hs, int base, int 
     }
 }
 
+// Which streams an emission writes: compile-time for the common requests,
+// kModeAny checks K2Args at run time.
+constexpr int kEct = 1, kOrd = 2, kCls = 4, kAlias = 8, kModeAny = 16;
+
+template <typename OutT>
+struct OutPtrs {
+    OutT *eh, *ev, *oh, *ov, *ch, *cv;
+    bool ect, ord, cls, alias;
+    __device__ explicit OutPtrs(const K2Args &a)
+        : eh((OutT *)a.ect.h), ev((OutT *)a.ect.v), oh((OutT *)a.ord.h), ov((OutT *)a.ord.v),
+          ch((OutT *)a.cls.h), cv((OutT *)a.cls.v), ect(a.do_ect), ord(a.do_ord), cls(a.do_cls),
+          alias(a.cls_alias) {}
+};
+
+template <int MODE, typename OutT>
+__device__ __forceinline__ void put_c(const OutPtrs<OutT> &o, int p, int h, int e, int cv) {
+    const bool ect = MODE == kModeAny ? o.ect : (MODE & kEct);
+    const bool cls = MODE == kModeAny ? o.cls : (MODE & kCls);
+    const bool alias = MODE == kModeAny ? o.alias : (MODE & kAlias);
+    if (ect) {
+        o.eh[p] = (OutT)h;
+        o.ev[p] = (OutT)e;
+    }
+    if (cls) {
+        if (!alias) o.ch[p] = (OutT)h;
+        o.cv[p] = (OutT)cv;
+    }
+}
+template <int MODE, typename OutT>
+__device__ __forceinline__ void put_o(const OutPtrs<OutT> &o, int p, int h, int r) {
+    const bool ord = MODE == kModeAny ? o.ord : (MODE & kOrd);
+    if (ord) {
+        o.oh[p] = (OutT)h;
+        o.ov[p] = (OutT)r;
+    }
+}
+
 // Emit one 128-bin group held by a warp (lane <-> 4 consecutive bins) in height
 // order: local sums per lane, one warp scan of (counts, sum Delta^-, sum J),
-// then up to 4 entries per stream per lane. Running values are warp-uniform.
-template <typename OutT, bool PACK>
-__device__ __forceinline__ void emit_group(const K2Args &a, const Hist<PACK> &hs, int base, int h0, int &e_run,
-                                           int &r_run, long long &pc, long long &po) {
+// then up to 4 entries per stream per lane. Running values are warp-uniform;
+// positions are int32 (< 2^31 entries per call, host-checked).
+template <int MODE, typename OutT, bool PACK>
+__device__ __forceinline__ void emit_group(const OutPtrs<OutT> &o, const Hist<PACK> &hs, int base, int h0,
+                                           int &e_run, int &r_run, int &pc, int &po) {
     const int lane = threadIdx.x & 31;
     int wc[4], wj[4];
     hs.load4(base + 4 * lane, wc, wj, true);
@@ -192,7 +244,7 @@ __device__ __forceinline__ void emit_group(const K2Args &a, const Hist<PACK> &hs
     const int cnt = lc | (lo << 16);
     const int ic = warp_incl_scan(cnt), isc = warp_incl_scan(sc), isj = warp_incl_scan(sj);
     const int ec = ic - cnt;
-    long long p_c = pc + (ec & 0xffff), p_o = po + (ec >> 16);
+    int p_c = pc + (ec & 0xffff), p_o = po + (ec >> 16);
     int e = e_run + (isc - sc), r = r_run + (isj - sj);
     const int hb = h0 + base + 4 * lane;
 #pragma unroll
@@ -200,18 +252,8 @@ __device__ __forceinline__ void emit_group(const K2Args &a, const Hist<PACK> &hs
         const int rb = r;
         e += wc[s];
         r += wj[s];
-        if (wc[s]) {
-            if (a.do_ect) put<OutT>(a.ect, p_c, hb + s, e);
-            if (a.do_cls) {
-                if (a.cls_alias) put_v<OutT>(a.cls, p_c, rb + wc[s]);
-                else put<OutT>(a.cls, p_c, hb + s, rb + wc[s]);
-            }
-            ++p_c;
-        }
-        if (wj[s]) {
-            if (a.do_ord) put<OutT>(a.ord, p_o, hb + s, r);
-            ++p_o;
-        }
+        if (wc[s]) put_c<MODE>(o, p_c++, hb + s, e, rb + wc[s]);
+        if (wj[s]) put_o<MODE>(o, p_o++, hb + s, r);
     }
     const int tc = __shfl_sync(0xffffffffu, ic, 31);
     pc += tc & 0xffff;
@@ -243,51 +285,214 @@ __device__ __forceinline__ int warp_sum(int v) {
 constexpr int kWarpThreads = 256;
 constexpr int kGroup = 128;  // bins per warp step (4 per lane)
 
-template <typename RecT, typename OutT, bool PACK>
-__global__ void __launch_bounds__(kWarpThreads) k2_warp(K2Args a, int rcap, int warps, long long nblk_total,
-                                                       int ndblk) {
-    extern __shared__ __align__(16) unsigned hist_all[];
-    __shared__ long long s_ticket;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+// Warp regime, three launches with no cross-segment waiting:
+//   k2w_count: per segment (one warp, dynamic ticket) histogram + count of the
+//              nonzero bins of each stream -> counts[s] (the histogram is
+//              cleared while counting);
+//   k2_scan  : exclusive scan of the counts -> CSR offsets;
+//   k2w_emit : per segment histogram again + ordered emission at its offset.
+// (A single pass with a segment look-back was measured to lose ~1/3 of the
+// time to look-back spinning when ~9k warps start at once.)
+template <typename RecT, bool PACK>
+__device__ __forceinline__ void fill_segment(const K2Args &a, const Hist<PACK> &hs, long long b, const DirInfo &di) {
+    const int lane = threadIdx.x & 31;
+    const RecT *list = reinterpret_cast<const RecT *>(a.rec) + (b * a.Q + di.q) * a.vcap;
+    const int n = a.count[b * a.Q + di.q];
+    for (int i = lane; i < n; i += 32) {
+        int bin, wc, wj;
+        decode(list[i], di, a, bin, wc, wj);
+        hs.add(bin, wc, wj);
+    }
+    __syncwarp();
+}
+
+// Sparse path for lists of <= 32 records (e.g. binary images): the records'
+// (height, Delta^-, J) are sorted across the warp by a register bitonic
+// network and equal heights merged by prefix sums — the paper's sort +
+// merge without touching R bins.
+struct SparseRuns {
+    int h;            // bin (height - hlo) of this lane's sorted record
+    int pc, pj;       // inclusive prefix sums of Delta^- and J in sorted order
+    int run_c, run_j; // sums over this lane's equal-height run (valid at run ends)
+    bool emit_c, emit_o;
+};
+
+template <typename RecT>
+__device__ __forceinline__ SparseRuns sparse_runs(const K2Args &a, long long b, const DirInfo &di, int n) {
+    const int lane = threadIdx.x & 31;
+    const RecT *list = reinterpret_cast<const RecT *>(a.rec) + (b * a.Q + di.q) * a.vcap;
+    int h = INT_MAX, wc = 0, wj = 0;
+    if (lane < n) decode(list[lane], di, a, h, wc, wj);
+#pragma unroll
+    for (int k = 2; k <= 32; k <<= 1) {
+#pragma unroll
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            const int oh = __shfl_xor_sync(0xffffffffu, h, j);
+            const int oc = __shfl_xor_sync(0xffffffffu, wc, j);
+            const int oj = __shfl_xor_sync(0xffffffffu, wj, j);
+            const bool asc = (lane & k) == 0, lower = (lane & j) == 0;
+            if (lower == asc ? (oh < h) : (oh > h)) {
+                h = oh;
+                wc = oc;
+                wj = oj;
+            }
+        }
+    }
+    SparseRuns r;
+    r.h = h;
+    r.pc = warp_incl_scan(wc);
+    r.pj = warp_incl_scan(wj);
+    const int hn = __shfl_down_sync(0xffffffffu, h, 1);
+    const int hp = __shfl_up_sync(0xffffffffu, h, 1);
+    const bool end = lane == 31 || hn != h;
+    const bool head = lane == 0 || hp != h;
+    int st = head ? lane : 0;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const int t = __shfl_up_sync(0xffffffffu, st, d);
+        if (lane >= d) st = max(st, t);
+    }
+    const int src = st > 0 ? st - 1 : 0;
+    const int bc = __shfl_sync(0xffffffffu, r.pc, src), bj = __shfl_sync(0xffffffffu, r.pj, src);
+    r.run_c = r.pc - (st > 0 ? bc : 0);
+    r.run_j = r.pj - (st > 0 ? bj : 0);
+    const bool valid = end && h != INT_MAX;
+    r.emit_c = valid && r.run_c != 0;
+    r.emit_o = valid && r.run_j != 0;
+    return r;
+}
+
+template <bool PACK>
+__device__ __forceinline__ Hist<PACK> warp_hist(unsigned *smem, int rcap) {
     constexpr int words = PACK ? 1 : 2;
+    const int warp = threadIdx.x >> 5;
     Hist<PACK> hs;
-    hs.c = hist_all + (size_t)warp * rcap * words;
+    hs.c = smem + (size_t)warp * rcap * words;
     hs.j = hs.c + rcap;
-    for (int i = threadIdx.x; i < warps * rcap * words; i += blockDim.x) hist_all[i] = 0;
-    const RecT *recs = reinterpret_cast<const RecT *>(a.rec);
-    while (true) {
-        __syncthreads();
-        if (threadIdx.x == 0) s_ticket = (long long)atomicAdd(a.ticket, 1u);
-        __syncthreads();
-        const long long tk = s_ticket;
-        if (tk >= nblk_total) break;
-        if (warp >= warps) continue;
-        const long long b = tk / ndblk;
-        const long long d = (tk % ndblk) * warps + warp;
-        if (d >= a.D) continue;
-        const long long s = b * a.D + d;
+    for (int i = threadIdx.x; i < (int)(blockDim.x / 32) * rcap * words; i += blockDim.x) smem[i] = 0;
+    __syncthreads();
+    return hs;
+}
+
+
+template <typename RecT, bool PACK>
+__global__ void __launch_bounds__(kWarpThreads) k2w_count(K2Args a, int rcap, int *cnt_c, int *cnt_o) {
+    extern __shared__ __align__(16) unsigned hist_all[];
+    const Hist<PACK> hs = warp_hist<PACK>(hist_all, rcap);
+    const long long S = a.batch * a.D;
+    const long long nw = (long long)gridDim.x * (blockDim.x >> 5);
+    for (long long s = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); s < S; s += nw) {
+        const long long b = s / a.D, d = s % a.D;
         const DirInfo di = a.dirs[d];
-        const RecT *list = recs + (b * a.Q + di.q) * a.vcap;
         const int n = a.count[b * a.Q + di.q];
-        // A4: histogram = run-length merge by height
-        for (int i = lane; i < n; i += 32) {
-            int bin, wc, wj;
-            decode(list[i], di, a, bin, wc, wj);
-            hs.add(bin, wc, wj);
+        int c = 0, o = 0;
+        if (n <= 32) {
+            const SparseRuns r = sparse_runs<RecT>(a, b, di, n);
+            c = __popc(__ballot_sync(0xffffffffu, r.emit_c));
+            o = __popc(__ballot_sync(0xffffffffu, r.emit_o));
+        } else {
+            fill_segment<RecT>(a, hs, b, di);
+            for (int base = 0; base < di.R; base += kGroup) count_group(hs, base, c, o, true);
+            c = warp_sum(c);
+            o = warp_sum(o);
+        }
+        if ((threadIdx.x & 31) == 0) {
+            cnt_c[s] = c;
+            cnt_o[s] = o;
         }
         __syncwarp();
-        // A5 pass 1: counts of nonzero bins
-        int c = 0, o = 0;
-        for (int base = 0; base < di.R; base += kGroup) count_group(hs, base, c, o, false);
-        const long long nc = warp_sum(c), no = warp_sum(o);
-        long long exc_c, exc_o;
-        seg_lookback(a.flags, s, nc, no, exc_c, exc_o);
-        if (lane == 0) write_offsets(a, s, exc_c, exc_o, nc, no);
-        // A5 pass 2: emit in height order + clear
-        int e_run = 0, r_run = 0;
-        long long pc = exc_c, po = exc_o;
-        for (int base = 0; base < di.R; base += kGroup) emit_group<OutT>(a, hs, base, di.hlo, e_run, r_run, pc, po);
+    }
+}
+
+template <typename RecT, typename OutT, bool PACK, int MODE>
+__global__ void __launch_bounds__(kWarpThreads) k2w_emit(K2Args a, int rcap) {
+    extern __shared__ __align__(16) unsigned hist_all[];
+    const Hist<PACK> hs = warp_hist<PACK>(hist_all, rcap);
+    const OutPtrs<OutT> o(a);
+    const int S = (int)(a.batch * a.D), D = (int)a.D;
+    const int64_t *off_c = a.do_ect ? a.ect.off : a.cls.off;
+    const bool any_c = a.do_ect || a.do_cls;
+    const int nw = gridDim.x * (blockDim.x >> 5);
+    for (int s = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); s < S; s += nw) {
+        const int b = s / D, d = s - b * D;
+        const DirInfo di = a.dirs[d];
+        const int n = a.count[b * a.Q + di.q];
+        int pc = any_c ? (int)off_c[s] : 0, po = a.do_ord ? (int)a.ord.off[s] : 0;
+        if (n <= 32) {
+            const SparseRuns r = sparse_runs<RecT>(a, b, di, n);
+            const unsigned lt = (1u << (threadIdx.x & 31)) - 1;
+            const unsigned mc = __ballot_sync(0xffffffffu, r.emit_c), mo = __ballot_sync(0xffffffffu, r.emit_o);
+            const int h = di.hlo + r.h;
+            // classical value: Radon(h-) + sum Delta^- at h
+            if (r.emit_c) put_c<MODE>(o, pc + __popc(mc & lt), h, r.pc, r.pj - r.run_j + r.run_c);
+            if (r.emit_o) put_o<MODE>(o, po + __popc(mo & lt), h, r.pj);
+        } else {
+            fill_segment<RecT>(a, hs, b, di);
+            int e_run = 0, r_run = 0;
+            for (int base = 0; base < di.R; base += kGroup)
+                emit_group<MODE>(o, hs, base, di.hlo, e_run, r_run, pc, po);
+        }
         __syncwarp();
+    }
+}
+
+// Single-pass exclusive scan of (cnt_c, cnt_o) into the CSR offset arrays
+// (tiles of 8192 counts, decoupled look-back between the few tiles).
+constexpr int kScanThreads = 1024, kScanPer = 8, kScanTile = kScanThreads * kScanPer;
+
+__global__ void __launch_bounds__(kScanThreads) k2_scan(K2Args a, const int *cnt_c, const int *cnt_o, long long S,
+                                                       unsigned long long *flags) {
+    __shared__ long long s_w[kScanThreads / 32][2];
+    __shared__ long long s_base[2];
+    __shared__ unsigned s_tile;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (threadIdx.x == 0) s_tile = atomicAdd(a.ticket + 2, 1u);
+    __syncthreads();
+    const long long t = s_tile;
+    const long long i0 = t * kScanTile + (long long)threadIdx.x * kScanPer;
+    long long lc[kScanPer], lo[kScanPer], tc = 0, to = 0;
+#pragma unroll
+    for (int k = 0; k < kScanPer; ++k) {
+        const long long i = i0 + k;
+        lc[k] = i < S ? cnt_c[i] : 0;
+        lo[k] = i < S ? cnt_o[i] : 0;
+        tc += lc[k];
+        to += lo[k];
+    }
+    // block exclusive scan of thread totals
+    long long ic = tc, io = to;
+    for (int d = 1; d < 32; d <<= 1) {
+        long long x = __shfl_up_sync(0xffffffffu, ic, d), y = __shfl_up_sync(0xffffffffu, io, d);
+        if (lane >= d) { ic += x; io += y; }
+    }
+    if (lane == 31) { s_w[warp][0] = ic; s_w[warp][1] = io; }
+    __syncthreads();
+    if (warp == 0) {
+        long long wc = s_w[lane][0], wo = s_w[lane][1];
+        long long xc = wc, xo = wo;
+        for (int d = 1; d < 32; d <<= 1) {
+            long long x = __shfl_up_sync(0xffffffffu, xc, d), y = __shfl_up_sync(0xffffffffu, xo, d);
+            if (lane >= d) { xc += x; xo += y; }
+        }
+        s_w[lane][0] = xc - wc;
+        s_w[lane][1] = xo - wo;
+        const long long aggc = __shfl_sync(0xffffffffu, xc, 31), aggo = __shfl_sync(0xffffffffu, xo, 31);
+        long long ec, eo;
+        seg_lookback(flags, t, aggc, aggo, ec, eo);
+        if (lane == 0) { s_base[0] = ec; s_base[1] = eo; }
+    }
+    __syncthreads();
+    long long pc = s_base[0] + s_w[warp][0] + ic - tc, po = s_base[1] + s_w[warp][1] + io - to;
+#pragma unroll
+    for (int k = 0; k < kScanPer; ++k) {
+        const long long i = i0 + k;
+        if (i <= S) {
+            if (a.do_ect) a.ect.off[i] = pc;
+            if (a.do_cls) a.cls.off[i] = pc;
+            if (a.do_ord) a.ord.off[i] = po;
+        }
+        pc += lc[k];
+        po += lo[k];
     }
 }
 
@@ -315,6 +520,7 @@ __global__ void __launch_bounds__(kBlockThreads, 1) k2_block(K2Args a, long long
     __shared__ long long s_exc[2];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     constexpr int words = PACK ? 1 : 2;
+    const OutPtrs<OutT> outp(a);
     Hist<PACK> hs;
     hs.c = hist;
     hs.j = hist + win;
@@ -398,7 +604,7 @@ __global__ void __launch_bounds__(kBlockThreads, 1) k2_block(K2Args a, long long
                 s_wsum[warp][3] = sj;
             }
             __syncthreads();
-            long long pc = pc_carry, po = po_carry;
+            int pc = (int)pc_carry, po = (int)po_carry;
             int er = e_carry, rr = r_carry;
             long long tc = 0, to = 0;
             int tsc = 0, tsj = 0;
@@ -414,7 +620,8 @@ __global__ void __launch_bounds__(kBlockThreads, 1) k2_block(K2Args a, long long
                 tsc += s_wsum[k][2];
                 tsj += s_wsum[k][3];
             }
-            for (int base = b0; base < b1; base += kGroup) emit_group<OutT>(a, hs, base, di.hlo + lo, er, rr, pc, po);
+            for (int base = b0; base < b1; base += kGroup)
+                emit_group<kModeAny>(outp, hs, base, di.hlo + lo, er, rr, pc, po);
             pc_carry += tc;
             po_carry += to;
             e_carry += tsc;
@@ -433,17 +640,35 @@ cudaError_t launch_t(const K2Args &a, cudaStream_t s, int num_sms) {
     const size_t per_warp = (size_t)rcap * 4 * words;
     int warps = (int)std::min<size_t>(8, (200 * 1024) / per_warp);
     if (warps >= 2 && a.max_count <= 32768) {
-        const int ndblk = (int)((a.D + warps - 1) / warps);
-        const long long nblk = a.batch * ndblk;
+        const int threads = warps * 32;
         const size_t smem = per_warp * warps;
-        auto kern = k2_warp<RecT, OutT, PACK>;
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        auto kc = k2w_count<RecT, PACK>;
+        void (*ke)(K2Args, int) = k2w_emit<RecT, OutT, PACK, kModeAny>;
+        if (std::is_same<RecT, Rec16>::value) {
+            const int mode = (a.do_ect ? kEct : 0) | (a.do_ord ? kOrd : 0) | (a.do_cls ? kCls : 0) |
+                             (a.do_cls && a.cls_alias ? kAlias : 0);
+            switch (mode) {
+            case kEct: ke = k2w_emit<RecT, OutT, PACK, kEct>; break;
+            case kOrd | kCls: ke = k2w_emit<RecT, OutT, PACK, kOrd | kCls>; break;
+            case kEct | kOrd | kCls: ke = k2w_emit<RecT, OutT, PACK, kEct | kOrd | kCls>; break;
+            case kEct | kOrd | kCls | kAlias: ke = k2w_emit<RecT, OutT, PACK, kEct | kOrd | kCls | kAlias>; break;
+            default: break;
+            }
+        }
+        cudaError_t e = cudaFuncSetAttribute(kc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e == cudaSuccess) e = cudaFuncSetAttribute(ke, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
         int occ = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kWarpThreads, smem);
-        long long grid = std::min<long long>(nblk, (long long)std::max(occ, 1) * num_sms);
-        kern<<<(unsigned)grid, kWarpThreads, smem, s>>>(a, rcap, warps, nblk, ndblk);
-        count_launch();
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kc, threads, smem);
+        const long long wblocks = (nseg + warps - 1) / warps;
+        const long long grid = std::min<long long>(wblocks, (long long)std::max(occ, 1) * num_sms);
+        kc<<<(unsigned)grid, threads, smem, s>>>(a, rcap, a.cnt_c, a.cnt_o);
+        const long long ntiles = (nseg + 1 + kScanTile - 1) / kScanTile;
+        k2_scan<<<(unsigned)ntiles, kScanThreads, 0, s>>>(a, a.cnt_c, a.cnt_o, nseg, a.flags);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, ke, threads, smem);
+        const long long grid2 = std::min<long long>(wblocks, (long long)std::max(occ, 1) * num_sms);
+        ke<<<(unsigned)grid2, threads, smem, s>>>(a, rcap);
+        count_launch(3);
         return cudaGetLastError();
     }
     const int win = (int)(kBlockSmem / (4 * words)) / kGroup * kGroup;

@@ -86,7 +86,7 @@ __global__ void __launch_bounds__(kThreads) k3_f32(K3Args a) {
     for (int s0 = beg; s0 < end; s0 += kStage) {
         const int cnt = min(kStage, end - s0);
         __syncthreads();
-        for (int i = threadIdx.x; i < cnt; i += kThreads) {
+        for (int i = threadIdx.x; i < cnt; i += blockDim.x) {
             const RecT r = list[s0 + i];
             int p0, p1, p2;
             rec_coords(r, a, p0, p1, p2);
@@ -166,7 +166,7 @@ __global__ void __launch_bounds__(kThreads) k3_f64(K3Args a) {
     for (int s0 = beg; s0 < end; s0 += kStage) {
         const int cnt = min(kStage, end - s0);
         __syncthreads();
-        for (int i = threadIdx.x; i < cnt; i += kThreads) {
+        for (int i = threadIdx.x; i < cnt; i += blockDim.x) {
             const RecT r = list[s0 + i];
             int p0, p1, p2;
             rec_coords(r, a, p0, p1, p2);
@@ -221,11 +221,11 @@ int k3_chunk() { return kChunk; }
 cudaError_t launch_k3(const K3Args &a, cudaStream_t s) {
     dim3 grid((unsigned)a.nchunks, (unsigned)a.ntiles, (unsigned)a.batch);
     if (a.precision == EUCALC_F32) {
-        if (a.wide) k3_f32<Rec32><<<grid, kThreads, 0, s>>>(a);
-        else k3_f32<Rec16><<<grid, kThreads, 0, s>>>(a);
+        if (a.wide) k3_f32<Rec32><<<grid, a.threads, 0, s>>>(a);
+        else k3_f32<Rec16><<<grid, a.threads, 0, s>>>(a);
     } else {
-        if (a.wide) k3_f64<Rec32><<<grid, kThreads, 0, s>>>(a);
-        else k3_f64<Rec16><<<grid, kThreads, 0, s>>>(a);
+        if (a.wide) k3_f64<Rec32><<<grid, a.threads, 0, s>>>(a);
+        else k3_f64<Rec16><<<grid, a.threads, 0, s>>>(a);
     }
     count_launch();
     cudaError_t e = cudaGetLastError();
