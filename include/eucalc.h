@@ -155,6 +155,40 @@ eucalc_status eucalc_radon(const eucalc_critical *cr, const int32_t *dirs, int64
 eucalc_status eucalc_hybrid(const eucalc_critical *cr, const int32_t *dirs, int64_t D, int kernel,
                             double param, int precision, void *out, void *stream);
 
+/* ---- evaluation and vectorisation (P:135-137 evaluation, P:339-341 vectorisation) ----
+ * Values of exact representations at real heights t, given in the paper's
+ * normalised units (vertices evenly spaced in [-0.5,0.5]^n):
+ *   kind EUCALC_EVAL_ECT  : ECT(xi,t) = E at the last breakpoint with height <= t,
+ *                           0 before the first;
+ *   kind EUCALC_EVAL_RADON: Radon(xi,t) = E_c if t equals a classical height
+ *                           (P:137), else E' at the last ordinary breakpoint
+ *                           strictly below t (E7), 0 before the first.
+ * Every comparison t(H) <= t / < t / == t is decided exactly (t is mapped to
+ * lattice units with an error-free product, E20), so the results are
+ * those of the definitions at the double t. t = +-inf is allowed; a NaN query
+ * yields 0.
+ * cx, dirs, D: the complex and the directions the representations were computed
+ *   for (segment s = image*D + direction, as produced by eucalc_transforms).
+ * rep: the ECT stream (ECT) or the ordinary Radon stream (T_o, E') (Radon);
+ * classical: the classical Radon stream (T_c, E_c) (Radon; NULL for ECT).
+ *   The classical height pointer may alias the ECT heights (T_c = T).
+ *   Host or device; elem_bytes 2, 4 or 8 (shared by rep and classical).
+ * eucalc_evaluate : queries t[nq] (host or device doubles), the same for every segment.
+ * eucalc_vectorize: the N evenly spaced points t_i = a + (i*(b-a))/(N-1),
+ *   i = 0..N-1 (t_0 = a when N = 1), computed in IEEE double round-to-nearest
+ *   in that order.
+ * out: [batch*D][nq or N] int32 or int64 (out_elem_bytes 4 or 8; 4 requires
+ *   the representation's elem_bytes <= 4), host or device, caller-owned.
+ * Asynchronous for device buffers; host buffers synchronise `stream`.
+ * Errors: E_ARG (NULL/shape/elem_bytes/kind), E_NONGENERIC, E_NOMEM, E_CUDA. */
+enum { EUCALC_EVAL_ECT = 0, EUCALC_EVAL_RADON = 1 };
+eucalc_status eucalc_evaluate(const eucalc_complex *cx, const int32_t *dirs, int64_t D, int kind,
+                              const eucalc_steps *rep, const eucalc_steps *classical,
+                              const double *t, int64_t nq, void *out, int out_elem_bytes, void *stream);
+eucalc_status eucalc_vectorize(const eucalc_complex *cx, const int32_t *dirs, int64_t D, int kind,
+                               const eucalc_steps *rep, const eucalc_steps *classical,
+                               double a, double b, int64_t N, void *out, int out_elem_bytes, void *stream);
+
 /* ---- helpers ---- */
 /* L and csum of the height map t = (2H - L*csum)/(2L) for direction dir (host, [ndim]). */
 eucalc_status eucalc_height_map(const eucalc_complex *cx, const int32_t *dir, int64_t *L, int64_t *csum);

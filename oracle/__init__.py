@@ -20,6 +20,7 @@ import math
 import os
 import subprocess
 import threading
+from fractions import Fraction
 from concurrent.futures import ThreadPoolExecutor
 
 import numpy as np
@@ -165,6 +166,45 @@ class Grid:
         return dict(T=bufs[0][:a].copy(), E=bufs[1][:a].copy(),
                     To=bufs[2][:b].copy(), Eo=bufs[3][:b].copy(),
                     Tc=bufs[4][:c].copy(), Ec=bufs[5][:c].copy())
+
+    # -- evaluation at real t straight from the definitions
+    def _t2(self, xi, t):
+        """The query t (a Python float = IEEE double, taken exactly) in doubled
+        lattice units: t2 = 2H with t = H/L - csum/2 (E10), i.e. t2 = 2Lt + L*csum,
+        an exact rational."""
+        return Fraction(t) * (2 * self.L) + self.L * self.csum(xi)
+
+    def ect_eval(self, xi, t) -> int:
+        """ECT(xi, t) = chi[phi_{xi <= t}] at real t: every cell with
+        2 max_P <= t2 counts, i.e. 2 max_P <= floor(t2) (max_P is a lattice height)."""
+        if math.isinf(t):
+            return 0 if t < 0 else self.euler()
+        return self.ect_at(xi, math.floor(self._t2(xi, t)))
+
+    def radon_eval(self, xi, t) -> int:
+        """Radon(xi, t) = chi[phi_{xi = t}] at real t. An integer t2 is
+        probed as is; a non-integer t2 lies strictly between two doubled lattice
+        heights (even numbers) and is replaced by the odd integer of its unit
+        interval, which satisfies the same strict comparisons against even values."""
+        if math.isinf(t):
+            return 0
+        t2 = self._t2(xi, t)
+        if t2.denominator == 1:
+            return self.radon_at(xi, int(t2))
+        k = math.floor(t2)
+        return self.radon_at(xi, k if k % 2 else k + 1)
+
+    @staticmethod
+    def sample_points(a: float, b: float, N: int):
+        """The vectorisation grid t_i = a + i(b-a)/(N-1), i = 0..N-1,
+        evaluated in IEEE double in the order (i*(b-a))/(N-1) then a + . (E20)."""
+        if N == 1:
+            return [float(a)]
+        return [float(a) + (i * (float(b) - float(a))) / (N - 1) for i in range(N)]
+
+    def vectorize(self, xi, a: float, b: float, N: int, kind: str = "ect"):
+        f = self.ect_eval if kind == "ect" else self.radon_eval
+        return np.array([f(xi, t) for t in self.sample_points(a, b, N)], dtype=np.int64)
 
     def ht_quad(self, xi, kernel: str, param: float = 1.0, nsub: int = 1) -> float:
         return float(_get().eo_ht_quad(_p(self.cells), self.n, _p(self.d), _p(self.xs(xi)), self.L,

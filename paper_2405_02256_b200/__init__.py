@@ -63,6 +63,8 @@ def lib():
         L.eucalc_ect.argtypes = [P, P, I64, SP, ctypes.POINTER(I64), P]
         L.eucalc_radon.argtypes = [P, P, I64, SP, SP, ctypes.POINTER(I64), P]
         L.eucalc_hybrid.argtypes = [P, P, I64, I32, ctypes.c_double, I32, P, P]
+        L.eucalc_evaluate.argtypes = [P, P, I64, I32, SP, SP, P, I64, P, I32, P]
+        L.eucalc_vectorize.argtypes = [P, P, I64, I32, SP, SP, ctypes.c_double, ctypes.c_double, I64, P, I32, P]
         L.eucalc_height_map.argtypes = [P, P, ctypes.POINTER(I64), ctypes.POINTER(I64)]
         L.eucalc_profile_enable.argtypes = [I32]
         L.eucalc_profile_enable.restype = None
@@ -75,7 +77,7 @@ def lib():
         for f in ("eucalc_build_complex", "eucalc_destroy_complex", "eucalc_critical_points",
                   "eucalc_destroy_critical", "eucalc_critical_counts", "eucalc_critical_export",
                   "eucalc_output_bound", "eucalc_transforms", "eucalc_ect", "eucalc_radon",
-                  "eucalc_hybrid", "eucalc_height_map"):
+                  "eucalc_hybrid", "eucalc_height_map", "eucalc_evaluate", "eucalc_vectorize"):
             getattr(L, f).restype = St
         _lib = L
     return _lib
@@ -291,6 +293,53 @@ def hybrid(cr: Critical, dirs, kernel="gauss", param=1.0, precision="f64", devic
     _check(lib().eucalc_hybrid(cr._h, p, D, KERNELS[kernel], float(param), PRECISIONS[precision],
                                ctypes.c_void_p(out.data_ptr()),
                                _stream(stream if stream is not None else cr.stream)))
+    return out
+
+
+def _steps_struct(st):
+    """ctypes eucalc_steps of a CSR dict returned by transforms()."""
+    h, v = st["height"], st["value"]
+    return _Steps(st["offsets"].data_ptr(), h.data_ptr(), v.data_ptr(), int(v.numel()), int(v.element_size()), 0)
+
+
+def evaluate(cx: Complex, dirs, t, ect=None, ordinary=None, classical=None, out_elem_bytes=8, device="cuda",
+             stream=None):
+    """eucalc_evaluate: ECT(xi,t) (pass ect=) or Radon(xi,t) (pass ordinary= and
+    classical=) at the queries t (paper units) for every (image, direction)
+    segment; returns [batch*D, len(t)]."""
+    return _eval(cx, dirs, ect, ordinary, classical, out_elem_bytes, device, stream, t=t)
+
+
+def vectorize(cx: Complex, dirs, a, b, N, ect=None, ordinary=None, classical=None, out_elem_bytes=8,
+              device="cuda", stream=None):
+    """eucalc_vectorize: values at t_i = a + (i*(b-a))/(N-1), i < N."""
+    return _eval(cx, dirs, ect, ordinary, classical, out_elem_bytes, device, stream, ab=(a, b, N))
+
+
+def _eval(cx, dirs, ect, ordinary, classical, out_elem_bytes, device, stream, t=None, ab=None):
+    import torch
+
+    d = _dirs_i32(dirs)
+    D = int(d.shape[0])
+    if ect is not None:
+        kind, rep, cls = 0, _steps_struct(ect), None
+    else:
+        kind, rep, cls = 1, _steps_struct(ordinary), _steps_struct(classical)
+    nq = len(t) if t is not None else int(ab[2])
+    pin = device == "cpu" and torch.cuda.is_available()
+    out = torch.empty((cx.batch * D, nq), dtype=torch.int32 if out_elem_bytes == 4 else torch.int64,
+                      device=device, pin_memory=pin)
+    p, keep = _ptr(d)
+    st = _stream(stream if stream is not None else cx.stream)
+    if t is not None:
+        tq = t if hasattr(t, "data_ptr") else np.ascontiguousarray(np.asarray(t, dtype=np.float64))
+        tp, keep_t = _ptr(tq)
+        _check(lib().eucalc_evaluate(cx._h, p, D, kind, ctypes.byref(rep), ctypes.byref(cls) if cls else None,
+                                     tp, nq, ctypes.c_void_p(out.data_ptr()), out_elem_bytes, st))
+    else:
+        _check(lib().eucalc_vectorize(cx._h, p, D, kind, ctypes.byref(rep), ctypes.byref(cls) if cls else None,
+                                      float(ab[0]), float(ab[1]), nq, ctypes.c_void_p(out.data_ptr()),
+                                      out_elem_bytes, st))
     return out
 
 

@@ -983,6 +983,130 @@ eucalc_status eucalc_hybrid(const eucalc_critical *ccr, const int32_t *dirs, int
     return EUCALC_OK;
 }
 
+}  // extern "C"
+
+namespace {
+
+// Shared body of eucalc_evaluate / eucalc_vectorize (K4).
+eucalc_status eval_common(const eucalc_complex *cx, const int32_t *dirs, int64_t D, int kind, const eucalc_steps *rep,
+                          const eucalc_steps *cls, const double *t, double ta, double tb, int64_t nq, void *out,
+                          int out_eb, void *stream) {
+    if (!cx || !cx->d_img) return fail(EUCALC_E_STATE, "invalid complex");
+    if (kind != EUCALC_EVAL_ECT && kind != EUCALC_EVAL_RADON) return fail(EUCALC_E_ARG, "bad kind");
+    if (!rep || !rep->offsets || !rep->height || !rep->value) return fail(EUCALC_E_ARG, "NULL representation");
+    if (kind == EUCALC_EVAL_RADON && (!cls || !cls->offsets || !cls->height || !cls->value))
+        return fail(EUCALC_E_ARG, "Radon evaluation needs the classical stream");
+    const int in_eb = rep->elem_bytes;
+    if (in_eb != 2 && in_eb != 4 && in_eb != 8) return fail(EUCALC_E_ARG, "elem_bytes must be 2, 4 or 8");
+    if (kind == EUCALC_EVAL_RADON && cls->elem_bytes != in_eb) return fail(EUCALC_E_ARG, "rep/classical elem_bytes differ");
+    if (out_eb != 4 && out_eb != 8) return fail(EUCALC_E_ARG, "out_elem_bytes must be 4 or 8");
+    if (out_eb == 4 && in_eb == 8) return fail(EUCALC_E_ARG, "int32 output of an int64 representation");
+    if (nq < 0) return fail(EUCALC_E_ARG, "negative query count");
+    if (nq > 0 && !out) return fail(EUCALC_E_ARG, "out is NULL");
+    if (t == nullptr && (ta != ta || tb != tb)) return fail(EUCALC_E_ARG, "NaN interval bound");
+    cudaStream_t st = (cudaStream_t)stream;
+    std::shared_ptr<PlanEntry> pe;
+    eucalc_status s = get_plan(cx, dirs, D, st, pe);
+    if (s != EUCALC_OK) return s;
+    const int64_t S = cx->batch * D;
+    if (S == 0 || nq == 0) return EUCALC_OK;
+    std::vector<void *> scratch;
+    auto dalloc = [&](size_t bytes) -> void * {
+        void *q = nullptr;
+        if (cudaMallocAsync(&q, std::max<size_t>(bytes, 1), st) != cudaSuccess) return nullptr;
+        scratch.push_back(q);
+        return q;
+    };
+    auto free_scratch = [&]() { for (void *q : scratch) cudaFreeAsync(q, st); };
+    // representations: device pointers used in place; host CSR staged to the device
+    struct Dev { const int64_t *off; const void *h, *v; };
+    auto stage = [&](const eucalc_steps *r, Dev &d) -> eucalc_status {
+        if (is_device_ptr(r->offsets)) {
+            d = Dev{r->offsets, r->height, r->value};
+            return EUCALC_OK;
+        }
+        const int64_t n = r->offsets[S] - r->offsets[0];
+        if (n < 0 || r->offsets[0] != 0) return fail(EUCALC_E_ARG, "bad host offsets");
+        void *o = dalloc(sizeof(int64_t) * (S + 1)), *h = dalloc(in_eb * n), *v = dalloc(in_eb * n);
+        if (!o || !h || !v) return fail(EUCALC_E_NOMEM, "evaluation staging");
+        cudaError_t e = cudaMemcpyAsync(o, r->offsets, sizeof(int64_t) * (S + 1), cudaMemcpyHostToDevice, st);
+        if (e == cudaSuccess && n) e = cudaMemcpyAsync(h, r->height, in_eb * n, cudaMemcpyHostToDevice, st);
+        if (e == cudaSuccess && n) e = cudaMemcpyAsync(v, r->value, in_eb * n, cudaMemcpyHostToDevice, st);
+        if (e != cudaSuccess) return cuda_fail(e, "evaluation staging");
+        d = Dev{(const int64_t *)o, h, v};
+        return EUCALC_OK;
+    };
+    Dev dr{}, dc{};
+    s = stage(rep, dr);
+    if (s == EUCALC_OK && kind == EUCALC_EVAL_RADON) s = stage(cls, dc);
+    const double *d_t = t;
+    if (s == EUCALC_OK && t && !is_device_ptr(t)) {
+        double *q = (double *)dalloc(sizeof(double) * nq);
+        if (!q) s = fail(EUCALC_E_NOMEM, "query staging");
+        else if (cudaMemcpyAsync(q, t, sizeof(double) * nq, cudaMemcpyHostToDevice, st) != cudaSuccess)
+            s = fail(EUCALC_E_CUDA, "query staging");
+        d_t = q;
+    }
+    const bool host_out = !is_device_ptr(out);
+    void *d_out = out;
+    if (s == EUCALC_OK && host_out) {
+        d_out = dalloc((size_t)out_eb * S * nq);
+        if (!d_out) s = fail(EUCALC_E_NOMEM, "output staging");
+    }
+    if (s != EUCALC_OK) {
+        free_scratch();
+        cudaStreamSynchronize(st);
+        return s;
+    }
+    K4Args a{};
+    a.kind = kind;
+    a.rep_off = dr.off;
+    a.rep_h = dr.h;
+    a.rep_v = dr.v;
+    a.cls_off = dc.off;
+    a.cls_h = dc.h;
+    a.cls_v = dc.v;
+    a.in_eb = in_eb;
+    a.out_eb = out_eb;
+    a.L = cx->L;
+    a.csum = pe->d_csum;
+    a.D = D;
+    a.batch = cx->batch;
+    a.t = d_t;
+    a.ta = ta;
+    a.tb = tb;
+    a.nq = nq;
+    a.out = d_out;
+    cudaError_t e;
+    {
+        ProfScope ps("k4_evaluate", st);
+        e = launch_k4(a, st, num_sms());
+    }
+    if (e == cudaSuccess && host_out) e = cudaMemcpyAsync(out, d_out, (size_t)out_eb * S * nq, cudaMemcpyDeviceToHost, st);
+    free_scratch();
+    if (e == cudaSuccess && host_out) e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) return cuda_fail(e, "evaluate");
+    return EUCALC_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+eucalc_status eucalc_evaluate(const eucalc_complex *cx, const int32_t *dirs, int64_t D, int kind,
+                              const eucalc_steps *rep, const eucalc_steps *classical, const double *t, int64_t nq,
+                              void *out, int out_elem_bytes, void *stream) {
+    if (nq > 0 && !t) return fail(EUCALC_E_ARG, "t is NULL");
+    return eval_common(cx, dirs, D, kind, rep, classical, t, 0.0, 0.0, nq, out, out_elem_bytes, stream);
+}
+
+eucalc_status eucalc_vectorize(const eucalc_complex *cx, const int32_t *dirs, int64_t D, int kind,
+                               const eucalc_steps *rep, const eucalc_steps *classical, double a, double b, int64_t N,
+                               void *out, int out_elem_bytes, void *stream) {
+    if (N < 0) return fail(EUCALC_E_ARG, "N < 0");
+    return eval_common(cx, dirs, D, kind, rep, classical, nullptr, a, b, N, out, out_elem_bytes, stream);
+}
+
 eucalc_status eucalc_height_map(const eucalc_complex *cx, const int32_t *dir, int64_t *L, int64_t *csum) {
     if (!cx || !dir) return fail(EUCALC_E_ARG, "NULL argument");
     int64_t cs = 0;

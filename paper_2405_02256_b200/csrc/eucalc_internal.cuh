@@ -149,6 +149,24 @@ struct K3Args {
 };
 cudaError_t launch_k3(const K3Args &a, cudaStream_t s);
 
+// K4: evaluation / vectorisation (NEXT f1)
+struct K4Args {
+    int kind;                   // EUCALC_EVAL_ECT / EUCALC_EVAL_RADON
+    const int64_t *rep_off;     // [batch*D+1] ECT or ordinary Radon stream
+    const void *rep_h, *rep_v;
+    const int64_t *cls_off;     // classical Radon stream (Radon only)
+    const void *cls_h, *cls_v;
+    int in_eb, out_eb;
+    int64_t L;
+    const int32_t *csum;        // [D]
+    int64_t D, batch;
+    const double *t;            // [nq] queries, or NULL: t_i = ta + (i*(tb-ta))/(nq-1)
+    double ta, tb;
+    int64_t nq;
+    void *out;                  // [batch*D][nq]
+};
+cudaError_t launch_k4(const K4Args &a, cudaStream_t s, int num_sms);
+
 // thread-local launch counter (eucalc_launch_count)
 void count_launch(int n = 1);
 
