@@ -155,6 +155,19 @@ eucalc_status eucalc_radon(const eucalc_critical *cr, const int32_t *dirs, int64
 eucalc_status eucalc_hybrid(const eucalc_critical *cr, const int32_t *dirs, int64_t D, int kernel,
                             double param, int precision, void *out, void *stream);
 
+/* eucalc_hybrid with an explicit algorithm (eucalc_hybrid = EUCALC_HT_AUTO):
+ *   EUCALC_HT_DIRECT: kbar evaluated per (ordinary point, direction) term;
+ *   EUCALC_HT_TABLE : kbar depends on a term only through the integer
+ *     u = 2H - L*csum (E10), so it is evaluated once per u in fp64 and looked up
+ *     (same values as DIRECT up to the final rounding of kbar to the output
+ *     precision). Needs packed byte-aligned coordinates (extents <= 65536 in
+ *     2-D, <= 256 in 3-D), axis-scaled |xs_i| <= 127 and a u-range whose half
+ *     table fits shared memory, else E_ARG;
+ *   EUCALC_HT_AUTO  : TABLE when it applies, else DIRECT. */
+enum { EUCALC_HT_AUTO = 0, EUCALC_HT_DIRECT = 1, EUCALC_HT_TABLE = 2 };
+eucalc_status eucalc_hybrid_ex(const eucalc_critical *cr, const int32_t *dirs, int64_t D, int kernel,
+                               double param, int precision, int algorithm, void *out, void *stream);
+
 /* ---- evaluation and vectorisation (P:135-137 evaluation, P:339-341 vectorisation) ----
  * Values of exact representations at real heights t, given in the paper's
  * normalised units (vertices evenly spaced in [-0.5,0.5]^n):

@@ -172,7 +172,11 @@ class Grid:
         """The query t (a Python float = IEEE double, taken exactly) in doubled
         lattice units: t2 = 2H with t = H/L - csum/2 (E10), i.e. t2 = 2Lt + L*csum,
         an exact rational."""
-        return Fraction(t) * (2 * self.L) + self.L * self.csum(xi)
+        t2 = Fraction(t) * (2 * self.L) + self.L * self.csum(xi)
+        # every cell height lies in [lo, hi]: thresholds beyond change nothing, and
+        # clamping keeps the doubled threshold inside the C oracle's int64
+        lo, hi = self.height_range(xi)
+        return min(max(t2, Fraction(2 * lo - 3)), Fraction(2 * hi + 3))
 
     def ect_eval(self, xi, t) -> int:
         """ECT(xi, t) = chi[phi_{xi <= t}] at real t: every cell with

@@ -63,6 +63,7 @@ def lib():
         L.eucalc_ect.argtypes = [P, P, I64, SP, ctypes.POINTER(I64), P]
         L.eucalc_radon.argtypes = [P, P, I64, SP, SP, ctypes.POINTER(I64), P]
         L.eucalc_hybrid.argtypes = [P, P, I64, I32, ctypes.c_double, I32, P, P]
+        L.eucalc_hybrid_ex.argtypes = [P, P, I64, I32, ctypes.c_double, I32, I32, P, P]
         L.eucalc_evaluate.argtypes = [P, P, I64, I32, SP, SP, P, I64, P, I32, P]
         L.eucalc_vectorize.argtypes = [P, P, I64, I32, SP, SP, ctypes.c_double, ctypes.c_double, I64, P, I32, P]
         L.eucalc_height_map.argtypes = [P, P, ctypes.POINTER(I64), ctypes.POINTER(I64)]
@@ -77,7 +78,8 @@ def lib():
         for f in ("eucalc_build_complex", "eucalc_destroy_complex", "eucalc_critical_points",
                   "eucalc_destroy_critical", "eucalc_critical_counts", "eucalc_critical_export",
                   "eucalc_output_bound", "eucalc_transforms", "eucalc_ect", "eucalc_radon",
-                  "eucalc_hybrid", "eucalc_height_map", "eucalc_evaluate", "eucalc_vectorize"):
+                  "eucalc_hybrid", "eucalc_hybrid_ex", "eucalc_height_map", "eucalc_evaluate",
+                  "eucalc_vectorize"):
             getattr(L, f).restype = St
         _lib = L
     return _lib
@@ -280,8 +282,13 @@ def radon(cr: Critical, dirs, **kw):
     return r["ordinary"], r["classical"]
 
 
-def hybrid(cr: Critical, dirs, kernel="gauss", param=1.0, precision="f64", device="cuda", stream=None):
-    """eucalc_hybrid: HT(xi) = int kappa(t) Radon(xi,t) dt for every (image, direction)."""
+HT_ALGORITHMS = {"auto": 0, "direct": 1, "table": 2}
+
+
+def hybrid(cr: Critical, dirs, kernel="gauss", param=1.0, precision="f64", device="cuda", stream=None,
+           algorithm="auto"):
+    """eucalc_hybrid_ex: HT(xi) = int kappa(t) Radon(xi,t) dt for every (image, direction).
+    algorithm: "auto", "direct" (kbar per term) or "table" (kbar tabulated per lattice u)."""
     import torch
 
     d = _dirs_i32(dirs)
@@ -290,8 +297,8 @@ def hybrid(cr: Critical, dirs, kernel="gauss", param=1.0, precision="f64", devic
     pin = device == "cpu" and torch.cuda.is_available()
     out = torch.empty((cr.cx.batch, D), dtype=dt, device=device, pin_memory=pin)
     p, keep = _ptr(d)
-    _check(lib().eucalc_hybrid(cr._h, p, D, KERNELS[kernel], float(param), PRECISIONS[precision],
-                               ctypes.c_void_p(out.data_ptr()),
+    _check(lib().eucalc_hybrid_ex(cr._h, p, D, KERNELS[kernel], float(param), PRECISIONS[precision],
+                                  HT_ALGORITHMS[algorithm], ctypes.c_void_p(out.data_ptr()),
                                _stream(stream if stream is not None else cr.stream)))
     return out
 

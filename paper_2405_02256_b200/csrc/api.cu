@@ -99,6 +99,26 @@ int num_sms() {
     return n;
 }
 
+// Keep freed stream-ordered allocations in the device's default pool (the
+// default release threshold of 0 returns them to the driver at every
+// synchronisation, so each later cudaMallocAsync became a full allocation:
+// ~1 ms per call measured on the bench step).
+void keep_pool() {
+    static std::mutex mu;
+    static bool done[64] = {};
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return;
+    std::lock_guard<std::mutex> lk(mu);
+    if (done[dev]) return;
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+        uint64_t thr = UINT64_MAX;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    cudaGetLastError();
+    done[dev] = true;
+}
+
 int bits_for(int64_t v) {  // bits to hold 0..v
     int b = 1;
     while ((int64_t(1) << b) <= v) ++b;
@@ -127,6 +147,7 @@ struct DirPlan {
     std::vector<int> orthant;
     int R_max = 0;
     int dp = 0;  // all directions fit int8 and the complex is byte-aligned
+    int64_t U0 = 0, U1 = 0;  // range of u = 2H - L*csum over all directions (K3 kbar table)
 };
 
 eucalc_status plan_dirs(const Complex *cx, const int32_t *dirs, int64_t D, cudaStream_t st, DirPlan &p) {
@@ -176,6 +197,9 @@ eucalc_status plan_dirs(const Complex *cx, const int32_t *dirs, int64_t D, cudaS
         p.csum[d] = (int32_t)cs;
         p.orthant[d] = e;
         p.R_max = std::max(p.R_max, di.R);
+        const int64_t Lc = cx->L * cs, ulo = 2 * lo - Lc, uhi = 2 * hi - Lc;
+        p.U0 = d == 0 ? ulo : std::min(p.U0, ulo);
+        p.U1 = d == 0 ? uhi : std::max(p.U1, uhi);
         bool fits8 = true;
         uint32_t x8 = 0;
         for (int k = 0; k < n; ++k) {
@@ -254,11 +278,13 @@ eucalc_status get_plan(const Complex *cx, const int32_t *dirs, int64_t D, cudaSt
     // HT tiles: directions grouped by orthant (Lemma 3), <= 256 per tile
     e->order.resize(D);
     std::iota(e->order.begin(), e->order.end(), 0);
-    std::stable_sort(e->order.begin(), e->order.end(),
-                     [&](int32_t x, int32_t y) { return e->p.orthant[x] < e->p.orthant[y]; });
+    // tile key: orthant (same critical list, Lemma 3) and the parity of L*csum
+    // (the parity of u = 2H - L*csum, which selects one half of K3's kbar table)
+    auto key = [&](int32_t d) { return e->p.orthant[d] * 2 + (int)((cx->L * (int64_t)e->p.csum[d]) & 1); };
+    std::stable_sort(e->order.begin(), e->order.end(), [&](int32_t x, int32_t y) { return key(x) < key(y); });
     for (int64_t i = 0; i < D;) {
         int64_t j = i;
-        while (j < D && e->p.orthant[e->order[j]] == e->p.orthant[e->order[i]] && j - i < 256) ++j;
+        while (j < D && key(e->order[j]) == key(e->order[i]) && j - i < 256) ++j;
         e->tstart.push_back((int32_t)i);
         e->tlen.push_back((int32_t)(j - i));
         i = j;
@@ -452,6 +478,7 @@ eucalc_status eucalc_build_complex(const void *img, int dtype, int ndim, const i
     if (batch < 1) return fail(EUCALC_E_ARG, "batch < 1");
     if (construction != EUCALC_VERTEX && construction != EUCALC_TOP) return fail(EUCALC_E_ARG, "bad construction");
     cudaStream_t st = (cudaStream_t)stream;
+    keep_pool();
     eucalc_complex *cx = new (std::nothrow) eucalc_complex();
     if (!cx) return fail(EUCALC_E_NOMEM, "host alloc");
     cx->ndim = ndim;
@@ -570,18 +597,39 @@ eucalc_status eucalc_critical_points(const eucalc_complex *cx, void *stream, euc
     const size_t rsz = cr->wide ? sizeof(Rec32) : sizeof(Rec16);
     const int64_t nlist = cx->batch * cr->Q;
     const int64_t nstats = cx->batch * (1 << n) * 2 + 2 * nlist;
-    // tile shape: full rows when they fit (row-major list order)
+    // tile shape: the whole image when it fits one tile (list order = row-major
+    // vertex order), else boxes of <= TV vertices (64 x 32 in 2-D, 16 x 16 x 8 in
+    // 3-D) spanning narrow height bands, for K2's tile culling
     const int TV = k1_tile_vertices();
-    const int MX = (int)cx->M[n - 1], MY = (int)cx->M[n - 2];
-    int TX = std::min(MX, TV);
-    int TY = std::max(1, std::min(MY, TV / TX));
+    const int MX = (int)cx->M[n - 1], MY = (int)cx->M[n - 2], MZ = n == 3 ? (int)cx->M[0] : 1;
+    int TX, TY, TZ = 1;
+    if ((int64_t)MX * MY * MZ <= TV) {
+        TX = MX;
+        TY = MY;
+        TZ = MZ;
+    } else if (n == 2) {
+        TX = std::min(MX, 64);
+        TY = std::max(1, std::min(MY, TV / TX));
+    } else {
+        TX = std::min(MX, 16);
+        TY = std::min(MY, 16);
+        TZ = std::max(1, std::min(MZ, TV / (TX * TY)));
+    }
     const int tiles_x = (MX + TX - 1) / TX, tiles_y = (MY + TY - 1) / TY;
-    const int tiles_z = n == 3 ? (int)cx->M[0] : 1;
+    const int tiles_z = n == 3 ? (MZ + TZ - 1) / TZ : 1;
+    cr->TX = TX;
+    cr->TY = TY;
+    cr->TZ = TZ;
+    cr->tiles_x = tiles_x;
+    cr->tiles_y = tiles_y;
+    cr->tiles_z = tiles_z;
+    cr->ntiles = tiles_x * tiles_y * tiles_z;
     const int64_t ntiles = cx->batch * (int64_t)tiles_x * tiles_y * tiles_z;
     unsigned long long *flags = nullptr;
     unsigned int *ticket = nullptr;
     cudaError_t e = cudaMallocAsync(&cr->d_rec, rsz * nlist * cr->vcap, st);
     if (e == cudaSuccess) e = cudaMallocAsync(&cr->d_count, sizeof(int32_t) * nlist, st);
+    if (e == cudaSuccess) e = cudaMallocAsync(&cr->d_tile_off, sizeof(int32_t) * nlist * (cr->ntiles + 1), st);
     if (e == cudaSuccess) e = cudaMallocAsync(&cr->d_stats, sizeof(int64_t) * nstats, st);
     if (e == cudaSuccess) e = cudaMallocAsync(&flags, sizeof(unsigned long long) * ntiles * cr->Q, st);
     if (e == cudaSuccess) e = cudaMallocAsync(&ticket, sizeof(unsigned int), st);
@@ -604,6 +652,8 @@ eucalc_status eucalc_critical_points(const eucalc_complex *cx, void *stream, euc
         }
         a.TX = TX;
         a.TY = TY;
+        a.TZ = TZ;
+        a.tile_off = cr->d_tile_off;
         a.tiles_x = tiles_x;
         a.tiles_y = tiles_y;
         a.tiles_z = tiles_z;
@@ -638,6 +688,7 @@ eucalc_status eucalc_critical_points(const eucalc_complex *cx, void *stream, euc
     if (e != cudaSuccess) {
         if (cr->d_rec) cudaFreeAsync(cr->d_rec, st);
         if (cr->d_count) cudaFreeAsync(cr->d_count, st);
+        if (cr->d_tile_off) cudaFreeAsync(cr->d_tile_off, st);
         if (cr->d_stats) cudaFreeAsync(cr->d_stats, st);
         if (cr->k1_done) cudaEventDestroy(cr->k1_done);
         cudaStreamSynchronize(st);
@@ -653,6 +704,7 @@ eucalc_status eucalc_destroy_critical(eucalc_critical *cr) {
     if (!cr) return fail(EUCALC_E_STATE, "NULL handle");
     cudaFreeAsync(cr->d_rec, cr->owner_stream);
     cudaFreeAsync(cr->d_count, cr->owner_stream);
+    cudaFreeAsync(cr->d_tile_off, cr->owner_stream);
     cudaFreeAsync(cr->d_stats, cr->owner_stream);
     if (cr->k1_done) {
         cudaEventSynchronize(cr->k1_done);  // the read-back into `pinned` has landed
@@ -846,6 +898,14 @@ eucalc_status eucalc_transforms(const eucalc_critical *ccr, const int32_t *dirs,
             a.msk[k] = cx->msk[k];
         }
         a.dirs = d_info;
+        a.tile_off = cr->d_tile_off;
+        a.ntiles = cr->ntiles;
+        a.tiles_x = cr->tiles_x;
+        a.tiles_y = cr->tiles_y;
+        a.TX = cr->TX;
+        a.TY = cr->TY;
+        a.TZ = cr->TZ;
+        for (int k = 0; k < cx->ndim; ++k) a.M[k] = (int)cx->M[k];
         a.D = D;
         a.batch = cx->batch;
         a.R_max = p.R_max;
@@ -906,7 +966,13 @@ eucalc_status eucalc_radon(const eucalc_critical *cr, const int32_t *dirs, int64
 
 eucalc_status eucalc_hybrid(const eucalc_critical *ccr, const int32_t *dirs, int64_t D, int kernel, double param,
                             int precision, void *out, void *stream) {
+    return eucalc_hybrid_ex(ccr, dirs, D, kernel, param, precision, EUCALC_HT_AUTO, out, stream);
+}
+
+eucalc_status eucalc_hybrid_ex(const eucalc_critical *ccr, const int32_t *dirs, int64_t D, int kernel, double param,
+                               int precision, int algorithm, void *out, void *stream) {
     if (!ccr) return fail(EUCALC_E_STATE, "NULL handle");
+    if (algorithm < EUCALC_HT_AUTO || algorithm > EUCALC_HT_TABLE) return fail(EUCALC_E_ARG, "bad algorithm");
     if (kernel < EUCALC_K_GAUSS || kernel > EUCALC_K_EXP) return fail(EUCALC_E_ARG, "bad kernel");
     if (precision != EUCALC_F32 && precision != EUCALC_F64) return fail(EUCALC_E_ARG, "bad precision");
     if ((kernel == EUCALC_K_GAUSS || kernel == EUCALC_K_COS) && !(param > 0)) return fail(EUCALC_E_ARG, "param must be > 0");
@@ -922,7 +988,15 @@ eucalc_status eucalc_hybrid(const eucalc_critical *ccr, const int32_t *dirs, int
     if (s != EUCALC_OK) return s;
     if (D == 0) return EUCALC_OK;
     const std::vector<int32_t> &tstart = pe->tstart;
-    const int chunk = k3_chunk();
+    // tabulated kbar when the packed-coordinate height (dp2a/dp4a) applies and the
+    // half table of one u-parity fits shared memory; else per-term evaluation
+    const int64_t U = p.U1 - p.U0 + 1;
+    const bool table_ok = p.dp != 0 && U < (int64_t(1) << 30) &&
+                          k3_table_smem(precision == EUCALC_F64, U) <= 200 * 1024;
+    if (algorithm == EUCALC_HT_TABLE && !table_ok)
+        return fail(EUCALC_E_ARG, "tabulated HT needs byte-aligned coordinates, |xs| <= 127 and a table that fits shared memory");
+    const bool use_table = algorithm == EUCALC_HT_TABLE || (algorithm == EUCALC_HT_AUTO && table_ok);
+    const int chunk = k3_chunk(use_table);
     const int nchunks = (int)std::max<int64_t>(1, (cr->max_count + chunk - 1) / chunk);
     const size_t osz = precision == EUCALC_F32 ? 4 : 8;
     const bool host_out = !is_device_ptr(out);
@@ -938,7 +1012,8 @@ eucalc_status eucalc_hybrid(const eucalc_critical *ccr, const int32_t *dirs, int
     const int32_t *d_order = pe->d_order, *d_ts = pe->d_ts, *d_tl = pe->d_tl, *d_cs = pe->d_csum;
     double *d_part = (double *)dalloc(sizeof(double) * cx->batch * nchunks * D);
     void *d_out = host_out ? dalloc(osz * cx->batch * D) : out;
-    if (!d_part || !d_out) {
+    void *d_tab = use_table ? dalloc(12 * (size_t)U) : nullptr;
+    if (!d_part || !d_out || (use_table && !d_tab)) {
         free_scratch();
         return fail(EUCALC_E_NOMEM, "scratch");
     }
@@ -973,6 +1048,11 @@ eucalc_status eucalc_hybrid(const eucalc_critical *ccr, const int32_t *dirs, int
         a.nchunks = nchunks;
         a.partial = d_part;
         a.out = d_out;
+        a.use_table = use_table ? 1 : 0;
+        a.U0 = p.U0;
+        a.U = U;
+        a.tab64 = (double *)d_tab;
+        a.tab32 = use_table ? (float *)((double *)d_tab + U) : nullptr;
         ProfScope ps("k3_hybrid", st);
         e = launch_k3(a, st);
     }

@@ -47,6 +47,8 @@ struct Critical {
     int64_t vcap = 0;   // records capacity per (image, pair) list = nvert
     void *d_rec = nullptr;       // [batch][Q][vcap]
     int32_t *d_count = nullptr;  // [batch][Q]
+    int32_t *d_tile_off = nullptr;  // [batch][Q][ntiles+1] (K1 tile -> list offset)
+    int TX = 1, TY = 1, TZ = 1, tiles_x = 1, tiles_y = 1, tiles_z = 1, ntiles = 1;
     int64_t *d_stats = nullptr;  // [batch][2^n][2] (N^-, N^ord), [batch][Q] sum(|a|+|b|), [batch][Q] max(|a|+|b|)
     // host cache (filled by sync_counts)
     bool have_host = false;
@@ -71,11 +73,12 @@ struct K1Args {
     int dtype, construction, ndim;
     int64_t batch, npix, vcap;
     int m[kMaxN], M[kMaxN];
-    int TX, TY, tiles_x, tiles_y, tiles_z;
+    int TX, TY, TZ, tiles_x, tiles_y, tiles_z;
     int sh[kMaxN];
     void *rec;
     bool wide;
     int32_t *count;
+    int32_t *tile_off;  // [batch][Q][ntiles+1] list offset of each tile (+ total)
     unsigned long long *flags;
     unsigned int *ticket;
     int64_t *stats;
@@ -117,6 +120,9 @@ struct K2Args {
     bool pack16;  // 16+16-bit packed histogram bins are exact (host-checked)
     bool do_ect, do_ord, do_cls, cls_alias;
     StepsOut ect, ord, cls;
+    const int32_t *tile_off;    // [batch][Q][ntiles+1] K1 tile -> list offset
+    int ntiles, tiles_x, tiles_y, TX, TY, TZ;
+    int M[kMaxN];               // vertex extents
     unsigned long long *flags;  // [batch*D] look-back flags (zeroed)
     unsigned int *ticket;       // [4] ticket counters (zeroed)
     int *cnt_c, *cnt_o;         // [batch*D] per-segment counts (warp regime)
@@ -146,7 +152,14 @@ struct K3Args {
     int nchunks;
     double *partial;           // [batch][nchunks][D]
     void *out;                 // [batch][D]
+    // tabulated kbar (use_table): u = 2H - L*csum in [U0, U0 + U)
+    int use_table;
+    int64_t U0, U;
+    double *tab64;
+    float *tab32;
 };
+int k3_chunk(bool table);
+size_t k3_table_smem(bool f64, long long U);
 cudaError_t launch_k3(const K3Args &a, cudaStream_t s);
 
 // K4: evaluation / vectorisation (NEXT f1)

@@ -24,7 +24,11 @@
 // give the in-tile order; a decoupled look-back over the image's tiles (dynamic
 // ticket order) gives each tile's global offset, so the list order is
 // deterministic (tile-major, row-major within a tile) with a single pass.
+// Tiles are boxes of <= kTileV vertices (the whole image when it fits; else
+// 64 x 32 in 2-D, 16 x 16 x 8 in 3-D), so a tile spans a narrow band of heights
+// in every direction; K1 records each tile's list offset for K2's culling.
 #include <climits>
+#include <type_traits>
 
 #include "eucalc_internal.cuh"
 
@@ -79,87 +83,97 @@ __device__ long long lookback(unsigned long long *flag_t, int t, int stride, lon
     return excl;
 }
 
+// Compile-time loop: f(std::integral_constant<int, I>) for I in [B, E). Every
+// index below is a constant expression, so the 3^n star values stay in
+// registers (a runtime-indexed array would live in local memory).
+template <int B, int E, typename F>
+__device__ __forceinline__ void static_for(F &&f) {
+    if constexpr (B < E) {
+        f(std::integral_constant<int, B>{});
+        static_for<B + 1, E>(f);
+    }
+}
+
+// digit k (axis k, 0 = slowest) of a base-3 star index, in {0,1,2} <-> offset {-1,0,+1}
+template <int N>
+__host__ __device__ constexpr int digit3(int idx, int k) { return (idx / pow3(N - 1 - k)) % 3; }
+
+// Does pixel corner c (bit k set <-> pixel index x_k, clear <-> x_k - 1) belong to
+// the top-cell cofaces of the star cell `idx` (TOP construction)?
+template <int N>
+__host__ __device__ constexpr bool top_coface(int idx, int c) {
+    for (int k = 0; k < N; ++k) {
+        const int o = digit3<N>(idx, k) - 1, cb = (c >> k) & 1;
+        if (o == -1 && cb != 0) return false;  // cell extends to x-1: pixel x-1 only
+        if (o == 1 && cb != 1) return false;   // cell extends to x+1: pixel x only
+    }
+    return true;
+}
+
 template <int N, int CONS>
 __device__ __forceinline__ void vertex_dminus(const int *s, int sz, int sy, int base, int (&dm)[1 << N]) {
     constexpr int P3 = pow3(N);
     int val[P3];
-    if (CONS == EUCALC_VERTEX) {
-        // point values of the 3^n neighbourhood, then separable box mins
-#pragma unroll
-        for (int idx = 0; idx < P3; ++idx) {
-            int off = 0, r = idx;
-#pragma unroll
-            for (int k = N - 1; k >= 0; --k) {
-                int o = r % 3 - 1;
-                r /= 3;
-                int stride = (k == N - 1) ? 1 : ((k == N - 2) ? sy : sz);
-                off += o * stride;
-            }
+    auto stride = [&](int k) { return (k == N - 1) ? 1 : ((k == N - 2) ? sy : sz); };
+    if constexpr (CONS == EUCALC_VERTEX) {
+        // point values of the 3^n neighbourhood, then separable box mins: after
+        // axis k, val[o] = min over the vertices of the cell spanned by x and x+o
+        static_for<0, P3>([&](auto I) {
+            constexpr int idx = decltype(I)::value;
+            int off = 0;
+            static_for<0, N>([&](auto K) { off += (digit3<N>(idx, decltype(K)::value) - 1) * stride(decltype(K)::value); });
             val[idx] = s[base + off];
-        }
-#pragma unroll
-        for (int k = 0; k < N; ++k) {
-            const int st = pow3(N - 1 - k);
-#pragma unroll
-            for (int idx = 0; idx < P3; ++idx) {
-                const int ok = (idx / st) % 3;
-                if (ok != 1) val[idx] = min(val[idx], val[idx + (1 - ok) * st]);
-            }
-        }
-#pragma unroll
-        for (int idx = 0; idx < P3; ++idx) val[idx] = (val[idx] == INT_MIN) ? 0 : val[idx];
+        });
+        static_for<0, N>([&](auto K) {
+            constexpr int k = decltype(K)::value, st = pow3(N - 1 - k);
+            static_for<0, P3>([&](auto I) {
+                constexpr int idx = decltype(I)::value, ok = digit3<N>(idx, k);
+                if constexpr (ok != 1) val[idx] = min(val[idx], val[idx + (1 - ok) * st]);
+            });
+        });
+        static_for<0, P3>([&](auto I) {
+            constexpr int idx = decltype(I)::value;
+            val[idx] = (val[idx] == INT_MIN) ? 0 : val[idx];
+        });
     } else {
         // 2^n pixels around the vertex (pixel x + c, c in {-1,0}^n); base <-> c = 0
         constexpr int P2 = 1 << N;
         int pix[P2];
-#pragma unroll
-        for (int c = 0; c < P2; ++c) {
+        static_for<0, P2>([&](auto C) {
+            constexpr int c = decltype(C)::value;
             int off = 0;
-#pragma unroll
-            for (int k = 0; k < N; ++k) {
-                int stride = (k == N - 1) ? 1 : ((k == N - 2) ? sy : sz);
-                if (!((c >> k) & 1)) off -= stride;  // bit 0 -> c_k = -1
-            }
+            static_for<0, N>([&](auto K) {
+                if constexpr (!((c >> decltype(K)::value) & 1)) off -= stride(decltype(K)::value);
+            });
             pix[c] = s[base + off];
-        }
-#pragma unroll
-        for (int idx = 0; idx < P3; ++idx) {
+        });
+        static_for<0, P3>([&](auto I) {
+            constexpr int idx = decltype(I)::value;
             int mval = INT_MAX;
-#pragma unroll
-            for (int c = 0; c < P2; ++c) {
-                bool ok = true;
-#pragma unroll
-                for (int k = 0; k < N; ++k) {
-                    const int o = (idx / pow3(N - 1 - k)) % 3 - 1;
-                    const int cb = (c >> k) & 1;
-                    if (o == -1 && cb != 0) ok = false;  // cell extends to x-1: pixel x-1 only
-                    if (o == 1 && cb != 1) ok = false;   // cell extends to x+1: pixel x only
-                }
-                if (ok) mval = min(mval, pix[c]);
-            }
+            static_for<0, P2>([&](auto C) {
+                if constexpr (top_coface<N>(idx, decltype(C)::value)) mval = min(mval, pix[decltype(C)::value]);
+            });
             val[idx] = (mval == INT_MAX) ? 0 : mval;
-        }
+        });
     }
     // inclusion-exclusion: along axis k, slot +1 <- z(0) - z(-1) (eps_k=+1), slot -1 <- z(0) - z(+1)
-#pragma unroll
-    for (int k = 0; k < N; ++k) {
-        const int st = pow3(N - 1 - k);
-#pragma unroll
-        for (int idx = 0; idx < P3; ++idx) {
-            if ((idx / st) % 3 == 1) {
+    static_for<0, N>([&](auto K) {
+        constexpr int k = decltype(K)::value, st = pow3(N - 1 - k);
+        static_for<0, P3>([&](auto I) {
+            constexpr int idx = decltype(I)::value;
+            if constexpr (digit3<N>(idx, k) == 1) {
                 const int a = val[idx - st], c = val[idx], b = val[idx + st];
                 val[idx + st] = c - a;
                 val[idx - st] = c - b;
             }
-        }
-    }
-#pragma unroll
-    for (int e = 0; e < (1 << N); ++e) {
-        int idx = 0;
-#pragma unroll
-        for (int k = 0; k < N; ++k) idx += (((e >> k) & 1) ? 2 : 0) * pow3(N - 1 - k);
+        });
+    });
+    static_for<0, (1 << N)>([&](auto E) {
+        constexpr int e = decltype(E)::value;
+        constexpr int idx = (((e >> 0) & 1) ? 2 * pow3(N - 1) : 0) + (N > 1 && ((e >> 1) & 1) ? 2 * pow3(N - 2) : 0) +
+                            (N > 2 && ((e >> 2) & 1) ? 2 * pow3(N - 3 < 0 ? 0 : N - 3) : 0);
         dm[e] = val[idx];
-    }
+    });
 }
 
 template <int N, int CONS, typename TIn, typename RecT>
@@ -186,35 +200,39 @@ __global__ void __launch_bounds__(kThreads) k1_kernel(K1Args a) {
     const int t = ticket % tiles_per_img;
     const int tx = t % a.tiles_x, ty = (t / a.tiles_x) % a.tiles_y, tz = t / (a.tiles_x * a.tiles_y);
 
-    // vertex-lattice extents along (z, y, x) view
+    // vertex-lattice extents along (z, y, x) view; a tile is a TZ x TY x TX box of vertices
     const int MX = a.M[N - 1];
     const int MY = (N >= 2) ? a.M[N - 2] : 1;
+    const int MZ = (N == 3) ? a.M[0] : 1;
     const int mX = a.m[N - 1];
     const int mY = (N >= 2) ? a.m[N - 2] : 1;
     const int mZ = (N == 3) ? a.m[0] : 1;
-    const int x0 = tx * a.TX, y0 = ty * a.TY, z = tz;
-    const int TXe = min(a.TX, MX - x0), TYe = min(a.TY, MY - y0);
-    const int RX = TXe + 2, RY = TYe + 2;
-    const int planes = (N == 3) ? 3 : 1;
+    const int x0 = tx * a.TX, y0 = ty * a.TY, z0 = tz * a.TZ;
+    const int TXe = min(a.TX, MX - x0), TYe = min(a.TY, MY - y0), TZe = (N == 3) ? min(a.TZ, MZ - z0) : 1;
+    const int RX = TXe + 2, RY = TYe + 2, RZ = (N == 3) ? TZe + 2 : 1;
 
-    // ---- stage input region rows y0-1 .. y0+TYe, cols x0-1 .. x0+TXe (image index = vertex idx for
-    // VERTEX, pixel idx for TOP), planes z-1..z+1
+    // ---- stage the input region (image index = vertex idx for VERTEX, pixel idx
+    // for TOP) with a one-voxel halo: planes z0-1 .. z0+TZe, rows y0-1 .. y0+TYe,
+    // cols x0-1 .. x0+TXe; one warp per region row, lanes along the row
     const TIn *img = reinterpret_cast<const TIn *>(a.img) + b * a.npix;
     const int SENT = (CONS == EUCALC_VERTEX) ? INT_MIN : INT_MAX;
-    const int nreg = planes * RY * RX;
-    for (int i = tid; i < nreg; i += kThreads) {
-        int rx = i % RX, ry = (i / RX) % RY, pz = i / (RX * RY);
-        int gx = x0 - 1 + rx, gy = y0 - 1 + ry, gz = z - 1 + pz;
-        if (N == 2) gz = 0;
-        bool in = gx >= 0 && gx < mX && gy >= 0 && gy < mY && gz >= 0 && gz < mZ;
-        int64_t gi = ((int64_t)gz * mY + gy) * mX + gx;
-        reg[i] = in ? load_img(img, gi) : SENT;
+    for (int row = warp; row < RZ * RY; row += kThreads / 32) {
+        const int pz = row / RY, ry = row - pz * RY;
+        const int gy = y0 - 1 + ry, gz = (N == 3) ? z0 - 1 + pz : 0;
+        const bool rin = gy >= 0 && gy < mY && gz >= 0 && gz < mZ;
+        const TIn *src = img + ((int64_t)gz * mY + gy) * mX;
+        int *dst = reg + row * RX;
+        for (int rx = lane; rx < RX; rx += 32) {
+            const int gx = x0 - 1 + rx;
+            dst[rx] = (rin && gx >= 0 && gx < mX) ? load_img(src, gx) : SENT;
+        }
     }
     __syncthreads();
 
     // ---- per vertex stencil + compaction into shared staging
     const int sy = RX, sz = RX * RY;
-    const int TV = TXe * TYe;
+    const int TP = TXe * TYe;
+    const int TV = TP * TZe;
     int cnt_o[1 << N][2];
 #pragma unroll
     for (int e = 0; e < (1 << N); ++e) cnt_o[e][0] = cnt_o[e][1] = 0;
@@ -230,11 +248,13 @@ __global__ void __launch_bounds__(kThreads) k1_kernel(K1Args a) {
         const int li = c0 + tid;
         const bool valid = li < TV;
         int dm[1 << N];
-        int ly = 0, lx = 0;
+        int lz = 0, ly = 0, lx = 0;
         if (valid) {
-            ly = li / TXe;
-            lx = li - ly * TXe;
-            const int base = ((N == 3) ? sz : 0) + (ly + 1) * sy + (lx + 1);
+            lz = li / TP;
+            const int r = li - lz * TP;
+            ly = r / TXe;
+            lx = r - ly * TXe;
+            const int base = ((N == 3) ? (lz + 1) * sz : 0) + (ly + 1) * sy + (lx + 1);
             vertex_dminus<N, CONS>(reg, sz, sy, base, dm);
         } else {
 #pragma unroll
@@ -250,7 +270,7 @@ __global__ void __launch_bounds__(kThreads) k1_kernel(K1Args a) {
             const int gx = x0 + lx, gy = y0 + ly;
             coord = ((uint32_t)gx << a.sh[N - 1]);
             if (N >= 2) coord |= ((uint32_t)gy << a.sh[N - 2]);
-            if (N == 3) coord |= ((uint32_t)z << a.sh[0]);
+            if (N == 3) coord |= ((uint32_t)(z0 + lz) << a.sh[0]);
         }
         bool keep[Q];
         unsigned bal[Q];
@@ -326,7 +346,14 @@ __global__ void __launch_bounds__(kThreads) k1_kernel(K1Args a) {
         }
         if (lane == 0) {
             s_excl[q] = excl;
-            if (t == tiles_per_img - 1) a.count[b * Q + q] = (int32_t)(excl + agg);
+            // per-tile list offsets: K2's height-window culling streams only the
+            // tiles whose height range meets the window
+            int32_t *toff = a.tile_off + (b * Q + q) * (int64_t)(tiles_per_img + 1);
+            toff[t] = (int32_t)excl;
+            if (t == tiles_per_img - 1) {
+                a.count[b * Q + q] = (int32_t)(excl + agg);
+                toff[tiles_per_img] = (int32_t)(excl + agg);
+            }
         }
     }
     __syncthreads();
@@ -342,7 +369,7 @@ __global__ void __launch_bounds__(kThreads) k1_kernel(K1Args a) {
 template <int N, int CONS, typename TIn, typename RecT>
 cudaError_t launch_t(const K1Args &a, cudaStream_t s) {
     constexpr int Q = 1 << (N - 1);
-    const int planes = (N == 3) ? 3 : 1;
+    const int planes = (N == 3) ? a.TZ + 2 : 1;
     size_t smem = sizeof(RecT) * Q * kTileV + sizeof(int) * planes * (a.TY + 2) * (a.TX + 2);
     auto kern = k1_kernel<N, CONS, TIn, RecT>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

@@ -501,14 +501,86 @@ constexpr int kBlockThreads = 512;
 constexpr int kBlockWarps = kBlockThreads / 32;
 constexpr size_t kBlockSmem = 208 * 1024;
 
+// Accumulate the records list[beg, end) whose bin lies in [lo, lo + wbins):
+// the warp's lanes stride the range, four records in flight per lane (the list
+// streams from L2; a lone load per lane leaves the SM latency-bound).
 template <typename RecT, bool PACK>
-__device__ void fill_window(const K2Args &a, const RecT *list, int n, const DirInfo &di, int lo, int wbins,
-                            const Hist<PACK> &hs) {
-    for (int i = threadIdx.x; i < n; i += kBlockThreads) {
+__device__ __forceinline__ void fill_range(const K2Args &a, const RecT *list, int beg, int end, const DirInfo &di,
+                                           int lo, int wbins, const Hist<PACK> &hs, int lane, int step) {
+    int i = beg + lane;
+    for (; i + 3 * step < end; i += 4 * step) {
+        RecT r[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) r[u] = list[i + u * step];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            int bin, wc, wj;
+            decode(r[u], di, a, bin, wc, wj);
+            bin -= lo;
+            if ((unsigned)bin < (unsigned)wbins) hs.add(bin, wc, wj);
+        }
+    }
+    for (; i < end; i += step) {
         int bin, wc, wj;
         decode(list[i], di, a, bin, wc, wj);
         bin -= lo;
         if ((unsigned)bin < (unsigned)wbins) hs.add(bin, wc, wj);
+    }
+}
+
+// Height range (bins relative to hlo) of K1 tile t: a TZ x TY x TX box of
+// vertices, so the range is sum_k min/max of xs_k times the box's extent on axis k.
+__device__ __forceinline__ void tile_bins(const K2Args &a, const DirInfo &di, int t, int &bmin, int &bmax) {
+    const int tx = t % a.tiles_x, ty = (t / a.tiles_x) % a.tiles_y, tz = t / (a.tiles_x * a.tiles_y);
+    const int n = a.ndim;
+    int lo3[kMaxN], hi3[kMaxN];
+    lo3[n - 1] = tx * a.TX;
+    hi3[n - 1] = min(lo3[n - 1] + a.TX, a.M[n - 1]) - 1;
+    lo3[n - 2] = ty * a.TY;
+    hi3[n - 2] = min(lo3[n - 2] + a.TY, a.M[n - 2]) - 1;
+    if (n == 3) {
+        lo3[0] = tz * a.TZ;
+        hi3[0] = min(lo3[0] + a.TZ, a.M[0]) - 1;
+    }
+    int hmin = 0, hmax = 0;
+#pragma unroll
+    for (int k = 0; k < kMaxN; ++k) {
+        if (k < n) {
+            const int x0 = di.xs[k] * lo3[k], x1 = di.xs[k] * hi3[k];
+            hmin += min(x0, x1);
+            hmax += max(x0, x1);
+        }
+    }
+    bmin = hmin - di.hlo;
+    bmax = hmax - di.hlo;
+}
+
+// One height window of a segment: every record whose bin is in [lo, lo+wbins).
+// A single window takes the whole list; several windows cull K1 tiles by their
+// height band, so each record is streamed about once over all windows instead
+// of once per window.
+template <typename RecT, bool PACK>
+__device__ void fill_window(const K2Args &a, const RecT *list, const int32_t *toff, int n, const DirInfo &di,
+                            int lo, int wbins, bool cull, const Hist<PACK> &hs) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (!cull) {
+        fill_range(a, list, 0, n, di, lo, wbins, hs, threadIdx.x, kBlockThreads);
+        return;
+    }
+    for (int t0 = warp * 32; t0 < a.ntiles; t0 += kBlockWarps * 32) {
+        const int t = t0 + lane;
+        bool hit = false;
+        if (t < a.ntiles) {
+            int bmin, bmax;
+            tile_bins(a, di, t, bmin, bmax);
+            hit = bmax >= lo && bmin < lo + wbins;
+        }
+        unsigned m = __ballot_sync(0xffffffffu, hit);
+        while (m) {
+            const int tt = t0 + __ffs(m) - 1;
+            m &= m - 1;
+            fill_range(a, list, toff[tt], toff[tt + 1], di, lo, wbins, hs, lane, 32);
+        }
     }
 }
 
@@ -535,15 +607,17 @@ __global__ void __launch_bounds__(kBlockThreads, 1) k2_block(K2Args a, long long
         const long long b = s / a.D, d = s % a.D;
         const DirInfo di = a.dirs[d];
         const RecT *list = recs + (b * a.Q + di.q) * a.vcap;
+        const int32_t *toff = a.tile_off + (b * a.Q + di.q) * (long long)(a.ntiles + 1);
         const int n = a.count[b * a.Q + di.q];
         const int nwin = (di.R + win - 1) / win;
+        const bool cull = nwin > 1 && a.ntiles > 1;
         // each warp owns a contiguous, 128-aligned range of the window
         const int per = ((win / kBlockWarps) + kGroup - 1) / kGroup * kGroup;
         // phase A: counts over all windows
         long long nc = 0, no = 0;
         for (int w = 0; w < nwin; ++w) {
             const int lo = w * win, wb = min(win, di.R - lo);
-            fill_window(a, list, n, di, lo, wb, hs);
+            fill_window(a, list, toff, n, di, lo, wb, cull, hs);
             __syncthreads();
             int c = 0, o = 0;
             const int b0 = min(wb, warp * per), b1 = min(wb, b0 + per);
@@ -577,7 +651,7 @@ __global__ void __launch_bounds__(kBlockThreads, 1) k2_block(K2Args a, long long
         for (int w = 0; w < nwin; ++w) {
             const int lo = w * win, wb = min(win, di.R - lo);
             if (nwin > 1) {
-                fill_window(a, list, n, di, lo, wb, hs);
+                fill_window(a, list, toff, n, di, lo, wb, cull, hs);
                 __syncthreads();
             }
             const int b0 = min(wb, warp * per), b1 = min(wb, b0 + per);

@@ -16,6 +16,7 @@
 // add — or the same in fp64. Chunk partials are combined in a fixed order by
 // a second kernel, so results are bit-identical run to run.
 #include <cmath>
+#include <type_traits>
 
 #include "eucalc_internal.cuh"
 
@@ -202,6 +203,139 @@ __global__ void __launch_bounds__(kThreads) k3_f64(K3Args a) {
     if (threadIdx.x < tlen) a.partial[(b * a.nchunks + c) * a.D + myd] = acc0 + acc1;
 }
 
+// ---------------------------------------------------------------------------
+// Tabulated kbar (the default path). t depends on the record only through the
+// integer u = 2H - L*csum (E10), so kbar(t(u)) is evaluated ONCE per u over the
+// range the directions span, in fp64 (the same formulas and the same exact
+// integer period reduction as above), and every term becomes a table lookup:
+//   idx = H + off_d  (one dp2a/dp4a on the packed coordinates; off_d folds in
+//                     -L*csum_d and the table origin, u halved: a tile's
+//                     directions share the parity of L*csum, hence of u),
+//   acc += J * tab[idx].
+// The half table of the tile's parity sits in shared memory; per term the work
+// is an LDS broadcast of the record, a DP4A, an LDS gather and the compensated
+// (fp32) or fp64 accumulation — precision-independent kbar cost, no SFU.
+constexpr int kChunkT = 8192;
+constexpr int kStageT = 1024;
+
+__global__ void k3_table(int kernel, double param, long long L, long long U0, long long U, double *t64, float *t32) {
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= U) return;
+    const long long u = U0 + i;
+    double f;
+    if (kernel == EUCALC_K_GAUSS) {
+        f = erf((double)u * (1.0 / (param * sqrt(2.0))) / (2.0 * (double)L));
+    } else if (kernel == EUCALC_K_COS) {
+        const double lp = (double)L * param;
+        if (param == rint(param) && lp < 1.0e15) {
+            const long long per = 2 * (long long)lp;  // period of u
+            long long r = u % per;
+            if (r < 0) r += per;
+            f = sinpi((double)r / lp);
+        } else {
+            f = sin((double)u * M_PI / lp);
+        }
+    } else if (kernel == EUCALC_K_SIN) {
+        f = cos((double)u / (2.0 * (double)L));
+    } else {
+        f = exp((double)u / (2.0 * (double)L));
+    }
+    t64[i] = f;
+    t32[i] = (float)f;
+}
+
+template <int DP>
+__device__ __forceinline__ int table_index(uint32_t c, int xs8, int off) {
+    int r;
+    if (DP == 2) asm("dp2a.lo.u32.s32 %0, %1, %2, %3;" : "=r"(r) : "r"(c), "r"(xs8), "r"(off));
+    else asm("dp4a.u32.s32 %0, %1, %2, %3;" : "=r"(r) : "r"(c), "r"(xs8), "r"(off));
+    return r;
+}
+
+template <typename RecT, bool F64, int DP>
+__global__ void __launch_bounds__(kThreads) k3t(K3Args a) {
+    using T = typename std::conditional<F64, double, float>::type;
+    using S = typename std::conditional<F64, int4, int2>::type;  // staged record: c, J (float bits / double)
+    extern __shared__ __align__(16) unsigned char k3t_smem[];
+    S *srec = reinterpret_cast<S *>(k3t_smem);
+    T *tab = reinterpret_cast<T *>(srec + kStageT);
+    const int c = blockIdx.x, tile = blockIdx.y;
+    const long long b = blockIdx.z;
+    const int tlen = a.tile_len[tile];
+    const int d0 = a.order[a.tile_start[tile]];
+    const int myd = threadIdx.x < tlen ? a.order[a.tile_start[tile] + threadIdx.x] : d0;
+    const DirInfo di = a.dirs[myd];
+    const DirInfo di0 = a.dirs[d0];
+    const int n = a.count[b * a.Q + di0.q];
+    const int beg = c * kChunkT, end = min(n, beg + kChunkT);
+    // the tile's half table: u = start + 2 j, u == L*csum (mod 2)
+    const int par = (int)((a.L * (long long)a.csum[d0]) & 1);
+    const long long start = a.U0 + (((a.U0 & 1) != par) ? 1 : 0);
+    const int half = (int)((a.U0 + a.U - 1 - start) / 2 + 1);
+    const T *gtab = F64 ? reinterpret_cast<const T *>(a.tab64) : reinterpret_cast<const T *>(a.tab32);
+    for (int j = threadIdx.x; j < half; j += blockDim.x) tab[j] = gtab[start - a.U0 + 2 * (long long)j];
+    // idx = (u - start) / 2 = H + off, off = (-L*csum - start) / 2 (exact: same parity)
+    const int off = (int)((-a.L * (long long)a.csum[myd] - start) / 2);
+    // H = sum xs_k p_k = dp(c, xs8) when the direction is its pair's representative;
+    // records are stored for the pair's representative orthant, which is this
+    // direction's orthant up to the antipodal swap (J -> -J, handled at staging)
+    const int sw = di0.swap;
+    const RecT *list = reinterpret_cast<const RecT *>(a.rec) + (b * a.Q + di0.q) * a.vcap;
+    T acc0 = 0, acc1 = 0, cmp0 = 0, cmp1 = 0;
+    for (int s0 = beg; s0 < end; s0 += kStageT) {
+        const int cnt = min(kStageT, end - s0);
+        __syncthreads();
+        for (int i = threadIdx.x; i < cnt; i += blockDim.x) {
+            const RecT r = list[s0 + i];
+            const int j = sw ? (r.b - r.a) : (r.a - r.b);
+            if constexpr (F64) {
+                const double jd = (double)j;
+                srec[i] = make_int4((int)r.c, 0, __double2loint(jd), __double2hiint(jd));
+            } else {
+                srec[i] = make_int2((int)r.c, __float_as_int((float)j));
+            }
+        }
+        __syncthreads();
+        if (threadIdx.x < tlen) {
+            int i = 0;
+            for (; i + 1 < cnt; i += 2) {
+                const S r0 = srec[i], r1 = srec[i + 1];
+                const T k0 = tab[table_index<DP>((uint32_t)r0.x, di.xs8, off)];
+                const T k1 = tab[table_index<DP>((uint32_t)r1.x, di.xs8, off)];
+                if constexpr (F64) {
+                    acc0 = fma(__hiloint2double(r0.w, r0.z), k0, acc0);
+                    acc1 = fma(__hiloint2double(r1.w, r1.z), k1, acc1);
+                } else {
+                    // Kahan-compensated fp32 (J * kbar formed inside the FMA)
+                    const float y0 = fmaf(__int_as_float(r0.y), k0, -cmp0), t0 = acc0 + y0;
+                    cmp0 = (t0 - acc0) - y0;
+                    acc0 = t0;
+                    const float y1 = fmaf(__int_as_float(r1.y), k1, -cmp1), t1 = acc1 + y1;
+                    cmp1 = (t1 - acc1) - y1;
+                    acc1 = t1;
+                }
+            }
+            if (i < cnt) {
+                const S r0 = srec[i];
+                const T k0 = tab[table_index<DP>((uint32_t)r0.x, di.xs8, off)];
+                if constexpr (F64) {
+                    acc0 = fma(__hiloint2double(r0.w, r0.z), k0, acc0);
+                } else {
+                    const float y0 = fmaf(__int_as_float(r0.y), k0, -cmp0), t0 = acc0 + y0;
+                    cmp0 = (t0 - acc0) - y0;
+                    acc0 = t0;
+                }
+            }
+        }
+    }
+    if (threadIdx.x < tlen) {
+        double tot;
+        if constexpr (F64) tot = acc0 + acc1;
+        else tot = ((double)acc0 - (double)cmp0) + ((double)acc1 - (double)cmp1);
+        a.partial[(b * a.nchunks + c) * a.D + myd] = tot;
+    }
+}
+
 // Fixed-order combine of the chunk partials; applies -scale of kbar.
 __global__ void k3_combine(const K3Args a, double scale) {
     const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
@@ -216,11 +350,41 @@ __global__ void k3_combine(const K3Args a, double scale) {
 
 }  // namespace
 
-int k3_chunk() { return kChunk; }
+int k3_chunk(bool table) { return table ? kChunkT : kChunk; }
+
+size_t k3_table_smem(bool f64, long long U) {
+    const long long half = (U + 1) / 2 + 1;
+    return (f64 ? sizeof(int4) : sizeof(int2)) * kStageT + (f64 ? 8 : 4) * half;
+}
+
+cudaError_t launch_k3_table(const K3Args &a, cudaStream_t s) {
+    // kbar table over u in [U0, U0 + U)
+    k3_table<<<(unsigned)((a.U + 255) / 256), 256, 0, s>>>(a.kernel, a.param, a.L, a.U0, a.U, a.tab64, a.tab32);
+    count_launch();
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    return cudaSuccess;
+}
 
 cudaError_t launch_k3(const K3Args &a, cudaStream_t s) {
     dim3 grid((unsigned)a.nchunks, (unsigned)a.ntiles, (unsigned)a.batch);
-    if (a.precision == EUCALC_F32) {
+    if (a.use_table) {
+        cudaError_t e = launch_k3_table(a, s);
+        if (e != cudaSuccess) return e;
+        const bool f64 = a.precision == EUCALC_F64;
+        const size_t smem = k3_table_smem(f64, a.U);
+        void (*k)(K3Args) = nullptr;
+        if (a.wide) {
+            if (f64) k = a.dp == 2 ? k3t<Rec32, true, 2> : k3t<Rec32, true, 3>;
+            else k = a.dp == 2 ? k3t<Rec32, false, 2> : k3t<Rec32, false, 3>;
+        } else {
+            if (f64) k = a.dp == 2 ? k3t<Rec16, true, 2> : k3t<Rec16, true, 3>;
+            else k = a.dp == 2 ? k3t<Rec16, false, 2> : k3t<Rec16, false, 3>;
+        }
+        e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        k<<<grid, a.threads, smem, s>>>(a);
+    } else if (a.precision == EUCALC_F32) {
         if (a.wide) k3_f32<Rec32><<<grid, a.threads, 0, s>>>(a);
         else k3_f32<Rec16><<<grid, a.threads, 0, s>>>(a);
     } else {

@@ -47,6 +47,9 @@ def test_appendix_radon_evaluation():
     assert g.radon_eval(xi, 1.0) == 1
     assert g.radon_eval(xi, 1.5) == 0
     assert g.radon_eval(xi, math.inf) == 0 and g.ect_eval(xi, math.inf) == 2 and g.ect_eval(xi, -math.inf) == 0
+    # far outside the support (beyond int64 in doubled lattice units): ECT(+-oo) limits
+    assert g.ect_eval(xi, 1e300) == g.euler() == 2 and g.ect_eval(xi, -1e300) == 0
+    assert g.radon_eval(xi, 1e300) == 0 and g.radon_eval(xi, -1e300) == 0
 
 
 def _queries(g, xi, r, rng):

@@ -73,13 +73,16 @@ def check_critical(images, construction, cr, imgs_to_check=None):
             np.testing.assert_array_equal(j, oj[keep], err_msg=f"J b={b} e={e}")
 
 
-def check_ht(images, dirs, construction, cr, kernel, param, precision, pairs=None):
-    out = eu.hybrid(cr, dirs, kernel, param, precision).cpu().numpy()
+def check_ht(images, dirs, construction, cr, kernel, param, precision, pairs=None, algorithms=("auto", "direct")):
+    """Both HT algorithms (per-term kbar and tabulated kbar, eucalc_hybrid_ex) vs the
+    oracle's quadrature of the Radon transform."""
     ref = oracle.ht_batch(images, dirs, construction, kernel, param, pairs=pairs)
     tol = HT_TOL[precision]
-    for (b, d), want in ref.items():
-        got = float(out[b, d])
-        assert abs(got - want) <= tol * max(abs(want), 1.0), (kernel, precision, b, d, got, want)
+    for alg in algorithms:
+        out = eu.hybrid(cr, dirs, kernel, param, precision, algorithm=alg).cpu().numpy()
+        for (b, d), want in ref.items():
+            got = float(out[b, d])
+            assert abs(got - want) <= tol * max(abs(want), 1.0), (alg, kernel, precision, b, d, got, want)
 
 
 # ----------------------------------------------------------------------------- golden
@@ -138,6 +141,14 @@ def test_block_regime_multiwindow():
     check_transforms(img, dirs, "vertex", res)
 
 
+def test_block_regime_3d_culled_windows():
+    """3-D, several K1 tiles (16x16x8 boxes) and height windows -> tile culling."""
+    vol = synth.smooth_volume(40, 77)[None]
+    dirs = np.concatenate([synth.random_directions(3, 3, 400, 12), np.array([[400, -399, 398]], np.int32)])
+    cx, cr, res = run_gpu(vol, dirs, "vertex")
+    check_transforms(vol, dirs, "vertex", res)
+
+
 def test_negative_and_int32_weights():
     rng = np.random.default_rng(3)
     images = rng.integers(-40000, 40000, size=(2, 12, 11)).astype(np.int32)
@@ -156,7 +167,7 @@ def test_ht_kernels(kernel, param, precision):
     dirs, _ = synth.fibonacci_directions(40, 8.0)
     cx = eu.build_complex(vols, "vertex")
     cr = eu.critical_points(cx)
-    check_ht(vols, dirs, "vertex", cr, kernel, param, precision)
+    check_ht(vols, dirs, "vertex", cr, kernel, param, precision, algorithms=("direct", "table"))
 
 
 # ----------------------------------------------------------------------------- ABI behaviour
@@ -314,4 +325,4 @@ def test_config5_sampled():
     pairs = [(0, 0), (1, 4999), (0, 9999)]
     for kernel, param in (("gauss", 1.0), ("cos", 64.0)):
         for precision in ("f64", "f32"):
-            check_ht(vols, dirs, "vertex", cr, kernel, param, precision, pairs=pairs)
+            check_ht(vols, dirs, "vertex", cr, kernel, param, precision, pairs=pairs, algorithms=("direct", "table"))

@@ -54,7 +54,7 @@ def run(eu, torch, k, variant, construction, steps, warmup, ht_kernels, out):
         cr = eu.critical_points(cx)
         r = eu.transforms(cr, dirs, elem_bytes="auto", share_heights=True) if do_tr else None
         hts = {}
-        for kern, param, prec in ht_kernels if k == 5 else ():
+        for kern, param, prec in ht_kernels[:1] if k == 5 else ():
             hts[(kern, prec)] = eu.hybrid(cr, dirs, kern, param, prec)
         return cx, cr, r, hts
 
@@ -106,18 +106,18 @@ def run(eu, torch, k, variant, construction, steps, warmup, ht_kernels, out):
         e = ((dirs > 0).astype(np.int64) << np.arange(dirs.shape[1])).sum(1)
         nterms = int(cnt[:, e, 1].sum())  # ordinary points summed over (image, direction)
         nrec = npair
-        for kern, param, prec in ht_kernels:
+        for (kern, param, prec), alg in [(h, a) for h in ht_kernels for a in ("direct", "table")]:
             for _ in range(2):
-                eu.hybrid(cr, dirs, kern, param, prec)
+                eu.hybrid(cr, dirs, kern, param, prec, algorithm=alg)
             torch.cuda.synchronize()
             eu.profile_enable(True)
             for _ in range(steps):
-                eu.hybrid(cr, dirs, kern, param, prec)
+                eu.hybrid(cr, dirs, kern, param, prec, algorithm=alg)
             torch.cuda.synchronize()
             ms, _ = eu.profile_read("k3_hybrid")
             eu.profile_enable(False)
             ms /= steps
-            out.append(dict(base, stage=f"k3_hybrid[{kern},{prec}]", ms=ms,
+            out.append(dict(base, stage=f"k3_hybrid[{kern},{prec},{alg}]", ms=ms,
                             image_directions_per_s=B * D / (ms / 1e3),
                             ordinary_terms=nterms, records_evaluated=nrec,
                             terms_per_s=nterms / (ms / 1e3), records_per_s=nrec / (ms / 1e3)))
