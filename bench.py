@@ -68,6 +68,9 @@ class Clocks:
         self.gpu = gpu_index
 
     def __enter__(self):
+        return self.start()
+
+    def start(self):
         q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
              "clocks_event_reasons.sw_power_cap")
@@ -81,11 +84,22 @@ class Clocks:
             self.proc = None
         return self
 
+    def mark(self):
+        """Only samples taken after this call count (the timed region starts)."""
+        self.first = len(self.samples)
+
+    def end(self):
+        """The timed region ends (one more sample, in flight, still counts)."""
+        self.last = len(self.samples) + 1
+
     def _read(self):
         for line in self.proc.stdout:
             self.samples.append([x.strip() for x in line.split(",")])
 
     def __exit__(self, *a):
+        self.stop()
+
+    def stop(self):
         if self.proc:
             time.sleep(0.25)
             self.proc.terminate()
@@ -95,6 +109,9 @@ class Clocks:
                 self.proc.kill()
 
     def summary(self):
+        first = getattr(self, "first", 0)
+        samples = self.samples[first:max(getattr(self, "last", len(self.samples)), first + 1)]
+        self.samples = samples
         if not self.samples:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
         sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
@@ -164,6 +181,11 @@ def gpu_arm(args):
             dist.barrier()
         torch.cuda.synchronize()
 
+    # the clock sampler starts before the warm-up: nvidia-smi's start-up (NVML
+    # initialisation) stalls the driver for milliseconds and must not fall in
+    # the timed region
+    clk = Clocks(local).start()
+    time.sleep(0.5)
     for _ in range(args.warmup):
         run_step(eu, torch, imgs_dev, dirs)
     torch.cuda.synchronize()
@@ -173,8 +195,9 @@ def gpu_arm(args):
     k2_ms = 0.0
     stage_ms = {}
     launches = 0
-    with Clocks(local) as clk:
+    if True:
         barrier()
+        clk.mark()
         for _ in range(args.steps):
             flush.fill_(1.0)
             ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -190,6 +213,8 @@ def gpu_arm(args):
                 stage_ms[st] = stage_ms.get(st, 0.0) + eu.profile_read(st)[0]
             eu.profile_enable(False)
         barrier()
+        clk.end()
+        clk.stop()
     dev_ms = float(np.sum(times))
     if world > 1:
         t = torch.tensor([dev_ms], device="cuda")
@@ -336,7 +361,7 @@ def reference_arm(args):
 def main(argv=None):
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=30)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cpu-sample", type=int, default=96, help="images per variant in the oracle sample")

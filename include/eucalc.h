@@ -59,14 +59,14 @@ typedef struct eucalc_critical eucalc_critical;
  * Segment s = image * D + direction holds entries [offsets[s], offsets[s+1]):
  * heights ascending (int lattice heights, see above) and the values there.
  * The value left of the first height is 0 (implicit leading E[0] = 0).
- * offsets: int64 [batch*D + 1]; height/value: int32 or int64 [capacity]
- * (elem_bytes 4 or 8). All three caller-owned. */
+ * offsets: int64 [batch*D + 1]; height/value: int16, int32 or int64 [capacity]
+ * (elem_bytes 2, 4 or 8). All three caller-owned. */
 typedef struct eucalc_steps {
     int64_t *offsets;
     void *height;
     void *value;
     int64_t capacity;   /* entries available in height[] and value[] */
-    int32_t elem_bytes; /* 4 or 8 */
+    int32_t elem_bytes; /* 2, 4 or 8 */
     int32_t reserved;   /* must be 0 */
 } eucalc_steps;
 
@@ -126,8 +126,9 @@ eucalc_status eucalc_output_bound(const eucalc_critical *cr, const int32_t *dirs
  * `height` pointer equal to the ect `height` pointer is written once (T_c = T).
  * Capacity: each non-NULL output must hold eucalc_output_bound() entries
  * (ect/classical: bound_ect, ordinary: bound_ordinary), else E_CAPACITY with
- * *required_out (if non-NULL) = that bound and nothing written. Element width 4 is
- * accepted when every height and value provably fits int32, else E_RANGE.
+ * *required_out (if non-NULL) = that bound and nothing written. Element widths
+ * 2 and 4 are accepted when every height and value provably fits int16 / int32
+ * (host-checked bounds from K1's statistics), else E_RANGE.
  * The exact total of segment s is offsets[s+1] - offsets[s].
  * Device outputs: asynchronous except the first bound query. Host outputs:
  * computed into library scratch and copied back, then `stream` is synchronised.

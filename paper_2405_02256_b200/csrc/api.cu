@@ -9,6 +9,7 @@
 #include <new>
 #include <numeric>
 #include <string>
+#include <tuple>
 #include <vector>
 
 #include "eucalc_internal.cuh"
@@ -275,7 +276,7 @@ eucalc_status get_plan(const Complex *cx, const int32_t *dirs, int64_t D, cudaSt
     e->aligned = cx->aligned;
     std::copy(cx->M, cx->M + n, e->M);
     std::copy(cx->scale, cx->scale + n, e->scale);
-    // HT tiles: directions grouped by orthant (Lemma 3), <= 256 per tile
+    // HT tiles: directions grouped by orthant (Lemma 3), <= 512 per tile
     e->order.resize(D);
     std::iota(e->order.begin(), e->order.end(), 0);
     // tile key: orthant (same critical list, Lemma 3) and the parity of L*csum
@@ -284,7 +285,7 @@ eucalc_status get_plan(const Complex *cx, const int32_t *dirs, int64_t D, cudaSt
     std::stable_sort(e->order.begin(), e->order.end(), [&](int32_t x, int32_t y) { return key(x) < key(y); });
     for (int64_t i = 0; i < D;) {
         int64_t j = i;
-        while (j < D && key(e->order[j]) == key(e->order[i]) && j - i < 256) ++j;
+        while (j < D && key(e->order[j]) == key(e->order[i]) && j - i < 512) ++j;
         e->tstart.push_back((int32_t)i);
         e->tlen.push_back((int32_t)(j - i));
         i = j;
@@ -381,6 +382,44 @@ int64_t bin_sum_bound(const Critical *cr) {
 }  // namespace
 
 void count_launch(int n) { g_launches += n; }
+
+namespace {
+struct PrepKey {
+    const void *fn;
+    int threads;
+    size_t smem;
+    int dev;
+    bool operator<(const PrepKey &o) const {
+        return std::tie(fn, threads, smem, dev) < std::tie(o.fn, o.threads, o.smem, o.dev);
+    }
+};
+std::mutex g_prep_mu;
+std::map<PrepKey, int> g_prep_occ;
+std::map<std::pair<const void *, int>, size_t> g_prep_smem;
+}  // namespace
+
+cudaError_t prepare_kernel(const void *fn, int threads, size_t smem, int *occ) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lk(g_prep_mu);
+    auto it = g_prep_occ.find(PrepKey{fn, threads, smem, dev});
+    if (it != g_prep_occ.end()) {
+        if (occ) *occ = it->second;
+        return cudaSuccess;
+    }
+    size_t &cur = g_prep_smem[{fn, dev}];
+    if (smem > cur) {
+        cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        cur = smem;
+    }
+    int o = 0;
+    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, fn, threads, smem);
+    if (e != cudaSuccess) return e;
+    g_prep_occ[PrepKey{fn, threads, smem, dev}] = o;
+    if (occ) *occ = o;
+    return cudaSuccess;
+}
 
 namespace {
 std::mutex g_pin_mu;
@@ -880,7 +919,14 @@ eucalc_status eucalc_transforms(const eucalc_critical *ccr, const int32_t *dirs,
     unsigned long long *flags = (unsigned long long *)dalloc(sizeof(unsigned long long) * S);
     unsigned int *ticket = (unsigned int *)dalloc(sizeof(unsigned int) * 4);
     int *cnts = (int *)dalloc(sizeof(int) * 2 * S);
-    if (!flags || !ticket || !cnts) {
+    // warp regime, lists of <= 32 records: k2w_count keeps the merged runs (16-bit
+    // fields: every bin index, value and running sum must fit) so that k2w_emit
+    // need not sort them again
+    int64_t min_count = INT64_MAX;
+    for (int64_t i = 0; i < cx->batch * cr->Q; ++i) min_count = std::min(min_count, cr->h_count[i]);
+    const bool slab_ok = min_count <= 32 && p.R_max <= 32767 && cr->max_abs_sum < 32768 && cr->max_count <= 32768;
+    uint2 *slab = slab_ok ? (uint2 *)dalloc(sizeof(uint2) * 33 * S) : nullptr;
+    if (!flags || !ticket || !cnts || (slab_ok && !slab)) {
         free_scratch();
         return fail(EUCALC_E_NOMEM, "scratch");
     }
@@ -924,6 +970,7 @@ eucalc_status eucalc_transforms(const eucalc_critical *ccr, const int32_t *dirs,
         a.ticket = ticket;
         a.cnt_c = cnts;
         a.cnt_o = cnts + S;
+        a.slab = slab;
         ProfScope ps("k2_transforms", st);
         e = launch_k2(a, st, num_sms());
     }

@@ -126,6 +126,7 @@ struct K2Args {
     unsigned long long *flags;  // [batch*D] look-back flags (zeroed)
     unsigned int *ticket;       // [4] ticket counters (zeroed)
     int *cnt_c, *cnt_o;         // [batch*D] per-segment counts (warp regime)
+    uint2 *slab;                // [batch*D][33] merged runs of lists <= 32 records, or NULL
 };
 cudaError_t launch_k2(const K2Args &a, cudaStream_t s, int num_sms);
 
@@ -139,7 +140,7 @@ struct K3Args {
     uint32_t msk[kMaxN];
     const DirInfo *dirs;       // per direction (original order)
     const int32_t *order;      // sorted direction index list (grouped by orthant)
-    const int32_t *tile_start; // [ntiles] start into order; tile = same-orthant run of <= 256
+    const int32_t *tile_start; // [ntiles] start into order; tile = same-orthant, same-parity run of <= 512
     const int32_t *tile_len;
     int ntiles;
     int64_t D, batch;
@@ -179,6 +180,12 @@ struct K4Args {
     void *out;                  // [batch*D][nq]
 };
 cudaError_t launch_k4(const K4Args &a, cudaStream_t s, int num_sms);
+
+// Launch preparation with a per-process cache: the dynamic shared memory
+// attribute is raised to the largest `smem` seen for `fn` and the occupancy
+// (blocks per SM at `threads`, `smem`) is memoised, so the host cost of a
+// repeated launch is a map lookup instead of two driver calls.
+cudaError_t prepare_kernel(const void *fn, int threads, size_t smem, int *occ);
 
 // thread-local launch counter (eucalc_launch_count)
 void count_launch(int n = 1);

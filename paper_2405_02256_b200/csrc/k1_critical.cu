@@ -372,7 +372,7 @@ cudaError_t launch_t(const K1Args &a, cudaStream_t s) {
     const int planes = (N == 3) ? a.TZ + 2 : 1;
     size_t smem = sizeof(RecT) * Q * kTileV + sizeof(int) * planes * (a.TY + 2) * (a.TX + 2);
     auto kern = k1_kernel<N, CONS, TIn, RecT>;
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaError_t e = prepare_kernel((const void *)kern, kThreads, smem, nullptr);
     if (e != cudaSuccess) return e;
     int64_t nblocks = a.batch * (int64_t)a.tiles_x * a.tiles_y * a.tiles_z;
     kern<<<(unsigned)nblocks, kThreads, smem, s>>>(a);

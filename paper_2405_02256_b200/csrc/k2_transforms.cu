@@ -114,21 +114,48 @@ __device__ __forceinline__ void decode(const RecT &r, const DirInfo &di, const K
 //   PACK : one u32 per bin holding wj * 2^16 + wc, a linear packing that is
 //          exact while every bin's |sum| < 2^15 (host-checked bound).
 //   SPLIT: two u32 arrays (sum Delta^-, sum J), int32 sums.
-template <bool PACK>
+// Bin b lives in word b ^ ((b >> 5) & 31) (a permutation inside each 32-bin
+// block): records streamed in vertex order hit bins in arithmetic progressions
+// of stride xs_x (often a multiple of 8, 16 or 32), which without the XOR fall
+// into a few of the 32 banks and serialise the atomics.
+__device__ __forceinline__ int swz(int b) { return b ^ ((b >> 5) & 31); }
+
+// SWZ: bin b lives in word swz(b) (block regime, long streams of 3-D / large
+// 2-D lists); else word b, and the scan reads a lane's 4 bins with one LDS.128
+// (warp regime, where the lists are short and the scan dominates).
+template <bool PACK, bool SWZ = false>
 struct Hist {
     unsigned *c;
     unsigned *j;
     __device__ __forceinline__ void add(int bin, int wc, int wj) const {
+        const int w = SWZ ? swz(bin) : bin;
         if (PACK) {
-            if (wc | wj) atomicAdd(c + bin, (unsigned)(wj * 65536 + wc));
+            if (wc | wj) atomicAdd(c + w, (unsigned)(wj * 65536 + wc));
         } else {
-            if (wc) atomicAdd(c + bin, (unsigned)wc);
-            if (wj) atomicAdd(j + bin, (unsigned)wj);
+            if (wc) atomicAdd(c + w, (unsigned)wc);
+            if (wj) atomicAdd(j + w, (unsigned)wj);
         }
     }
     // bins b0..b0+3 (b0 % 4 == 0), optionally cleared
     __device__ __forceinline__ void load4(int b0, int (&wc)[4], int (&wj)[4], bool clear) const {
-        if (PACK) {
+        if constexpr (SWZ) {
+#pragma unroll
+            for (int s = 0; s < 4; ++s) {
+                const int w = swz(b0 + s);
+                if (PACK) {
+                    const unsigned u = c[w];
+                    wc[s] = (int)(short)(u & 0xffffu);
+                    wj[s] = ((int)u - wc[s]) >> 16;
+                } else {
+                    wc[s] = (int)c[w];
+                    wj[s] = (int)j[w];
+                }
+                if (clear) {
+                    c[w] = 0;
+                    if (!PACK) j[w] = 0;
+                }
+            }
+        } else if constexpr (PACK) {
             uint4 v = *reinterpret_cast<const uint4 *>(c + b0);
             if (clear) *reinterpret_cast<uint4 *>(c + b0) = make_uint4(0, 0, 0, 0);
             const unsigned u[4] = {v.x, v.y, v.z, v.w};
@@ -175,8 +202,8 @@ __device__ __forceinline__ int warp_incl_scan(int v) {
 }
 
 // Count the nonzero bins of one 128-bin group (lane <-> 4 consecutive bins).
-template <bool PACK>
-__device__ __forceinline__ void count_group(const Hist<PACK> &hs, int base, int &c, int &o, bool clear) {
+template <bool PACK, bool SWZ>
+__device__ __forceinline__ void count_group(const Hist<PACK, SWZ> &hs, int base, int &c, int &o, bool clear) {
     int wc[4], wj[4];
     hs.load4(base + 4 * (threadIdx.x & 31), wc, wj, clear);
 #pragma unroll
@@ -227,8 +254,8 @@ __device__ __forceinline__ void put_o(const OutPtrs<OutT> &o, int p, int h, int 
 // order: local sums per lane, one warp scan of (counts, sum Delta^-, sum J),
 // then up to 4 entries per stream per lane. Running values are warp-uniform;
 // positions are int32 (< 2^31 entries per call, host-checked).
-template <int MODE, typename OutT, bool PACK>
-__device__ __forceinline__ void emit_group(const OutPtrs<OutT> &o, const Hist<PACK> &hs, int base, int h0,
+template <int MODE, typename OutT, bool PACK, bool SWZ>
+__device__ __forceinline__ void emit_group(const OutPtrs<OutT> &o, const Hist<PACK, SWZ> &hs, int base, int h0,
                                            int &e_run, int &r_run, int &pc, int &po) {
     const int lane = threadIdx.x & 31;
     int wc[4], wj[4];
@@ -388,8 +415,18 @@ __global__ void __launch_bounds__(kWarpThreads) k2w_count(K2Args a, int rcap, in
         int c = 0, o = 0;
         if (n <= 32) {
             const SparseRuns r = sparse_runs<RecT>(a, b, di, n);
-            c = __popc(__ballot_sync(0xffffffffu, r.emit_c));
-            o = __popc(__ballot_sync(0xffffffffu, r.emit_o));
+            const unsigned mc = __ballot_sync(0xffffffffu, r.emit_c), mo = __ballot_sync(0xffffffffu, r.emit_o);
+            c = __popc(mc);
+            o = __popc(mo);
+            if (a.slab) {
+                // keep the merged runs for k2w_emit (16-bit fields, host-checked):
+                // bin | E << 16, E_c | E' << 16; the emission masks in slot 32
+                const int ec = r.pj - r.run_j + r.run_c;
+                uint2 *sl = a.slab + s * 33;
+                sl[threadIdx.x & 31] = make_uint2((unsigned)(r.h & 0xffff) | ((unsigned)r.pc << 16),
+                                                  (unsigned)(ec & 0xffff) | ((unsigned)r.pj << 16));
+                if ((threadIdx.x & 31) == 0) sl[32] = make_uint2(mc, mo);
+            }
         } else {
             fill_segment<RecT>(a, hs, b, di);
             for (int base = 0; base < di.R; base += kGroup) count_group(hs, base, c, o, true);
@@ -419,13 +456,22 @@ __global__ void __launch_bounds__(kWarpThreads) k2w_emit(K2Args a, int rcap) {
         const int n = a.count[b * a.Q + di.q];
         int pc = any_c ? (int)off_c[s] : 0, po = a.do_ord ? (int)a.ord.off[s] : 0;
         if (n <= 32) {
-            const SparseRuns r = sparse_runs<RecT>(a, b, di, n);
             const unsigned lt = (1u << (threadIdx.x & 31)) - 1;
-            const unsigned mc = __ballot_sync(0xffffffffu, r.emit_c), mo = __ballot_sync(0xffffffffu, r.emit_o);
-            const int h = di.hlo + r.h;
-            // classical value: Radon(h-) + sum Delta^- at h
-            if (r.emit_c) put_c<MODE>(o, pc + __popc(mc & lt), h, r.pc, r.pj - r.run_j + r.run_c);
-            if (r.emit_o) put_o<MODE>(o, po + __popc(mo & lt), h, r.pj);
+            if (a.slab) {
+                const uint2 *sl = a.slab + (long long)s * 33;
+                const uint2 v = sl[threadIdx.x & 31], m = sl[32];
+                const int h = di.hlo + (int)(v.x & 0xffff);
+                const int e = (int)v.x >> 16, ec = (int)(short)(v.y & 0xffff), eo = (int)v.y >> 16;
+                if ((m.x >> (threadIdx.x & 31)) & 1) put_c<MODE>(o, pc + __popc(m.x & lt), h, e, ec);
+                if ((m.y >> (threadIdx.x & 31)) & 1) put_o<MODE>(o, po + __popc(m.y & lt), h, eo);
+            } else {
+                const SparseRuns r = sparse_runs<RecT>(a, b, di, n);
+                const unsigned mc = __ballot_sync(0xffffffffu, r.emit_c), mo = __ballot_sync(0xffffffffu, r.emit_o);
+                const int h = di.hlo + r.h;
+                // classical value: Radon(h-) + sum Delta^- at h
+                if (r.emit_c) put_c<MODE>(o, pc + __popc(mc & lt), h, r.pc, r.pj - r.run_j + r.run_c);
+                if (r.emit_o) put_o<MODE>(o, po + __popc(mo & lt), h, r.pj);
+            }
         } else {
             fill_segment<RecT>(a, hs, b, di);
             int e_run = 0, r_run = 0;
@@ -504,9 +550,9 @@ constexpr size_t kBlockSmem = 208 * 1024;
 // Accumulate the records list[beg, end) whose bin lies in [lo, lo + wbins):
 // the warp's lanes stride the range, four records in flight per lane (the list
 // streams from L2; a lone load per lane leaves the SM latency-bound).
-template <typename RecT, bool PACK>
+template <typename RecT, bool PACK, bool SWZ>
 __device__ __forceinline__ void fill_range(const K2Args &a, const RecT *list, int beg, int end, const DirInfo &di,
-                                           int lo, int wbins, const Hist<PACK> &hs, int lane, int step) {
+                                           int lo, int wbins, const Hist<PACK, SWZ> &hs, int lane, int step) {
     int i = beg + lane;
     for (; i + 3 * step < end; i += 4 * step) {
         RecT r[4];
@@ -559,9 +605,9 @@ __device__ __forceinline__ void tile_bins(const K2Args &a, const DirInfo &di, in
 // A single window takes the whole list; several windows cull K1 tiles by their
 // height band, so each record is streamed about once over all windows instead
 // of once per window.
-template <typename RecT, bool PACK>
+template <typename RecT, bool PACK, bool SWZ>
 __device__ void fill_window(const K2Args &a, const RecT *list, const int32_t *toff, int n, const DirInfo &di,
-                            int lo, int wbins, bool cull, const Hist<PACK> &hs) {
+                            int lo, int wbins, bool cull, const Hist<PACK, SWZ> &hs) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     if (!cull) {
         fill_range(a, list, 0, n, di, lo, wbins, hs, threadIdx.x, kBlockThreads);
@@ -593,7 +639,7 @@ __global__ void __launch_bounds__(kBlockThreads, 1) k2_block(K2Args a, long long
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     constexpr int words = PACK ? 1 : 2;
     const OutPtrs<OutT> outp(a);
-    Hist<PACK> hs;
+    Hist<PACK, true> hs;
     hs.c = hist;
     hs.j = hist + win;
     for (int i = threadIdx.x; i < win * words; i += kBlockThreads) hist[i] = 0;
@@ -729,25 +775,23 @@ cudaError_t launch_t(const K2Args &a, cudaStream_t s, int num_sms) {
             default: break;
             }
         }
-        cudaError_t e = cudaFuncSetAttribute(kc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e == cudaSuccess) e = cudaFuncSetAttribute(ke, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        int occ = 0, occ2 = 0;
+        cudaError_t e = prepare_kernel((const void *)kc, threads, smem, &occ);
+        if (e == cudaSuccess) e = prepare_kernel((const void *)ke, threads, smem, &occ2);
         if (e != cudaSuccess) return e;
-        int occ = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kc, threads, smem);
         const long long wblocks = (nseg + warps - 1) / warps;
         const long long grid = std::min<long long>(wblocks, (long long)std::max(occ, 1) * num_sms);
         kc<<<(unsigned)grid, threads, smem, s>>>(a, rcap, a.cnt_c, a.cnt_o);
         const long long ntiles = (nseg + 1 + kScanTile - 1) / kScanTile;
         k2_scan<<<(unsigned)ntiles, kScanThreads, 0, s>>>(a, a.cnt_c, a.cnt_o, nseg, a.flags);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, ke, threads, smem);
-        const long long grid2 = std::min<long long>(wblocks, (long long)std::max(occ, 1) * num_sms);
+        const long long grid2 = std::min<long long>(wblocks, (long long)std::max(occ2, 1) * num_sms);
         ke<<<(unsigned)grid2, threads, smem, s>>>(a, rcap);
         count_launch(3);
         return cudaGetLastError();
     }
     const int win = (int)(kBlockSmem / (4 * words)) / kGroup * kGroup;
     auto kern = k2_block<RecT, OutT, PACK>;
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kBlockSmem);
+    cudaError_t e = prepare_kernel((const void *)kern, kBlockThreads, kBlockSmem, nullptr);
     if (e != cudaSuccess) return e;
     long long grid = std::min<long long>(nseg, num_sms);
     kern<<<(unsigned)grid, kBlockThreads, kBlockSmem, s>>>(a, nseg, win);

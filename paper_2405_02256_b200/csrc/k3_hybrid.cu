@@ -8,7 +8,7 @@
 // The additive constant of kbar cancels because sum J = 0.
 //
 // Work decomposition: directions are grouped by orthant on the host (Lemma 3,
-// same sign vector -> same critical list) into tiles of <= 256; a CTA
+// same sign vector -> same critical list) into tiles of <= 512; a CTA
 // owns (image, tile, chunk of kChunk records) with one direction per thread in
 // registers and the chunk staged in shared memory (broadcast reads). Per term:
 // 3 FMA for the height, 1 FMA for the kernel argument, kbar (erf / sinpi /
@@ -23,7 +23,7 @@
 namespace eucalc {
 namespace {
 
-constexpr int kThreads = 256;
+constexpr int kThreads = 512;  // max block: one direction per thread, tiles of <= 512
 constexpr int kChunk = 4096;
 constexpr int kStage = 1024;
 
@@ -216,7 +216,7 @@ __global__ void __launch_bounds__(kThreads) k3_f64(K3Args a) {
 // is an LDS broadcast of the record, a DP4A, an LDS gather and the compensated
 // (fp32) or fp64 accumulation — precision-independent kbar cost, no SFU.
 constexpr int kChunkT = 8192;
-constexpr int kStageT = 1024;
+constexpr int kStageT = 2048;
 
 __global__ void k3_table(int kernel, double param, long long L, long long U0, long long U, double *t64, float *t32) {
     const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
@@ -297,25 +297,30 @@ __global__ void __launch_bounds__(kThreads) k3t(K3Args a) {
         }
         __syncthreads();
         if (threadIdx.x < tlen) {
+            // four independent record chains per iteration (LDS -> IDP -> LDS -> FMA)
             int i = 0;
-            for (; i + 1 < cnt; i += 2) {
-                const S r0 = srec[i], r1 = srec[i + 1];
-                const T k0 = tab[table_index<DP>((uint32_t)r0.x, di.xs8, off)];
-                const T k1 = tab[table_index<DP>((uint32_t)r1.x, di.xs8, off)];
-                if constexpr (F64) {
-                    acc0 = fma(__hiloint2double(r0.w, r0.z), k0, acc0);
-                    acc1 = fma(__hiloint2double(r1.w, r1.z), k1, acc1);
-                } else {
-                    // Kahan-compensated fp32 (J * kbar formed inside the FMA)
-                    const float y0 = fmaf(__int_as_float(r0.y), k0, -cmp0), t0 = acc0 + y0;
-                    cmp0 = (t0 - acc0) - y0;
-                    acc0 = t0;
-                    const float y1 = fmaf(__int_as_float(r1.y), k1, -cmp1), t1 = acc1 + y1;
-                    cmp1 = (t1 - acc1) - y1;
-                    acc1 = t1;
+            for (; i + 3 < cnt; i += 4) {
+                S r[4];
+                T k[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) r[u] = srec[i + u];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) k[u] = tab[table_index<DP>((uint32_t)r[u].x, di.xs8, off)];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    if constexpr (F64) {
+                        if (u & 1) acc1 = fma(__hiloint2double(r[u].w, r[u].z), k[u], acc1);
+                        else acc0 = fma(__hiloint2double(r[u].w, r[u].z), k[u], acc0);
+                    } else {
+                        // Kahan-compensated fp32 (J * kbar formed inside the FMA)
+                        float &acc = (u & 1) ? acc1 : acc0, &cmp = (u & 1) ? cmp1 : cmp0;
+                        const float y = fmaf(__int_as_float(r[u].y), k[u], -cmp), t = acc + y;
+                        cmp = (t - acc) - y;
+                        acc = t;
+                    }
                 }
             }
-            if (i < cnt) {
+            for (; i < cnt; ++i) {
                 const S r0 = srec[i];
                 const T k0 = tab[table_index<DP>((uint32_t)r0.x, di.xs8, off)];
                 if constexpr (F64) {
@@ -381,7 +386,7 @@ cudaError_t launch_k3(const K3Args &a, cudaStream_t s) {
             if (f64) k = a.dp == 2 ? k3t<Rec16, true, 2> : k3t<Rec16, true, 3>;
             else k = a.dp == 2 ? k3t<Rec16, false, 2> : k3t<Rec16, false, 3>;
         }
-        e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        e = prepare_kernel((const void *)k, a.threads, smem, nullptr);
         if (e != cudaSuccess) return e;
         k<<<grid, a.threads, smem, s>>>(a);
     } else if (a.precision == EUCALC_F32) {

@@ -12,7 +12,10 @@ __global__ void k(unsigned long long* out, int iters, int bins) {
   long long t0 = clock64();
   for (int i = 0; i < iters; ++i) {
     x = x * 1664525u + 1013904223u;
-    int b = (MODE == 2 || MODE == 3) ? ((threadIdx.x * 37 + i * 101) % bins) : (x >> 8) % bins;
+    int b = (MODE == 2 || MODE == 3) ? ((threadIdx.x * 37 + i * 101) % bins)
+            : MODE == 4 ? ((threadIdx.x + i * 64) % bins)          // lane-distinct banks
+            : MODE == 5 ? ((threadIdx.x & ~31) + i * 8) % bins      // whole warp on one address
+            : (x >> 8) % bins;
     if (MODE == 0 || MODE == 2) atomicAdd(&h64[b], (unsigned long long)(x & 7));
     else atomicAdd(&h32[b], x & 7);
   }
@@ -23,9 +26,9 @@ __global__ void k(unsigned long long* out, int iters, int bins) {
 int main() {
   unsigned long long* d; cudaMalloc(&d, 4096 * 8);
   int iters = 4096;
-  for (int mode = 0; mode < 4; ++mode) for (int bins : {512, 4096, 16384}) for (int thr : {256, 512, 1024}) {
+  for (int mode = 1; mode < 6; mode += (mode == 1 ? 2 : 1)) for (int bins : {4096, 16384}) for (int thr : {256, 1024}) {
     size_t sm = bins * 8;
-    void (*f)(unsigned long long*, int, int) = mode == 0 ? k<0> : mode == 1 ? k<1> : mode == 2 ? k<2> : k<3>;
+    void (*f)(unsigned long long*, int, int) = mode == 0 ? k<0> : mode == 1 ? k<1> : mode == 2 ? k<2> : mode == 3 ? k<3> : mode == 4 ? k<4> : k<5>;
     cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 200000);
     cudaEvent_t a, b; cudaEventCreate(&a); cudaEventCreate(&b);
     f<<<148, thr, sm>>>(d, iters, bins);
