@@ -1,7 +1,8 @@
 """Benchmark of the hot path on BASELINE.json config 2.
 
 One step = build (A0) + critical points (A1-A2) + exact ECT and Radon (A3-A5)
-+ hybrid transform (A6, kappa = sin as in the paper's experiments P:140, fp64)
++ hybrid transform (A6, kappa = sin as in the paper's experiments P:140, fp64;
+computed from K2's merged histogram, eucalc_transforms_ht = NEXT row f2)
 for a batch of 1024 synthetic 28x28 u8 blob images AND its binarised variant
 (BJ:8), vertex construction, 256 integer directions in [-16,16]^2.
 
@@ -131,9 +132,9 @@ def run_step(eu, torch, imgs_dev, dirs, record=None):
     crs = [eu.critical_points(cx) for cx in cxs]
     out = []
     for cx, cr in zip(cxs, crs):
-        r = eu.transforms(cr, dirs, elem_bytes="auto", share_heights=True)
-        ht = eu.hybrid(cr, dirs, HT_KERNEL, 1.0, "f64")
-        out.append((cx, cr, r, ht))
+        # ECT + Radon + HT in one pass over the merged histogram (eucalc_transforms_ht)
+        r = eu.transforms(cr, dirs, elem_bytes="auto", share_heights=True, ht=(HT_KERNEL, 1.0, "f64"))
+        out.append((cx, cr, r, r["ht"]))
     return out
 
 
@@ -145,8 +146,9 @@ def run_step_e2e(eu, torch, imgs_host, dirs):
     crs = [eu.critical_points(cx) for cx in cxs]
     for img, cx, cr in zip(imgs_host, cxs, crs):
         h2d += img.numel() * img.element_size()
-        r = eu.transforms(cr, dirs, elem_bytes="auto", share_heights=True, device="cpu")  # D2H inside the ABI
-        ht = eu.hybrid(cr, dirs, HT_KERNEL, 1.0, "f64", device="cpu")
+        r = eu.transforms(cr, dirs, elem_bytes="auto", share_heights=True, device="cpu",
+                          ht=(HT_KERNEL, 1.0, "f64"))  # D2H inside the ABI
+        ht = r.pop("ht")
         for k, st in r.items():
             n = int(st["offsets"][-1])
             eb = st["value"].element_size()
@@ -232,8 +234,8 @@ def gpu_arm(args):
         no = int(r["ordinary"]["offsets"][S])
         eb = r["ect"]["value"].element_size()
         lists = list_bytes(cr, dirs)
-        # ECT (h,v) + ordinary (h,v) + classical (v; heights shared) + 3 offset arrays
-        k2_bytes += lists + ne * 2 * eb + no * 2 * eb + ne * eb + 3 * (S + 1) * 8
+        # ECT (h,v) + ordinary (h,v) + classical (v; heights shared) + 3 offset arrays + HT (f64)
+        k2_bytes += lists + ne * 2 * eb + no * 2 * eb + ne * eb + 3 * (S + 1) * 8 + S * 8
     k2_bytes /= 2  # per launch (two variants per step)
     peak, peak_src = peaks()
     achieved = k2_bytes / (k2_launch_ms / 1e3) / 1e9
@@ -268,7 +270,8 @@ def gpu_arm(args):
             "config": {
                 "workload": "BASELINE.json configs[1]: 1024 x 28x28 u8 Gaussian-blob images + binary variant "
                             "(>=128), vertex construction, 256 integer directions in [-16,16]^2; "
-                            "ECT + Radon (all three streams) + HT (kappa=sin, fp64) per image-direction",
+                            "ECT + Radon (all three streams) + HT (kappa=sin, fp64) per image-direction "
+                            "(HT fused into K2, eucalc_transforms_ht)",
                 "images_per_gpu": 2 * IMAGES_PER_SHARD, "directions": NDIRS, "parallelism": f"dp{world}",
                 "l2": "flushed between timed steps (256 MB write, untimed)",
                 "output": "CSR, int32 heights/values, classical heights shared with ECT",

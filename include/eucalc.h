@@ -137,6 +137,18 @@ eucalc_status eucalc_output_bound(const eucalc_critical *cr, const int32_t *dirs
 eucalc_status eucalc_transforms(const eucalc_critical *cr, const int32_t *dirs, int64_t D,
                                 eucalc_steps *ect, eucalc_steps *ordinary, eucalc_steps *classical,
                                 int64_t *required_out, void *stream);
+/* eucalc_transforms plus the hybrid transform of every (image, direction) from
+ * the same merged height histogram (NEXT row f2): HT(xi) = -sum_h H_J(h) kbar(t(h)),
+ * H_J(h) the sum of J over the critical points at lattice height h — Lemma 2's
+ * sum with equal heights grouped, so one kbar (tabulated per lattice
+ * u, E21) per distinct height instead of one per ordinary point. kernel, param,
+ * precision and ht_out ([batch][D], host or device) as for eucalc_hybrid; the
+ * ordinary stream must be requested. Deterministic (fixed-order sums). Errors
+ * as for eucalc_transforms and eucalc_hybrid. */
+eucalc_status eucalc_transforms_ht(const eucalc_critical *cr, const int32_t *dirs, int64_t D,
+                                   eucalc_steps *ect, eucalc_steps *ordinary, eucalc_steps *classical,
+                                   int kernel, double param, int precision, void *ht_out,
+                                   int64_t *required_out, void *stream);
 eucalc_status eucalc_ect(const eucalc_critical *cr, const int32_t *dirs, int64_t D,
                          eucalc_steps *ect, int64_t *required_out, void *stream);
 eucalc_status eucalc_radon(const eucalc_critical *cr, const int32_t *dirs, int64_t D,

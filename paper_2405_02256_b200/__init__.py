@@ -60,6 +60,8 @@ def lib():
         L.eucalc_output_bound.argtypes = [P, P, I64, ctypes.POINTER(I64), ctypes.POINTER(I64), P]
         SP = ctypes.POINTER(_Steps)
         L.eucalc_transforms.argtypes = [P, P, I64, SP, SP, SP, ctypes.POINTER(I64), P]
+        L.eucalc_transforms_ht.argtypes = [P, P, I64, SP, SP, SP, I32, ctypes.c_double, I32, P,
+                                           ctypes.POINTER(I64), P]
         L.eucalc_ect.argtypes = [P, P, I64, SP, ctypes.POINTER(I64), P]
         L.eucalc_radon.argtypes = [P, P, I64, SP, SP, ctypes.POINTER(I64), P]
         L.eucalc_hybrid.argtypes = [P, P, I64, I32, ctypes.c_double, I32, P, P]
@@ -78,7 +80,7 @@ def lib():
         for f in ("eucalc_build_complex", "eucalc_destroy_complex", "eucalc_critical_points",
                   "eucalc_destroy_critical", "eucalc_critical_counts", "eucalc_critical_export",
                   "eucalc_output_bound", "eucalc_transforms", "eucalc_ect", "eucalc_radon",
-                  "eucalc_hybrid", "eucalc_hybrid_ex", "eucalc_height_map", "eucalc_evaluate",
+                  "eucalc_hybrid", "eucalc_hybrid_ex", "eucalc_height_map", "eucalc_evaluate", "eucalc_transforms_ht",
                   "eucalc_vectorize"):
             getattr(L, f).restype = St
         _lib = L
@@ -232,19 +234,51 @@ def _alloc_steps(torch, S, cap, elem_bytes, device, with_height=True):
     return dict(offsets=off, height=h, value=v), st
 
 
+def _alloc_all(torch, S, cap, elem_bytes, device, names, share):
+    """All requested CSR streams carved out of ONE allocation (one allocator call
+    instead of up to nine): offsets first (8-byte aligned), then heights/values."""
+    dt = {2: torch.int16, 4: torch.int32, 8: torch.int64}[elem_bytes]
+    pin = device == "cpu" and torch.cuda.is_available()
+    cap1 = max(cap, 1)
+    arr = cap1 * elem_bytes
+    arr = (arr + 255) // 256 * 256
+    offb = ((S + 1) * 8 + 255) // 256 * 256
+    plan = []
+    total = 0
+    for name in names:
+        has_h = not (name == "classical" and share)
+        plan.append((name, total, has_h))
+        total += offb + arr * (2 if has_h else 1)
+    buf = torch.empty(total, dtype=torch.uint8, device=device, pin_memory=pin)
+    res, sts = {}, {}
+    for name, o, has_h in plan:
+        off = buf[o:o + (S + 1) * 8].view(torch.int64)
+        p = o + offb
+        h = None
+        if has_h:
+            h = buf[p:p + cap1 * elem_bytes].view(dt)
+            p += arr
+        v = buf[p:p + cap1 * elem_bytes].view(dt)
+        res[name] = dict(offsets=off, height=h, value=v)
+        sts[name] = _Steps(off.data_ptr(), h.data_ptr() if h is not None else 0, v.data_ptr(), cap, elem_bytes, 0)
+    return res, sts
+
+
 def transforms(cr: Critical, dirs, ect=True, ordinary=True, classical=True, elem_bytes=8, device="cuda",
-               share_heights=False, stream=None):
+               share_heights=False, stream=None, ht=None):
     """eucalc_transforms: canonical ECT (T,E) and Radon (T_o,E'), (T_c,E_c) for every
     (image, direction), as CSR torch tensors on `device` ("cuda" or "cpu").
 
     elem_bytes: 2, 4 or 8 (int16/int32/int64 heights and values), or "auto" for
     the narrowest width the library accepts (E_RANGE -> next width).
     share_heights=True lets the classical stream reuse the ECT heights (T_c = T,
-    Lemma 6) instead of writing them twice; its "height" is then the ECT tensor."""
+    Lemma 6) instead of writing them twice; its "height" is then the ECT tensor.
+    ht=(kernel, param, precision) also returns res["ht"] [batch, D], the hybrid
+    transform from the same merged histogram (eucalc_transforms_ht, NEXT f2)."""
     if elem_bytes == "auto":
         for eb in (2, 4):
             try:
-                return transforms(cr, dirs, ect, ordinary, classical, eb, device, share_heights, stream)
+                return transforms(cr, dirs, ect, ordinary, classical, eb, device, share_heights, stream, ht)
             except EucalcError as e:
                 if e.status != E_RANGE:
                     raise
@@ -254,22 +288,30 @@ def transforms(cr: Critical, dirs, ect=True, ordinary=True, classical=True, elem
     d = _dirs_i32(dirs)
     D = int(d.shape[0])
     S = cr.cx.batch * D
-    bound, _ = cr.output_bound(d)
-    res = {}
-    sts = [None, None, None]
-    for i, (name, want) in enumerate((("ect", ect), ("ordinary", ordinary), ("classical", classical))):
-        if not want:
-            continue
-        share = name == "classical" and share_heights and ect
-        res[name], sts[i] = _alloc_steps(torch, S, bound, elem_bytes, device, with_height=not share)
-        if share:
-            res[name]["height"] = res["ect"]["height"]
-            sts[i].height = sts[0].height
+    st = _stream(stream if stream is not None else cr.stream)
     p, keep = _ptr(d)
+    be, bo = ctypes.c_int64(), ctypes.c_int64()
+    _check(lib().eucalc_output_bound(cr._h, p, D, ctypes.byref(be), ctypes.byref(bo), st))
+    bound = be.value
+    names = [n for n, want in (("ect", ect), ("ordinary", ordinary), ("classical", classical)) if want]
+    share = share_heights and ect and classical
+    res, sts = _alloc_all(torch, S, bound, elem_bytes, device, names, share)
+    if share:
+        res["classical"]["height"] = res["ect"]["height"]
+        sts["classical"].height = sts["ect"].height
     req = ctypes.c_int64()
-    refs = [ctypes.byref(s) if s is not None else None for s in sts]
-    _check(lib().eucalc_transforms(cr._h, p, D, refs[0], refs[1], refs[2], ctypes.byref(req),
-                                   _stream(stream if stream is not None else cr.stream)), req.value)
+    refs = [ctypes.byref(sts[n]) if n in sts else None for n in ("ect", "ordinary", "classical")]
+    if ht is None:
+        _check(lib().eucalc_transforms(cr._h, p, D, refs[0], refs[1], refs[2], ctypes.byref(req), st), req.value)
+    else:
+        kern, param, prec = ht
+        pin = device == "cpu" and torch.cuda.is_available()
+        out = torch.empty((cr.cx.batch, D), dtype=torch.float32 if prec == "f32" else torch.float64, device=device,
+                          pin_memory=pin)
+        _check(lib().eucalc_transforms_ht(cr._h, p, D, refs[0], refs[1], refs[2], KERNELS[kern], float(param),
+                                          PRECISIONS[prec], ctypes.c_void_p(out.data_ptr()), ctypes.byref(req), st),
+               req.value)
+        res["ht"] = out
     return res
 
 

@@ -1,6 +1,7 @@
 // eucalc C ABI — host runtime (handles, validation, capacity protocol, launches).
 // See include/eucalc.h for the contract of every entry point.
 #include <algorithm>
+#include <atomic>
 #include <cstdio>
 #include <cstring>
 #include <map>
@@ -149,6 +150,9 @@ struct DirPlan {
     int R_max = 0;
     int dp = 0;  // all directions fit int8 and the complex is byte-aligned
     int64_t U0 = 0, U1 = 0;  // range of u = 2H - L*csum over all directions (K3 kbar table)
+    // per antipodal pair q: the height ranges R of its directions, sorted, with prefix sums
+    std::vector<std::vector<int64_t>> Rq, preq;
+    uint64_t id = 0;         // unique per plan (bound cache key)
 };
 
 eucalc_status plan_dirs(const Complex *cx, const int32_t *dirs, int64_t D, cudaStream_t st, DirPlan &p) {
@@ -211,6 +215,17 @@ eucalc_status plan_dirs(const Complex *cx, const int32_t *dirs, int64_t D, cudaS
         if (d == 0) p.dp = cx->aligned;
         if (!fits8) p.dp = 0;
     }
+    const int Q = 1 << (n - 1);
+    p.Rq.assign(Q, {});
+    p.preq.assign(Q, {});
+    for (int64_t d = 0; d < D; ++d) p.Rq[p.info[d].q].push_back(p.info[d].R);
+    for (int q = 0; q < Q; ++q) {
+        std::sort(p.Rq[q].begin(), p.Rq[q].end());
+        p.preq[q].assign(p.Rq[q].size() + 1, 0);
+        for (size_t i = 0; i < p.Rq[q].size(); ++i) p.preq[q][i + 1] = p.preq[q][i] + p.Rq[q][i];
+    }
+    static std::atomic<uint64_t> next_id{1};
+    p.id = next_id++;
     return EUCALC_OK;
 }
 
@@ -315,6 +330,7 @@ eucalc_status get_plan(const Complex *cx, const int32_t *dirs, int64_t D, cudaSt
 }
 
 eucalc_status sync_counts(Critical *cr, cudaStream_t st) {
+    std::lock_guard<std::mutex> lk(cr->mu);
     if (cr->have_host) return EUCALC_OK;
     (void)st;
     const Complex *cx = cr->cx;
@@ -348,22 +364,23 @@ eucalc_status sync_counts(Critical *cr, cudaStream_t st) {
 eucalc_status bounds(Critical *cr, const DirPlan &p, cudaStream_t st, int64_t &bound) {
     eucalc_status s = sync_counts(cr, st);
     if (s != EUCALC_OK) return s;
+    std::lock_guard<std::mutex> lk(cr->mu);
+    if (cr->bound_plan == p.id && p.id) {  // same critical handle and direction plan
+        bound = cr->bound_val;
+        return EUCALC_OK;
+    }
     bound = 0;
-    const int64_t D = (int64_t)p.info.size();
-    for (int q = 0; q < cr->Q; ++q) {
-        std::vector<int64_t> R;
-        for (int64_t d = 0; d < D; ++d)
-            if (p.info[d].q == q) R.push_back(p.info[d].R);
+    for (int q = 0; q < cr->Q && q < (int)p.Rq.size(); ++q) {
+        const std::vector<int64_t> &R = p.Rq[q], &pre = p.preq[q];
         if (R.empty()) continue;
-        std::sort(R.begin(), R.end());
-        std::vector<int64_t> pre(R.size() + 1, 0);
-        for (size_t i = 0; i < R.size(); ++i) pre[i + 1] = pre[i] + R[i];
         for (int64_t b = 0; b < cr->cx->batch; ++b) {
             const int64_t c = cr->h_count[b * cr->Q + q];
             const size_t k = std::upper_bound(R.begin(), R.end(), c) - R.begin();  // R[<k] <= c
             bound += pre[k] + (int64_t)(R.size() - k) * c;
         }
     }
+    cr->bound_plan = p.id;
+    cr->bound_val = bound;
     return EUCALC_OK;
 }
 
@@ -845,10 +862,27 @@ eucalc_status eucalc_output_bound(const eucalc_critical *ccr, const int32_t *dir
     return EUCALC_OK;
 }
 
-eucalc_status eucalc_transforms(const eucalc_critical *ccr, const int32_t *dirs, int64_t D, eucalc_steps *ect,
-                                eucalc_steps *ordinary, eucalc_steps *classical, int64_t *required_out,
-                                void *stream) {
+}  // extern "C"
+
+namespace {
+struct HtReq {
+    int kernel, precision;
+    double param;
+    void *out;
+};
+
+eucalc_status transforms_impl(const eucalc_critical *ccr, const int32_t *dirs, int64_t D, eucalc_steps *ect,
+                              eucalc_steps *ordinary, eucalc_steps *classical, const HtReq *ht, int64_t *required_out,
+                              void *stream) {
     if (!ccr) return fail(EUCALC_E_STATE, "NULL handle");
+    if (ht) {
+        if (ht->kernel < EUCALC_K_GAUSS || ht->kernel > EUCALC_K_EXP) return fail(EUCALC_E_ARG, "bad kernel");
+        if (ht->precision != EUCALC_F32 && ht->precision != EUCALC_F64) return fail(EUCALC_E_ARG, "bad precision");
+        if ((ht->kernel == EUCALC_K_GAUSS || ht->kernel == EUCALC_K_COS) && !(ht->param > 0))
+            return fail(EUCALC_E_ARG, "param must be > 0");
+        if (D > 0 && !ht->out) return fail(EUCALC_E_ARG, "ht_out is NULL");
+        if (!ordinary) return fail(EUCALC_E_ARG, "the fused HT needs the ordinary stream");
+    }
     eucalc_critical *cr = const_cast<eucalc_critical *>(ccr);
     const Complex *cx = cr->cx;
     cudaStream_t st = (cudaStream_t)stream;
@@ -930,9 +964,32 @@ eucalc_status eucalc_transforms(const eucalc_critical *ccr, const int32_t *dirs,
         free_scratch();
         return fail(EUCALC_E_NOMEM, "scratch");
     }
+    // fused HT: the kbar table over the directions' u range, and the output
+    const int64_t U = p.U1 - p.U0 + 1;
+    double *d_tab = nullptr;
+    void *d_ht = nullptr;
+    const bool ht_host = ht && !is_device_ptr(ht->out);
+    const size_t ht_osz = ht && ht->precision == EUCALC_F32 ? 4 : 8;
+    if (ht) {
+        d_tab = (double *)dalloc(12 * (size_t)U);
+        d_ht = ht_host ? dalloc(ht_osz * S) : ht->out;
+        if (!d_tab || !d_ht) {
+            free_scratch();
+            return fail(EUCALC_E_NOMEM, "HT table");
+        }
+    }
     cudaError_t e = cudaMemsetAsync(flags, 0, sizeof(unsigned long long) * S, st);
     if (e == cudaSuccess) e = cudaMemsetAsync(ticket, 0, sizeof(unsigned int) * 4, st);
+    if (e == cudaSuccess && ht)
+        e = launch_k3_table_only(ht->kernel, ht->param, cx->L, p.U0, U, d_tab, (float *)(d_tab + U), st);
     if (e == cudaSuccess) {
+        a.ht_tab = d_tab;
+        a.ht_U0 = p.U0;
+        a.L = cx->L;
+        a.csum = pe->d_csum;
+        a.ht_scale = ht ? k3_scale(ht->kernel, ht->param) : 0.0;
+        a.ht_prec = ht ? ht->precision : 0;
+        a.ht_out = d_ht;
         a.rec = cr->d_rec;
         a.wide = cr->wide;
         a.vcap = cr->vcap;
@@ -992,10 +1049,28 @@ eucalc_status eucalc_transforms(const eucalc_critical *ccr, const int32_t *dirs,
                 e = cudaMemcpyAsync(o->height, dev[i].h, nbytes, cudaMemcpyDeviceToHost, st);
         }
     }
+    if (e == cudaSuccess && ht_host) e = cudaMemcpyAsync(ht->out, d_ht, ht_osz * S, cudaMemcpyDeviceToHost, st);
     free_scratch();
-    if (e == cudaSuccess && host_out) e = cudaStreamSynchronize(st);
+    if (e == cudaSuccess && (host_out || ht_host)) e = cudaStreamSynchronize(st);
     if (e != cudaSuccess) return cuda_fail(e, "transforms");
     return EUCALC_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+eucalc_status eucalc_transforms(const eucalc_critical *cr, const int32_t *dirs, int64_t D, eucalc_steps *ect,
+                                eucalc_steps *ordinary, eucalc_steps *classical, int64_t *required_out,
+                                void *stream) {
+    return transforms_impl(cr, dirs, D, ect, ordinary, classical, nullptr, required_out, stream);
+}
+
+eucalc_status eucalc_transforms_ht(const eucalc_critical *cr, const int32_t *dirs, int64_t D, eucalc_steps *ect,
+                                   eucalc_steps *ordinary, eucalc_steps *classical, int kernel, double param,
+                                   int precision, void *ht_out, int64_t *required_out, void *stream) {
+    const HtReq h{kernel, precision, param, ht_out};
+    return transforms_impl(cr, dirs, D, ect, ordinary, classical, &h, required_out, stream);
 }
 
 eucalc_status eucalc_ect(const eucalc_critical *cr, const int32_t *dirs, int64_t D, eucalc_steps *ect,

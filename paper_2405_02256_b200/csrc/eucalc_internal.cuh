@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <mutex>
 #include <string>
 
 #include "../../include/eucalc.h"
@@ -57,6 +58,9 @@ struct Critical {
     int64_t max_count = 0;
     int64_t max_abs_sum = 0;
     int64_t max_rec = 0;
+    std::mutex mu;            // guards the host caches below (concurrent read-only use)
+    uint64_t bound_plan = 0;  // eucalc_output_bound cache: direction plan id -> bound
+    int64_t bound_val = 0;
     cudaStream_t owner_stream = nullptr;
     cudaEvent_t k1_done = nullptr;  // after the async read-back of counts/stats
     void *pinned = nullptr;         // pinned host copy: int32 counts, then int64 stats
@@ -127,6 +131,13 @@ struct K2Args {
     unsigned int *ticket;       // [4] ticket counters (zeroed)
     int *cnt_c, *cnt_o;         // [batch*D] per-segment counts (warp regime)
     uint2 *slab;                // [batch*D][33] merged runs of lists <= 32 records, or NULL
+    // fused HT (NEXT f2): kbar table (fp64) over u in [ht_U0, ...), or NULL
+    const double *ht_tab;
+    int64_t ht_U0, L;
+    const int32_t *csum;        // [D]
+    double ht_scale;            // HT = ht_scale * sum_h H_J(h) f(u(h))
+    int ht_prec;
+    void *ht_out;               // [batch][D]
 };
 cudaError_t launch_k2(const K2Args &a, cudaStream_t s, int num_sms);
 
@@ -162,6 +173,10 @@ struct K3Args {
 int k3_chunk(bool table);
 size_t k3_table_smem(bool f64, long long U);
 cudaError_t launch_k3(const K3Args &a, cudaStream_t s);
+// kbar table for u in [U0, U0 + U) (fp64 and fp32 copies) and the HT scale of each kernel
+cudaError_t launch_k3_table_only(int kernel, double param, int64_t L, int64_t U0, int64_t U, double *t64, float *t32,
+                                 cudaStream_t s);
+double k3_scale(int kernel, double param);
 
 // K4: evaluation / vectorisation (NEXT f1)
 struct K4Args {

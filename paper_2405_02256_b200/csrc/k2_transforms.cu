@@ -215,17 +215,32 @@ __device__ __forceinline__ void count_group(const Hist<PACK, SWZ> &hs, int base,
 
 // Which streams an emission writes: compile-time for the common requests,
 // kModeAny checks K2Args at run time.
-constexpr int kEct = 1, kOrd = 2, kCls = 4, kAlias = 8, kModeAny = 16;
+constexpr int kEct = 1, kOrd = 2, kCls = 4, kAlias = 8, kModeAny = 16, kHt = 32;
 
 template <typename OutT>
 struct OutPtrs {
     OutT *eh, *ev, *oh, *ov, *ch, *cv;
+    const double *tab;  // fused HT (NEXT f2): kbar table over u = 2H - L*csum, or NULL
     bool ect, ord, cls, alias;
     __device__ explicit OutPtrs(const K2Args &a)
         : eh((OutT *)a.ect.h), ev((OutT *)a.ect.v), oh((OutT *)a.ord.h), ov((OutT *)a.ord.v),
-          ch((OutT *)a.cls.h), cv((OutT *)a.cls.v), ect(a.do_ect), ord(a.do_ord), cls(a.do_cls),
+          ch((OutT *)a.cls.h), cv((OutT *)a.cls.v), tab(a.ht_tab), ect(a.do_ect), ord(a.do_ord), cls(a.do_cls),
           alias(a.cls_alias) {}
 };
+
+// Fused HT (NEXT row f2): the merged histogram already holds, per lattice
+// height h, H_J(h) = sum of J over the records at h, so
+//   HT(xi) = -sum_x J(x) kbar(t(x)) = -sum_h H_J(h) kbar(t(h))      (Lemma 2)
+// costs one table lookup per nonzero bin instead of one kbar per record.
+// `tab_off` = -L*csum - U0, so the table index of height h is 2h + tab_off.
+__device__ __forceinline__ void ht_write(const K2Args &a, long long s, double acc) {
+    const double v = a.ht_scale * acc;
+    if (a.ht_prec == EUCALC_F32) reinterpret_cast<float *>(a.ht_out)[s] = (float)v;
+    else reinterpret_cast<double *>(a.ht_out)[s] = v;
+}
+__device__ __forceinline__ long long ht_tab_off(const K2Args &a, long long d) {
+    return -a.L * (long long)a.csum[d] - a.ht_U0;
+}
 
 template <int MODE, typename OutT>
 __device__ __forceinline__ void put_c(const OutPtrs<OutT> &o, int p, int h, int e, int cv) {
@@ -256,7 +271,8 @@ __device__ __forceinline__ void put_o(const OutPtrs<OutT> &o, int p, int h, int 
 // positions are int32 (< 2^31 entries per call, host-checked).
 template <int MODE, typename OutT, bool PACK, bool SWZ>
 __device__ __forceinline__ void emit_group(const OutPtrs<OutT> &o, const Hist<PACK, SWZ> &hs, int base, int h0,
-                                           int &e_run, int &r_run, int &pc, int &po) {
+                                           int &e_run, int &r_run, int &pc, int &po, double &ht,
+                                           long long tab_off) {
     const int lane = threadIdx.x & 31;
     int wc[4], wj[4];
     hs.load4(base + 4 * lane, wc, wj, true);
@@ -281,6 +297,8 @@ __device__ __forceinline__ void emit_group(const OutPtrs<OutT> &o, const Hist<PA
         r += wj[s];
         if (wc[s]) put_c<MODE>(o, p_c++, hb + s, e, rb + wc[s]);
         if (wj[s]) put_o<MODE>(o, p_o++, hb + s, r);
+        const bool do_ht = (MODE == kModeAny) ? (o.tab != nullptr) : ((MODE & kHt) != 0);
+        if (do_ht && wj[s]) ht = fma((double)wj[s], __ldg(o.tab + 2 * (long long)(hb + s) + tab_off), ht);
     }
     const int tc = __shfl_sync(0xffffffffu, ic, 31);
     pc += tc & 0xffff;
@@ -427,6 +445,13 @@ __global__ void __launch_bounds__(kWarpThreads) k2w_count(K2Args a, int rcap, in
                                                   (unsigned)(ec & 0xffff) | ((unsigned)r.pj << 16));
                 if ((threadIdx.x & 31) == 0) sl[32] = make_uint2(mc, mo);
             }
+            if (a.ht_tab) {
+                // fused HT of a sparse segment: one term per merged run (fixed-order tree sum)
+                double acc = 0.0;
+                if (r.emit_o) acc = (double)r.run_j * __ldg(a.ht_tab + 2 * (long long)(di.hlo + r.h) + ht_tab_off(a, d));
+                for (int k = 16; k; k >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, k);
+                if ((threadIdx.x & 31) == 0) ht_write(a, s, acc);
+            }
         } else {
             fill_segment<RecT>(a, hs, b, di);
             for (int base = 0; base < di.R; base += kGroup) count_group(hs, base, c, o, true);
@@ -475,8 +500,14 @@ __global__ void __launch_bounds__(kWarpThreads) k2w_emit(K2Args a, int rcap) {
         } else {
             fill_segment<RecT>(a, hs, b, di);
             int e_run = 0, r_run = 0;
+            double ht = 0.0;
+            const long long toff = (MODE & kHt) || (MODE == kModeAny && o.tab) ? ht_tab_off(a, d) : 0;
             for (int base = 0; base < di.R; base += kGroup)
-                emit_group<MODE>(o, hs, base, di.hlo, e_run, r_run, pc, po);
+                emit_group<MODE>(o, hs, base, di.hlo, e_run, r_run, pc, po, ht, toff);
+            if ((MODE & kHt) || (MODE == kModeAny && o.tab)) {
+                for (int k = 16; k; k >>= 1) ht += __shfl_xor_sync(0xffffffffu, ht, k);
+                if ((threadIdx.x & 31) == 0) ht_write(a, s, ht);
+            }
         }
         __syncwarp();
     }
@@ -636,6 +667,7 @@ __global__ void __launch_bounds__(kBlockThreads, 1) k2_block(K2Args a, long long
     __shared__ long long s_seg;
     __shared__ int s_wsum[kBlockWarps][4];  // per-warp (nc, no, sum wc, sum wj)
     __shared__ long long s_exc[2];
+    __shared__ double s_ht[kBlockWarps];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     constexpr int words = PACK ? 1 : 2;
     const OutPtrs<OutT> outp(a);
@@ -694,6 +726,8 @@ __global__ void __launch_bounds__(kBlockThreads, 1) k2_block(K2Args a, long long
         // phase B: emit window by window
         long long pc_carry = s_exc[0], po_carry = s_exc[1];
         int e_carry = 0, r_carry = 0;
+        double ht = 0.0;
+        const long long ht_off = outp.tab ? ht_tab_off(a, d) : 0;
         for (int w = 0; w < nwin; ++w) {
             const int lo = w * win, wb = min(win, di.R - lo);
             if (nwin > 1) {
@@ -741,12 +775,22 @@ __global__ void __launch_bounds__(kBlockThreads, 1) k2_block(K2Args a, long long
                 tsj += s_wsum[k][3];
             }
             for (int base = b0; base < b1; base += kGroup)
-                emit_group<kModeAny>(outp, hs, base, di.hlo + lo, er, rr, pc, po);
+                emit_group<kModeAny>(outp, hs, base, di.hlo + lo, er, rr, pc, po, ht, ht_off);
             pc_carry += tc;
             po_carry += to;
             e_carry += tsc;
             r_carry += tsj;
             __syncthreads();
+        }
+        if (outp.tab) {  // fused HT: warp partials, then a fixed-order sum over warps
+            for (int k = 16; k; k >>= 1) ht += __shfl_xor_sync(0xffffffffu, ht, k);
+            if (lane == 0) s_ht[warp] = ht;
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                double t = 0.0;
+                for (int k = 0; k < kBlockWarps; ++k) t += s_ht[k];
+                ht_write(a, s, t);
+            }
         }
     }
 }
@@ -766,12 +810,15 @@ cudaError_t launch_t(const K2Args &a, cudaStream_t s, int num_sms) {
         void (*ke)(K2Args, int) = k2w_emit<RecT, OutT, PACK, kModeAny>;
         if (std::is_same<RecT, Rec16>::value) {
             const int mode = (a.do_ect ? kEct : 0) | (a.do_ord ? kOrd : 0) | (a.do_cls ? kCls : 0) |
-                             (a.do_cls && a.cls_alias ? kAlias : 0);
+                             (a.do_cls && a.cls_alias ? kAlias : 0) | (a.ht_tab ? kHt : 0);
             switch (mode) {
             case kEct: ke = k2w_emit<RecT, OutT, PACK, kEct>; break;
             case kOrd | kCls: ke = k2w_emit<RecT, OutT, PACK, kOrd | kCls>; break;
             case kEct | kOrd | kCls: ke = k2w_emit<RecT, OutT, PACK, kEct | kOrd | kCls>; break;
             case kEct | kOrd | kCls | kAlias: ke = k2w_emit<RecT, OutT, PACK, kEct | kOrd | kCls | kAlias>; break;
+            case kEct | kOrd | kCls | kAlias | kHt:
+                ke = k2w_emit<RecT, OutT, PACK, kEct | kOrd | kCls | kAlias | kHt>;
+                break;
             default: break;
             }
         }

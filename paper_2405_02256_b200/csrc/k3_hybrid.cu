@@ -371,6 +371,23 @@ cudaError_t launch_k3_table(const K3Args &a, cudaStream_t s) {
     return cudaSuccess;
 }
 
+cudaError_t launch_k3_table_only(int kernel, double param, int64_t L, int64_t U0, int64_t U, double *t64, float *t32,
+                                 cudaStream_t s) {
+    k3_table<<<(unsigned)((U + 255) / 256), 256, 0, s>>>(kernel, param, L, U0, U, t64, t32);
+    count_launch();
+    return cudaGetLastError();
+}
+
+double k3_scale(int kernel, double param) {
+    // HT = -sum J kbar; kbar = scale_k * f  (f is what the table holds)
+    switch (kernel) {
+    case EUCALC_K_GAUSS: return -param * sqrt(M_PI / 2.0);
+    case EUCALC_K_COS: return -param / (2.0 * M_PI);
+    case EUCALC_K_SIN: return 1.0;  // kbar = -cos
+    default: return -1.0;           // kbar = exp
+    }
+}
+
 cudaError_t launch_k3(const K3Args &a, cudaStream_t s) {
     dim3 grid((unsigned)a.nchunks, (unsigned)a.ntiles, (unsigned)a.batch);
     if (a.use_table) {
@@ -399,14 +416,7 @@ cudaError_t launch_k3(const K3Args &a, cudaStream_t s) {
     count_launch();
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
-    // HT = -sum J kbar; kbar = scale_k * f
-    double scale;
-    switch (a.kernel) {
-    case EUCALC_K_GAUSS: scale = -a.param * sqrt(M_PI / 2.0); break;
-    case EUCALC_K_COS: scale = -a.param / (2.0 * M_PI); break;
-    case EUCALC_K_SIN: scale = 1.0; break;  // kbar = -cos
-    default: scale = -1.0; break;           // kbar = exp
-    }
+    const double scale = k3_scale(a.kernel, a.param);
     const long long tot = a.batch * a.D;
     k3_combine<<<(unsigned)((tot + 255) / 256), 256, 0, s>>>(a, scale);
     count_launch();

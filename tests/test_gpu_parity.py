@@ -85,6 +85,23 @@ def check_ht(images, dirs, construction, cr, kernel, param, precision, pairs=Non
             assert abs(got - want) <= tol * max(abs(want), 1.0), (alg, kernel, precision, b, d, got, want)
 
 
+def check_fused_ht(images, dirs, construction, cr, kernel, param, precision, pairs=None, elem_bytes=8):
+    """eucalc_transforms_ht (HT from K2's merged histogram, NEXT f2) vs the oracle's
+    quadrature, and its representations vs eucalc_transforms."""
+    r = eu.transforms(cr, dirs, elem_bytes=elem_bytes, share_heights=True, ht=(kernel, param, precision))
+    out = r["ht"].cpu().numpy()
+    ref = oracle.ht_batch(images, dirs, construction, kernel, param, pairs=pairs)
+    tol = HT_TOL[precision]
+    for (b, d), want in ref.items():
+        got = float(out[b, d])
+        assert abs(got - want) <= tol * max(abs(want), 1.0), ("fused", kernel, precision, b, d, got, want)
+    plain = eu.transforms(cr, dirs, elem_bytes=elem_bytes, share_heights=True)
+    for k in ("ect", "ordinary", "classical"):
+        n = int(plain[k]["offsets"][-1])
+        assert torch.equal(plain[k]["offsets"], r[k]["offsets"])
+        assert torch.equal(plain[k]["value"][:n], r[k]["value"][:n])
+
+
 # ----------------------------------------------------------------------------- golden
 
 def test_ex4_golden_gpu():
@@ -131,6 +148,8 @@ def test_random_parity(case):
     check_transforms(images, dirs, construction, res)
     check_ht(images, dirs, construction, cr, "gauss", 1.0, "f64")
     check_ht(images, dirs, construction, cr, "cos", 64.0, "f32")
+    check_fused_ht(images, dirs, construction, cr, "sin", 1.0, "f64")
+    check_fused_ht(images, dirs, construction, cr, "gauss", 1.0, "f32")
 
 
 def test_block_regime_multiwindow():
@@ -139,6 +158,7 @@ def test_block_regime_multiwindow():
     dirs = np.concatenate([synth.random_directions(6, 2, 90, 5), np.array([[90, -89], [-90, 90]], np.int32)])
     cx, cr, res = run_gpu(img, dirs, "vertex")
     check_transforms(img, dirs, "vertex", res)
+    check_fused_ht(img, dirs, "vertex", cr, "cos", 7.5, "f64", pairs=[(0, 0), (0, 6), (0, 7)])
 
 
 def test_block_regime_3d_culled_windows():
@@ -288,6 +308,7 @@ def test_config2_small_full(variant, construction):
     _, cr, res = run_gpu(imgs, dirs, construction)
     check_transforms(imgs, dirs, construction, res)
     check_critical(imgs, construction, cr, imgs_to_check=range(4))
+    check_fused_ht(imgs, dirs, construction, cr, "sin", 1.0, "f64", pairs=[(0, 0), (3, 17), (15, 255)], elem_bytes=2)
 
 
 def test_config2_full_size_sampled():
@@ -300,6 +321,7 @@ def test_config2_full_size_sampled():
     pairs = [(int(b), int(d)) for b, d in zip(rng.integers(0, 1024, 300), rng.integers(0, 256, 300))]
     pairs += [(0, 0), (1023, 255)]
     check_transforms(imgs, dirs, "vertex", res, pairs=pairs)
+    check_fused_ht(imgs, dirs, "vertex", cr, "sin", 1.0, "f64", pairs=pairs[:40], elem_bytes=4)
 
 
 def test_config3_sampled():
