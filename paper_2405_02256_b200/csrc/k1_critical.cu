@@ -23,7 +23,8 @@
 // since J(eps) = Delta^-(eps) - Delta^-(-eps)). Warp ballot/popc + block scan
 // give the in-tile order; a decoupled look-back over the image's tiles (dynamic
 // ticket order) gives each tile's global offset, so the list order is
-// deterministic (tile-major, row-major within a tile) with a single pass.
+// deterministic (tile-major; within a tile by warp, vertex batch and lane) with
+// a single pass.
 // Tiles are boxes of <= kTileV vertices (the whole image when it fits; else
 // 64 x 32 in 2-D, 16 x 16 x 8 in 3-D), so a tile spans a narrow band of heights
 // in every direction; K1 records each tile's list offset for K2's culling.
@@ -37,6 +38,7 @@ namespace {
 
 constexpr int kThreads = 256;
 constexpr int kTileV = 2048;  // vertices per tile (max)
+constexpr int kPerWarp = kTileV / (kThreads / 32);  // staging slice per warp
 
 __host__ __device__ constexpr int pow3(int k) { return k == 0 ? 1 : 3 * pow3(k - 1); }
 
@@ -191,7 +193,6 @@ __global__ void __launch_bounds__(kThreads) k1_kernel(K1Args a) {
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     if (tid == 0) s_ticket = atomicAdd(a.ticket, 1u);
-    if (tid < Q) s_run[tid] = 0;
     if (tid < (1 << N) * 2) (&s_ostat[0][0])[tid] = 0;
     __syncthreads();
     const unsigned ticket = s_ticket;
@@ -216,6 +217,7 @@ __global__ void __launch_bounds__(kThreads) k1_kernel(K1Args a) {
     // cols x0-1 .. x0+TXe; one warp per region row, lanes along the row
     const TIn *img = reinterpret_cast<const TIn *>(a.img) + b * a.npix;
     const int SENT = (CONS == EUCALC_VERTEX) ? INT_MIN : INT_MAX;
+#pragma unroll 4
     for (int row = warp; row < RZ * RY; row += kThreads / 32) {
         const int pz = row / RY, ry = row - pz * RY;
         const int gy = y0 - 1 + ry, gz = (N == 3) ? z0 - 1 + pz : 0;
@@ -244,6 +246,9 @@ __global__ void __launch_bounds__(kThreads) k1_kernel(K1Args a) {
         max_rec[q] = 0;
     }
 
+    int wrun[Q];
+#pragma unroll
+    for (int q = 0; q < Q; ++q) wrun[q] = 0;
     for (int c0 = 0; c0 < TV; c0 += kThreads) {
         const int li = c0 + tid;
         const bool valid = li < TV;
@@ -272,36 +277,34 @@ __global__ void __launch_bounds__(kThreads) k1_kernel(K1Args a) {
             if (N >= 2) coord |= ((uint32_t)gy << a.sh[N - 2]);
             if (N == 3) coord |= ((uint32_t)(z0 + lz) << a.sh[0]);
         }
-        bool keep[Q];
-        unsigned bal[Q];
+        // warp-private compaction: warp w appends to its own slice of the
+        // staging area (no block barrier per vertex batch); the tile's order is
+        // (warp, batch, lane) and the slices are concatenated at copy-out
 #pragma unroll
         for (int q = 0; q < Q; ++q) {
-            keep[q] = dm[q] != 0 || dm[q ^ FULL] != 0;
-            bal[q] = __ballot_sync(0xffffffffu, keep[q]);
-            if (lane == 0) s_warp[warp][q] = __popc(bal[q]);
-            abs_sum[q] += abs(dm[q]) + abs(dm[q ^ FULL]);
-            max_rec[q] = max(max_rec[q], abs(dm[q]) + abs(dm[q ^ FULL]));
-        }
-        __syncthreads();
-#pragma unroll
-        for (int q = 0; q < Q; ++q) {
-            if (keep[q]) {
-                int pos = s_run[q] + __popc(bal[q] & ((1u << lane) - 1));
-                for (int w = 0; w < warp; ++w) pos += s_warp[w][q];
+            const bool keep = dm[q] != 0 || dm[q ^ FULL] != 0;
+            const unsigned bal = __ballot_sync(0xffffffffu, keep);
+            if (keep) {
                 RecT r;
                 r.c = coord;
                 r.a = dm[q];
                 r.b = dm[q ^ FULL];
-                stage[q * kTileV + pos] = r;
+                stage[q * kTileV + warp * kPerWarp + wrun[q] + __popc(bal & ((1u << lane) - 1))] = r;
             }
+            wrun[q] += __popc(bal);
+            abs_sum[q] += abs(dm[q]) + abs(dm[q ^ FULL]);
+            max_rec[q] = max(max_rec[q], abs(dm[q]) + abs(dm[q ^ FULL]));
         }
-        __syncthreads();
-        if (tid < Q) {
-            int tot = 0;
-            for (int w = 0; w < kThreads / 32; ++w) tot += s_warp[w][tid];
-            s_run[tid] += tot;
-        }
-        __syncthreads();
+    }
+    if (lane == 0) {
+#pragma unroll
+        for (int q = 0; q < Q; ++q) s_warp[warp][q] = wrun[q];
+    }
+    __syncthreads();
+    if (tid < Q) {
+        int tot = 0;
+        for (int w = 0; w < kThreads / 32; ++w) tot += s_warp[w][tid];
+        s_run[tid] = tot;
     }
 
     // ---- per-image statistics (order-independent integer sums: deterministic)
@@ -360,9 +363,11 @@ __global__ void __launch_bounds__(kThreads) k1_kernel(K1Args a) {
     RecT *out = reinterpret_cast<RecT *>(a.rec);
 #pragma unroll
     for (int q = 0; q < Q; ++q) {
-        RecT *dst = out + (b * Q + q) * a.vcap + s_excl[q];
-        const RecT *src = stage + q * kTileV;
-        for (int i = tid; i < s_run[q]; i += kThreads) dst[i] = src[i];
+        int before = 0;  // this warp's slice follows the slices of warps 0..warp-1
+        for (int w = 0; w < warp; ++w) before += s_warp[w][q];
+        RecT *dst = out + (b * Q + q) * a.vcap + s_excl[q] + before;
+        const RecT *src = stage + q * kTileV + warp * kPerWarp;
+        for (int i = lane; i < s_warp[warp][q]; i += 32) dst[i] = src[i];
     }
 }
 
