@@ -216,7 +216,6 @@ __global__ void __launch_bounds__(kThreads) k3_f64(K3Args a) {
 // is an LDS broadcast of the record, a DP4A, an LDS gather and the compensated
 // (fp32) or fp64 accumulation — precision-independent kbar cost, no SFU.
 constexpr int kChunkT = 8192;
-constexpr int kStageT = 2048;
 
 __global__ void k3_table(int kernel, double param, long long L, long long U0, long long U, double *t64, float *t32) {
     const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
@@ -256,9 +255,11 @@ template <typename RecT, bool F64, int DP>
 __global__ void __launch_bounds__(kThreads) k3t(K3Args a) {
     using T = typename std::conditional<F64, double, float>::type;
     using S = typename std::conditional<F64, int4, int2>::type;  // staged record: c, J (float bits / double)
+    constexpr int PER = F64 ? 2 : 4;                             // records staged per thread per chunk
     extern __shared__ __align__(16) unsigned char k3t_smem[];
-    S *srec = reinterpret_cast<S *>(k3t_smem);
-    T *tab = reinterpret_cast<T *>(srec + kStageT);
+    S *sbuf = reinterpret_cast<S *>(k3t_smem);  // two staging buffers of PER * blockDim records
+    const int stage_n = PER * blockDim.x;
+    T *tab = reinterpret_cast<T *>(sbuf + 2 * PER * kThreads);
     const int c = blockIdx.x, tile = blockIdx.y;
     const long long b = blockIdx.z;
     const int tlen = a.tile_len[tile];
@@ -276,34 +277,66 @@ __global__ void __launch_bounds__(kThreads) k3t(K3Args a) {
     for (int j = threadIdx.x; j < half; j += blockDim.x) tab[j] = gtab[start - a.U0 + 2 * (long long)j];
     // idx = (u - start) / 2 = H + off, off = (-L*csum - start) / 2 (exact: same parity)
     const int off = (int)((-a.L * (long long)a.csum[myd] - start) / 2);
-    // H = sum xs_k p_k = dp(c, xs8) when the direction is its pair's representative;
-    // records are stored for the pair's representative orthant, which is this
-    // direction's orthant up to the antipodal swap (J -> -J, handled at staging)
+    // H = sum xs_k p_k = dp(c, xs8): records carry the vertex coordinates; the
+    // pair's representative orthant is this direction's orthant up to the
+    // antipodal swap (J -> -J, handled at staging)
     const int sw = di0.swap;
     const RecT *list = reinterpret_cast<const RecT *>(a.rec) + (b * a.Q + di0.q) * a.vcap;
-    T acc0 = 0, acc1 = 0, cmp0 = 0, cmp1 = 0;
-    for (int s0 = beg; s0 < end; s0 += kStageT) {
-        const int cnt = min(kStageT, end - s0);
-        __syncthreads();
-        for (int i = threadIdx.x; i < cnt; i += blockDim.x) {
-            const RecT r = list[s0 + i];
-            const int j = sw ? (r.b - r.a) : (r.a - r.b);
-            if constexpr (F64) {
-                const double jd = (double)j;
-                srec[i] = make_int4((int)r.c, 0, __double2loint(jd), __double2hiint(jd));
-            } else {
-                srec[i] = make_int2((int)r.c, __float_as_int((float)j));
+    // staging, double-buffered: the next chunk's records are loaded into
+    // registers before the current chunk is consumed, and stored after it
+    RecT pre[PER];
+    auto load_chunk = [&](int s0) {
+#pragma unroll
+        for (int k = 0; k < PER; ++k) {
+            const int i = s0 + k * blockDim.x + threadIdx.x;
+            if (i < end) pre[k] = list[i];
+        }
+    };
+    auto store_chunk = [&](S *dst, int s0) {
+#pragma unroll
+        for (int k = 0; k < PER; ++k) {
+            const int li = k * blockDim.x + threadIdx.x;
+            if (s0 + li < end) {
+                const int j = sw ? (pre[k].b - pre[k].a) : (pre[k].a - pre[k].b);
+                if constexpr (F64) {
+                    const double jd = (double)j;
+                    dst[li] = make_int4((int)pre[k].c, 0, __double2loint(jd), __double2hiint(jd));
+                } else {
+                    dst[li] = make_int2((int)pre[k].c, __float_as_int((float)j));
+                }
             }
         }
-        __syncthreads();
+    };
+    T acc0 = 0, acc1 = 0, cmp0 = 0, cmp1 = 0;
+    if (beg < end) {
+        load_chunk(beg);
+        store_chunk(sbuf, beg);
+    }
+    __syncthreads();
+    int cur = 0;
+    for (int s0 = beg; s0 < end; s0 += stage_n) {
+        const int cnt = min(stage_n, end - s0);
+        const int nxt = s0 + stage_n;
+        if (nxt < end) load_chunk(nxt);  // in flight while this chunk is consumed
+        const S *srec = sbuf + cur * PER * kThreads;
         if (threadIdx.x < tlen) {
             // four independent record chains per iteration (LDS -> IDP -> LDS -> FMA)
             int i = 0;
             for (; i + 3 < cnt; i += 4) {
                 S r[4];
                 T k[4];
+                if constexpr (F64) {
 #pragma unroll
-                for (int u = 0; u < 4; ++u) r[u] = srec[i + u];
+                    for (int u = 0; u < 4; ++u) r[u] = srec[i + u];
+                } else {
+                    // two records per 16-byte broadcast load
+                    const int4 p0 = *reinterpret_cast<const int4 *>(srec + i);
+                    const int4 p1 = *reinterpret_cast<const int4 *>(srec + i + 2);
+                    r[0] = make_int2(p0.x, p0.y);
+                    r[1] = make_int2(p0.z, p0.w);
+                    r[2] = make_int2(p1.x, p1.y);
+                    r[3] = make_int2(p1.z, p1.w);
+                }
 #pragma unroll
                 for (int u = 0; u < 4; ++u) k[u] = tab[table_index<DP>((uint32_t)r[u].x, di.xs8, off)];
 #pragma unroll
@@ -332,6 +365,9 @@ __global__ void __launch_bounds__(kThreads) k3t(K3Args a) {
                 }
             }
         }
+        if (nxt < end) store_chunk(sbuf + (cur ^ 1) * PER * kThreads, nxt);
+        __syncthreads();
+        cur ^= 1;
     }
     if (threadIdx.x < tlen) {
         double tot;
@@ -359,7 +395,8 @@ int k3_chunk(bool table) { return table ? kChunkT : kChunk; }
 
 size_t k3_table_smem(bool f64, long long U) {
     const long long half = (U + 1) / 2 + 1;
-    return (f64 ? sizeof(int4) : sizeof(int2)) * kStageT + (f64 ? 8 : 4) * half;
+    // two staging buffers of PER * kThreads records (PER = 2 in fp64, 4 in fp32)
+    return (f64 ? sizeof(int4) * 2 : sizeof(int2) * 4) * 2 * kThreads + (f64 ? 8 : 4) * half;
 }
 
 cudaError_t launch_k3_table(const K3Args &a, cudaStream_t s) {
