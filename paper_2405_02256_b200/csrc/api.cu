@@ -1118,7 +1118,11 @@ eucalc_status eucalc_hybrid_ex(const eucalc_critical *ccr, const int32_t *dirs, 
     if (algorithm == EUCALC_HT_TABLE && !table_ok)
         return fail(EUCALC_E_ARG, "tabulated HT needs byte-aligned coordinates, |xs| <= 127 and a table that fits shared memory");
     const bool use_table = algorithm == EUCALC_HT_TABLE || (algorithm == EUCALC_HT_AUTO && table_ok);
-    const int chunk = k3_chunk(use_table);
+    // records per CTA: the kernel's chunk, shrunk (to >= 512) when the grid would
+    // not cover the SMs twice (few images / tiles, e.g. one large image)
+    int chunk = k3_chunk(use_table);
+    const int64_t ctas_per_chunk = (int64_t)pe->tstart.size() * cx->batch;
+    while (chunk > 512 && ctas_per_chunk * ((cr->max_count + chunk - 1) / chunk) < 2 * num_sms()) chunk /= 2;
     const int nchunks = (int)std::max<int64_t>(1, (cr->max_count + chunk - 1) / chunk);
     const size_t osz = precision == EUCALC_F32 ? 4 : 8;
     const bool host_out = !is_device_ptr(out);
@@ -1168,6 +1172,7 @@ eucalc_status eucalc_hybrid_ex(const eucalc_critical *ccr, const int32_t *dirs, 
         const int maxlen = *std::max_element(pe->tlen.begin(), pe->tlen.end());
         a.threads = std::max(32, (maxlen + 31) / 32 * 32);
         a.nchunks = nchunks;
+        a.chunk = chunk;
         a.partial = d_part;
         a.out = d_out;
         a.use_table = use_table ? 1 : 0;

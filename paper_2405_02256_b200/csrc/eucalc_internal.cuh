@@ -162,6 +162,7 @@ struct K3Args {
     int dp;                    // as K2Args::dp
     int threads;               // block size = longest tile rounded up to a warp
     int nchunks;
+    int chunk;                 // records per CTA
     double *partial;           // [batch][nchunks][D]
     void *out;                 // [batch][D]
     // tabulated kbar (use_table): u = 2H - L*csum in [U0, U0 + U)

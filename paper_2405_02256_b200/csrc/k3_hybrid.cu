@@ -57,7 +57,7 @@ __global__ void __launch_bounds__(kThreads) k3_f32(K3Args a) {
     const DirInfo di0 = a.dirs[d0];  // orthant shared by the tile
     const int n = a.count[b * a.Q + di0.q];
     const RecT *list = reinterpret_cast<const RecT *>(a.rec) + (b * a.Q + di0.q) * a.vcap;
-    const int beg = c * kChunk, end = min(n, beg + kChunk);
+    const int beg = c * a.chunk, end = min(n, beg + a.chunk);
     // per-direction constants
     const float x0 = (float)di.xs[0], x1 = (float)di.xs[1], x2 = (a.ndim == 3) ? (float)di.xs[2] : 0.f;
     const double L = (double)a.L;
@@ -140,7 +140,7 @@ __global__ void __launch_bounds__(kThreads) k3_f64(K3Args a) {
     const DirInfo di0 = a.dirs[a.order[a.tile_start[tile]]];
     const int n = a.count[b * a.Q + di0.q];
     const RecT *list = reinterpret_cast<const RecT *>(a.rec) + (b * a.Q + di0.q) * a.vcap;
-    const int beg = c * kChunk, end = min(n, beg + kChunk);
+    const int beg = c * a.chunk, end = min(n, beg + a.chunk);
     const int x0 = di.xs[0], x1 = di.xs[1], x2 = (a.ndim == 3) ? di.xs[2] : 0;
     const double L = (double)a.L;
     const double cs = (double)a.csum[myd];
@@ -268,7 +268,7 @@ __global__ void __launch_bounds__(kThreads) k3t(K3Args a) {
     const DirInfo di = a.dirs[myd];
     const DirInfo di0 = a.dirs[d0];
     const int n = a.count[b * a.Q + di0.q];
-    const int beg = c * kChunkT, end = min(n, beg + kChunkT);
+    const int beg = c * a.chunk, end = min(n, beg + a.chunk);
     // the tile's half table: u = start + 2 j, u == L*csum (mod 2)
     const int par = (int)((a.L * (long long)a.csum[d0]) & 1);
     const long long start = a.U0 + (((a.U0 & 1) != par) ? 1 : 0);

@@ -17,9 +17,9 @@
 // intrinsics (no contraction into an FMA), the exact double sequence the oracle
 // uses (E20).
 //
-// One warp per segment (image, direction); lanes take 32 consecutive queries and
-// binary-search the segment's breakpoints (read through L1; a segment's
-// heights are contiguous). Bound: the output write plus the log-depth reads.
+// One thread per (segment, query): a binary search over the segment's
+// breakpoints (read through L1; a segment's heights are contiguous). Bound:
+// the output write plus the log-depth reads.
 #include <algorithm>
 #include <cmath>
 
@@ -84,62 +84,59 @@ __device__ __forceinline__ long long upper_bound(const T *h, long long n, long l
 
 template <typename InT, typename OutT>
 __global__ void __launch_bounds__(kThreads) k4_eval(K4Args a) {
-    const int lane = threadIdx.x & 31;
     const long long S = a.batch * a.D;
-    const long long nw = (long long)gridDim.x * (kThreads / 32);
+    const long long total = S * a.nq;
     const InT *rh = (const InT *)a.rep_h, *rv = (const InT *)a.rep_v;
     const InT *ch = (const InT *)a.cls_h, *cv = (const InT *)a.cls_v;
     OutT *out = (OutT *)a.out;
-    for (long long s = (long long)blockIdx.x * (kThreads / 32) + (threadIdx.x >> 5); s < S; s += nw) {
+    // one thread per (segment, query): consecutive threads take consecutive
+    // queries of a segment (coalesced output; the segment's breakpoints are
+    // shared through L1), so a few segments with many points (vectorisation of
+    // one large image) spread over the whole GPU as well
+    for (long long item = (long long)blockIdx.x * kThreads + threadIdx.x; item < total;
+         item += (long long)gridDim.x * kThreads) {
+        const long long s = item / a.nq, q = item - s * a.nq;
         const long long d = s % a.D;
         const long long L2 = 2 * a.L, Lc = a.L * (long long)a.csum[d];
         const long long r0 = a.rep_off[s], rn = a.rep_off[s + 1] - r0;
-        long long c0 = 0, cn = 0;
-        if (a.kind == EUCALC_EVAL_RADON) {
-            c0 = a.cls_off[s];
-            cn = a.cls_off[s + 1] - c0;
+        double t;
+        if (a.t) {
+            t = a.t[q];
+        } else if (a.nq == 1) {
+            t = a.ta;
+        } else {
+            t = __dadd_rn(a.ta, __ddiv_rn(__dmul_rn((double)q, __dsub_rn(a.tb, a.ta)), (double)(a.nq - 1)));
         }
-        for (long long q0 = 0; q0 < a.nq; q0 += 32) {
-            const long long q = q0 + lane;
-            if (q >= a.nq) break;
-            double t;
-            if (a.t) {
-                t = a.t[q];
-            } else if (a.nq == 1) {
-                t = a.ta;
+        const Threshold th = threshold(t, L2, Lc);
+        long long v = 0;
+        if (!th.nan) {
+            if (a.kind == EUCALC_EVAL_ECT) {
+                const long long i = upper_bound(rh + r0, rn, th.le);
+                v = i ? (long long)rv[r0 + i - 1] : 0;
             } else {
-                t = __dadd_rn(a.ta, __ddiv_rn(__dmul_rn((double)q, __dsub_rn(a.tb, a.ta)), (double)(a.nq - 1)));
-            }
-            const Threshold th = threshold(t, L2, Lc);
-            long long v = 0;
-            if (!th.nan) {
-                if (a.kind == EUCALC_EVAL_ECT) {
-                    const long long i = upper_bound(rh + r0, rn, th.le);
-                    v = i ? (long long)rv[r0 + i - 1] : 0;
-                } else {
-                    bool hit = false;
-                    if (th.exact != kBig && cn) {
-                        const long long j = upper_bound(ch + c0, cn, th.exact);
-                        if (j && (long long)ch[c0 + j - 1] == th.exact) {
-                            v = (long long)cv[c0 + j - 1];
-                            hit = true;
-                        }
-                    }
-                    if (!hit) {
-                        const long long i = upper_bound(rh + r0, rn, th.lt);
-                        v = i ? (long long)rv[r0 + i - 1] : 0;
+                const long long c0 = a.cls_off[s], cn = a.cls_off[s + 1] - c0;
+                bool hit = false;
+                if (th.exact != kBig && cn) {
+                    const long long j = upper_bound(ch + c0, cn, th.exact);
+                    if (j && (long long)ch[c0 + j - 1] == th.exact) {
+                        v = (long long)cv[c0 + j - 1];
+                        hit = true;
                     }
                 }
+                if (!hit) {
+                    const long long i = upper_bound(rh + r0, rn, th.lt);
+                    v = i ? (long long)rv[r0 + i - 1] : 0;
+                }
             }
-            out[s * a.nq + q] = (OutT)v;
         }
+        out[item] = (OutT)v;
     }
 }
 
 template <typename InT>
 cudaError_t launch_in(const K4Args &a, cudaStream_t s, int num_sms) {
-    const long long S = a.batch * a.D;
-    const long long blocks = std::min<long long>((S + kThreads / 32 - 1) / (kThreads / 32), 32ll * num_sms);
+    const long long total = a.batch * a.D * a.nq;
+    const long long blocks = std::min<long long>((total + kThreads - 1) / kThreads, 16ll * num_sms);
     if (a.out_eb == 4) k4_eval<InT, int32_t><<<(unsigned)blocks, kThreads, 0, s>>>(a);
     else k4_eval<InT, int64_t><<<(unsigned)blocks, kThreads, 0, s>>>(a);
     count_launch();
