@@ -59,6 +59,7 @@ def _get():
             lib.eo_radon_at.argtypes = [P, ctypes.c_int, P, P, i64]
             lib.eo_radon_at.restype = i64
             lib.eo_transforms.argtypes = [P, ctypes.c_int, P, P, i64] + [P] * 9
+            lib.eo_transforms_real.argtypes = [P, ctypes.c_int, P, P, i64] + [P] * 9
             lib.eo_ht_quad.argtypes = [P, ctypes.c_int, P, P, i64, i64, ctypes.c_int, ctypes.c_double, ctypes.c_int]
             lib.eo_ht_quad.restype = ctypes.c_double
             lib.eo_ht_cells.argtypes = [P, ctypes.c_int, P, P, i64, i64, ctypes.c_int, ctypes.c_double]
@@ -167,6 +168,26 @@ class Grid:
                     To=bufs[2][:b].copy(), Eo=bufs[3][:b].copy(),
                     Tc=bufs[4][:c].copy(), Ec=bufs[5][:c].copy())
 
+    def transforms_real(self, xi):
+        """Canonical ECT / Radon for a real-valued direction (NEXT f3, E22): heights
+        are the doubles <xi, x> of the vertices (P:116 embedding, left-to-right,
+        no FMA); returns T/To/Tc as float64 and E/Eo/Ec as int64."""
+        xi = np.ascontiguousarray(np.asarray(xi, dtype=np.float64))
+        if xi.shape != (self.n,) or np.any(xi == 0):
+            raise ValueError("direction must have n nonzero coordinates (P:105)")
+        cap = int(np.prod(self.M))
+        hb = [np.empty(cap, dtype=np.float64) for _ in range(3)]
+        vb = [np.empty(cap, dtype=np.int64) for _ in range(3)]
+        cnt = [np.zeros(1, dtype=np.int64) for _ in range(3)]
+        rc = _get().eo_transforms_real(_p(self.cells), self.n, _p(self.d), _p(xi), cap,
+                                       _p(hb[0]), _p(vb[0]), _p(cnt[0]), _p(hb[1]), _p(vb[1]), _p(cnt[1]),
+                                       _p(hb[2]), _p(vb[2]), _p(cnt[2]))
+        if rc != 0:
+            raise RuntimeError(f"eo_transforms_real rc={rc}")
+        a, b, c = (int(x[0]) for x in cnt)
+        return dict(T=hb[0][:a].copy(), E=vb[0][:a].copy(), To=hb[1][:b].copy(), Eo=vb[1][:b].copy(),
+                    Tc=hb[2][:c].copy(), Ec=vb[2][:c].copy())
+
     # -- evaluation at real t (P:135-137) straight from the definitions
     def _t2(self, xi, t):
         """The query t (a Python float = IEEE double, taken exactly) in doubled
@@ -239,6 +260,19 @@ def transforms_batch(images, dirs, construction, pairs=None, threads=None):
     with ThreadPoolExecutor(_threads(threads)) as ex:
         grids = dict(zip(need, ex.map(lambda b: Grid(images[b], construction), need)))
         res = ex.map(lambda bd: grids[bd[0]].transforms(dirs[bd[1]]), pairs)
+        return dict(zip(pairs, res))
+
+
+def transforms_real_batch(images, dirs, construction, pairs=None, threads=None):
+    """Oracle ECT/Radon for real-valued directions (float64 [D, n]) per (image, direction)."""
+    images = np.asarray(images)
+    dirs = np.asarray(dirs, dtype=np.float64)
+    if pairs is None:
+        pairs = [(b, d) for b in range(images.shape[0]) for d in range(dirs.shape[0])]
+    need = sorted({b for b, _ in pairs})
+    with ThreadPoolExecutor(_threads(threads)) as ex:
+        grids = dict(zip(need, ex.map(lambda b: Grid(images[b], construction), need)))
+        res = ex.map(lambda bd: grids[bd[0]].transforms_real(dirs[bd[1]]), pairs)
         return dict(zip(pairs, res))
 
 

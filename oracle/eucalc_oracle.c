@@ -423,3 +423,139 @@ double eo_ht_cells(const int32_t *cells, int n, const int64_t *d, const int64_t 
     }
     return (double)(acc.s + acc.c);
 }
+
+/* ---------------------------------------------------------------------------
+ * Real-valued directions (NEXT row f3; the paper's experimental setting,
+ * P:140). Vertex p is embedded at x_i = p_i / (M_i - 1) - 0.5 (0 when
+ * M_i = 1) and its height is the double
+ *     h(p) = ((xi_0 x_0 + xi_1 x_1) + xi_2 x_2)
+ * evaluated left to right in IEEE double, round to nearest, no fused
+ * multiply-add (E22: ties are exact equalities of these identically
+ * computed dots). A cell's heights are the min / max over its vertices.
+ * The transforms are the same cell sums as eo_transforms (E2 / Lemma 4),
+ * swept over the sorted distinct vertex heights c_0 < c_1 < ... (every
+ * breakpoint is a vertex height): ECT at c_k counts the cells with
+ * max_P <= c_k; Radon at c_k counts the vertices at c_k and the cells with
+ * min_P < c_k < max_P, and on (c_k, c_{k+1}) the cells with min_P <= c_k and
+ * max_P >= c_{k+1}. Canonical extraction as in eo_transforms.
+ * ------------------------------------------------------------------------- */
+static int cmp_double(const void *a, const void *b)
+{
+    double x = *(const double *)a, y = *(const double *)b;
+    return x < y ? -1 : x > y ? 1 : 0;
+}
+
+static int64_t find_height(const double *c, int64_t nc, double h)
+{
+    int64_t lo = 0, hi = nc - 1;
+    while (lo < hi) {
+        int64_t mid = (lo + hi) / 2;
+        if (c[mid] < h) lo = mid + 1; else hi = mid;
+    }
+    return lo; /* c[lo] == h: h is a vertex height */
+}
+
+static double vertex_height(int n, const int64_t *d, const int64_t *p, const double *xi)
+{
+    volatile double h = 0.0; /* volatile: keep the written order, no contraction */
+    for (int i = 0; i < n; ++i) {
+        const int64_t M = (d[i] + 1) / 2;
+        volatile double x = M > 1 ? (double)p[i] / (double)(M - 1) : 0.0;
+        if (M > 1) x = x - 0.5;
+        volatile double t = xi[i] * x;
+        h = (i == 0) ? t : h + t;
+    }
+    h = h + 0.0; /* -0.0 -> +0.0 */
+    return h;
+}
+
+int eo_transforms_real(const int32_t *cells, int n, const int64_t *d, const double *xi, int64_t cap,
+                       double *T, int64_t *E, int64_t *nT,
+                       double *To, int64_t *Eo, int64_t *nTo,
+                       double *Tc, int64_t *Ec, int64_t *nTc)
+{
+    if (n < 1 || n > EO_MAXN) return -1;
+    int64_t ncell = 1, nv = 1, M[EO_MAXN];
+    for (int i = 0; i < n; ++i) {
+        ncell *= d[i];
+        M[i] = (d[i] + 1) / 2;
+        nv *= M[i];
+    }
+    double *vh = malloc(sizeof(double) * (size_t)nv), *c = malloc(sizeof(double) * (size_t)nv);
+    if (!vh || !c) { free(vh); free(c); return -3; }
+    for (int64_t k = 0; k < nv; ++k) {
+        int64_t p[EO_MAXN];
+        unrank(k, n, M, p);
+        vh[k] = vertex_height(n, d, p, xi);
+        c[k] = vh[k];
+    }
+    qsort(c, (size_t)nv, sizeof(double), cmp_double);
+    int64_t nc = 0;
+    for (int64_t k = 0; k < nv; ++k)
+        if (nc == 0 || c[k] != c[nc - 1]) c[nc++] = c[k];
+    int64_t *ect = calloc((size_t)nc + 1, sizeof(int64_t));
+    int64_t *rv = calloc((size_t)nc + 1, sizeof(int64_t));
+    int64_t *rd = calloc((size_t)(2 * nc + 2), sizeof(int64_t));
+    if (!ect || !rv || !rd) { free(vh); free(c); free(ect); free(rv); free(rd); return -3; }
+    for (int64_t k = 0; k < ncell; ++k) {
+        int64_t u[EO_MAXN];
+        unrank(k, n, d, u);
+        int dim = 0;
+        for (int i = 0; i < n; ++i) dim += (int)(u[i] & 1);
+        /* the cell's vertices: u_i even -> u_i/2; odd -> (u_i-1)/2 and (u_i+1)/2 */
+        double hmin = 0, hmax = 0;
+        for (int mask = 0; mask < (1 << n); ++mask) {
+            int64_t p[EO_MAXN];
+            int dup = 0;
+            for (int i = 0; i < n; ++i) {
+                int bit = (mask >> i) & 1;
+                if (u[i] % 2 == 0) { p[i] = u[i] / 2; if (bit) dup = 1; }
+                else p[i] = (u[i] - 1) / 2 + bit;
+            }
+            if (dup) continue;
+            double h = vh[rank_of(n, M, p)];
+            if (mask == 0 || h < hmin) hmin = h;
+            if (mask == 0 || h > hmax) hmax = h;
+        }
+        int64_t kmin = find_height(c, nc, hmin), kmax = find_height(c, nc, hmax);
+        int64_t w = cells[k];
+        ect[kmax] += (dim & 1) ? -w : w;
+        if (dim == 0) {
+            rv[kmin] += w;
+        } else {
+            /* (-1)^(dim-1) w on the open interval (hmin, hmax): on the points c_k with
+               kmin < k < kmax and on the gaps (c_k, c_k+1) with kmin <= k < kmax */
+            int64_t s = (dim & 1) ? w : -w;
+            rd[2 * kmin + 1] += s;
+            rd[2 * kmax] -= s;
+        }
+    }
+    int64_t nt = 0, nto = 0, ntc = 0, run = 0, rrun = 0, prev_e = 0, prev_r = 0;
+    for (int64_t k = 0; k < nc; ++k) {
+        run += ect[k];
+        if (run != prev_e) {
+            if (T && nt < cap) { T[nt] = c[k]; E[nt] = run; }
+            ++nt;
+            prev_e = run;
+        }
+        rrun += rd[2 * k];
+        int64_t at = rv[k] + rrun;
+        rrun += rd[2 * k + 1];
+        int64_t after = rrun;
+        if (at != prev_r) {
+            if (Tc && ntc < cap) { Tc[ntc] = c[k]; Ec[ntc] = at; }
+            ++ntc;
+        }
+        if (after != prev_r) {
+            if (To && nto < cap) { To[nto] = c[k]; Eo[nto] = after; }
+            ++nto;
+        }
+        prev_r = after;
+    }
+    free(vh); free(c); free(ect); free(rv); free(rd);
+    if (nT) *nT = nt;
+    if (nTo) *nTo = nto;
+    if (nTc) *nTc = ntc;
+    if ((T && nt > cap) || (To && nto > cap) || (Tc && ntc > cap)) return -2;
+    return 0;
+}

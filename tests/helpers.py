@@ -25,10 +25,11 @@ def lemma2_transforms(heights_c, dminus, heights_o, jump):
 
     wc = defaultdict(int)
     wj = defaultdict(int)
+    key = lambda h: h.item() if hasattr(h, "item") else h  # int lattice heights or float heights (f3)
     for h, w in zip(heights_c, dminus):
-        wc[int(h)] += int(w)
+        wc[key(h)] += int(w)
     for h, w in zip(heights_o, jump):
-        wj[int(h)] += int(w)
+        wj[key(h)] += int(w)
     keys = sorted(set(wc) | set(wj))
     T, E, To, Eo, Tc, Ec = [], [], [], [], [], []
     e = 0
@@ -45,7 +46,9 @@ def lemma2_transforms(heights_c, dminus, heights_o, jump):
             To.append(h)
             Eo.append(r)
     a = lambda x: np.array(x, dtype=np.int64)
-    return dict(T=a(T), E=a(E), To=a(To), Eo=a(Eo), Tc=a(Tc), Ec=a(Ec))
+    hdt = np.float64 if any(isinstance(k, float) for k in keys) else np.int64
+    ah = lambda x: np.array(x, dtype=hdt)
+    return dict(T=ah(T), E=a(E), To=ah(To), Eo=a(Eo), Tc=ah(Tc), Ec=a(Ec))
 
 
 def evaluate_ect(T, E, h):
