@@ -149,6 +149,21 @@ eucalc_status eucalc_transforms_ht(const eucalc_critical *cr, const int32_t *dir
                                    eucalc_steps *ect, eucalc_steps *ordinary, eucalc_steps *classical,
                                    int kernel, double param, int precision, void *ht_out,
                                    int64_t *required_out, void *stream);
+/* ---- real-valued directions (NEXT row f3; the paper's setting) ----
+ * dirs: double [D][ndim] (host or device), finite, every coordinate nonzero
+ * (E_NONGENERIC otherwise). A vertex p is embedded at
+ * x_i = p_i/(M_i-1) - 0.5 (0 when M_i = 1) and its height is the double
+ * ((xi_0 x_0 + xi_1 x_1) + xi_2 x_2) + 0.0 computed left to right in IEEE
+ * double, round to nearest, no fused multiply-add; equal heights are equal
+ * computed dots (E22). Breakpoints are sorted (the paper's
+ * sort + merge) per (image, direction). Outputs as for
+ * eucalc_transforms, with height[] double and value[] int64: elem_bytes must
+ * be 8. Capacity: sum over (image, direction) of the list length (reported in
+ * *required_out). Lists of up to 4096 records (E_ARG beyond). Host outputs
+ * synchronise `stream`. */
+eucalc_status eucalc_transforms_real(const eucalc_critical *cr, const double *dirs, int64_t D,
+                                     eucalc_steps *ect, eucalc_steps *ordinary, eucalc_steps *classical,
+                                     int64_t *required_out, void *stream);
 eucalc_status eucalc_ect(const eucalc_critical *cr, const int32_t *dirs, int64_t D,
                          eucalc_steps *ect, int64_t *required_out, void *stream);
 eucalc_status eucalc_radon(const eucalc_critical *cr, const int32_t *dirs, int64_t D,

@@ -62,6 +62,7 @@ def lib():
         L.eucalc_transforms.argtypes = [P, P, I64, SP, SP, SP, ctypes.POINTER(I64), P]
         L.eucalc_transforms_ht.argtypes = [P, P, I64, SP, SP, SP, I32, ctypes.c_double, I32, P,
                                            ctypes.POINTER(I64), P]
+        L.eucalc_transforms_real.argtypes = [P, P, I64, SP, SP, SP, ctypes.POINTER(I64), P]
         L.eucalc_ect.argtypes = [P, P, I64, SP, ctypes.POINTER(I64), P]
         L.eucalc_radon.argtypes = [P, P, I64, SP, SP, ctypes.POINTER(I64), P]
         L.eucalc_hybrid.argtypes = [P, P, I64, I32, ctypes.c_double, I32, P, P]
@@ -81,6 +82,7 @@ def lib():
                   "eucalc_destroy_critical", "eucalc_critical_counts", "eucalc_critical_export",
                   "eucalc_output_bound", "eucalc_transforms", "eucalc_ect", "eucalc_radon",
                   "eucalc_hybrid", "eucalc_hybrid_ex", "eucalc_height_map", "eucalc_evaluate", "eucalc_transforms_ht",
+                  "eucalc_transforms_real",
                   "eucalc_vectorize"):
             getattr(L, f).restype = St
         _lib = L
@@ -312,6 +314,33 @@ def transforms(cr: Critical, dirs, ect=True, ordinary=True, classical=True, elem
                                           PRECISIONS[prec], ctypes.c_void_p(out.data_ptr()), ctypes.byref(req), st),
                req.value)
         res["ht"] = out
+    return res
+
+
+def transforms_real(cr: Critical, dirs, ect=True, ordinary=True, classical=True, device="cuda", share_heights=False,
+                    stream=None):
+    """eucalc_transforms_real: canonical ECT / Radon for real-valued directions
+    (float64 [D, n]); heights are float64 paper heights <xi, x>, values int64."""
+    import torch
+
+    d = dirs if hasattr(dirs, "data_ptr") else np.ascontiguousarray(np.asarray(dirs, dtype=np.float64).reshape(len(dirs), -1))
+    D = int(d.shape[0])
+    S = cr.cx.batch * D
+    st = _stream(stream if stream is not None else cr.stream)
+    p, keep = _ptr(d)
+    names = [n for n, want in (("ect", ect), ("ordinary", ordinary), ("classical", classical)) if want]
+    share = share_heights and ect and classical
+    req = ctypes.c_int64()
+    # first call with no outputs: the library reports the capacity it needs
+    _check(lib().eucalc_transforms_real(cr._h, p, D, None, None, None, ctypes.byref(req), st))
+    res, sts = _alloc_all(torch, S, req.value, 8, device, names, share)
+    for name in names:
+        res[name]["height"] = res[name]["height"].view(torch.float64) if res[name]["height"] is not None else None
+    if share:
+        res["classical"]["height"] = res["ect"]["height"]
+        sts["classical"].height = sts["ect"].height
+    refs = [ctypes.byref(sts[n]) if n in sts else None for n in ("ect", "ordinary", "classical")]
+    _check(lib().eucalc_transforms_real(cr._h, p, D, refs[0], refs[1], refs[2], ctypes.byref(req), st), req.value)
     return res
 
 

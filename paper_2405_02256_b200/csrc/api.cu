@@ -2,6 +2,7 @@
 // See include/eucalc.h for the contract of every entry point.
 #include <algorithm>
 #include <atomic>
+#include <cmath>
 #include <cstdio>
 #include <cstring>
 #include <map>
@@ -1071,6 +1072,174 @@ eucalc_status eucalc_transforms_ht(const eucalc_critical *cr, const int32_t *dir
                                    int precision, void *ht_out, int64_t *required_out, void *stream) {
     const HtReq h{kernel, precision, param, ht_out};
     return transforms_impl(cr, dirs, D, ect, ordinary, classical, &h, required_out, stream);
+}
+
+eucalc_status eucalc_transforms_real(const eucalc_critical *ccr, const double *dirs, int64_t D, eucalc_steps *ect,
+                                     eucalc_steps *ordinary, eucalc_steps *classical, int64_t *required_out,
+                                     void *stream) {
+    if (!ccr) return fail(EUCALC_E_STATE, "NULL handle");
+    eucalc_critical *cr = const_cast<eucalc_critical *>(ccr);
+    const Complex *cx = cr->cx;
+    const int n = cx->ndim, full = (1 << n) - 1;
+    cudaStream_t st = (cudaStream_t)stream;
+    if (D < 0) return fail(EUCALC_E_ARG, "D < 0");
+    if (D > 0 && !dirs) return fail(EUCALC_E_ARG, "dirs is NULL");
+    std::vector<double> h((size_t)D * n);
+    if (D > 0) {
+        if (is_device_ptr(dirs)) {
+            CK(cudaMemcpyAsync(h.data(), dirs, sizeof(double) * D * n, cudaMemcpyDeviceToHost, st));
+            CK(cudaStreamSynchronize(st));
+        } else {
+            memcpy(h.data(), dirs, sizeof(double) * D * n);
+        }
+    }
+    std::vector<int32_t> hq(D), hsw(D);
+    for (int64_t d = 0; d < D; ++d) {
+        int e = 0;
+        for (int k = 0; k < n; ++k) {
+            const double v = h[d * n + k];
+            if (!(v == v) || v == INFINITY || v == -INFINITY) return fail(EUCALC_E_ARG, "direction is not finite");
+            if (v == 0.0) {
+                g_bad = d;
+                return fail(EUCALC_E_NONGENERIC, "direction " + std::to_string(d) + " has a zero coordinate (P:105)");
+            }
+            if (v > 0) e |= 1 << k;
+        }
+        const bool rep = ((e >> (n - 1)) & 1) == 0;
+        hq[d] = rep ? e : (e ^ full);
+        hsw[d] = rep ? 0 : 1;
+    }
+    eucalc_status s = sync_counts(cr, st);
+    if (s != EUCALC_OK) return s;
+    // every stream has at most one entry per distinct height <= list length
+    int64_t bnd = 0;
+    {
+        std::vector<int64_t> per_q(cr->Q, 0), dirs_q(cr->Q, 0);
+        for (int64_t b = 0; b < cx->batch; ++b)
+            for (int q = 0; q < cr->Q; ++q) per_q[q] += cr->h_count[b * cr->Q + q];
+        for (int64_t d = 0; d < D; ++d) dirs_q[hq[d]] += 1;
+        for (int q = 0; q < cr->Q; ++q) bnd += per_q[q] * dirs_q[q];
+    }
+    if (required_out) *required_out = bnd;
+    eucalc_steps *outs[3] = {ect, ordinary, classical};
+    for (eucalc_steps *o : outs) {
+        if (!o) continue;
+        if (!o->offsets || (!o->height && o != classical) || !o->value) return fail(EUCALC_E_ARG, "NULL output array");
+        if (o->elem_bytes != 8) return fail(EUCALC_E_ARG, "real-valued directions need elem_bytes 8 (double heights, int64 values)");
+        if (o->capacity < bnd) return fail(EUCALC_E_CAPACITY, "capacity " + std::to_string(o->capacity) + " < required bound " + std::to_string(bnd));
+    }
+    if (!ect && !ordinary && !classical) return EUCALC_OK;
+    if (cr->max_count > 4096) return fail(EUCALC_E_ARG, "real-valued directions: critical lists of more than 4096 records are not supported (bitonic sort in shared memory)");
+    if (cr->max_abs_sum >= (int64_t(1) << 31)) return fail(EUCALC_E_RANGE, "total |weight| of a critical list exceeds 2^31");
+    const int64_t S = cx->batch * D;
+    if (S == 0) return EUCALC_OK;
+    const bool cls_alias = classical && ect && (classical->height == ect->height || !classical->height);
+    if (classical && !classical->height && !ect) return fail(EUCALC_E_ARG, "classical height is NULL");
+    bool host_out = false;
+    for (eucalc_steps *o : outs)
+        if (o && !is_device_ptr(o->value)) host_out = true;
+    std::vector<void *> scratch;
+    auto dalloc = [&](size_t bytes) -> void * {
+        void *q = nullptr;
+        if (cudaMallocAsync(&q, std::max<size_t>(bytes, 1), st) != cudaSuccess) return nullptr;
+        scratch.push_back(q);
+        return q;
+    };
+    auto free_scratch = [&]() { for (void *q : scratch) cudaFreeAsync(q, st); };
+    StepsOut dev[3] = {};
+    for (int i = 0; i < 3; ++i) {
+        eucalc_steps *o = outs[i];
+        if (!o) continue;
+        if (host_out) {
+            dev[i].off = (int64_t *)dalloc(sizeof(int64_t) * (S + 1));
+            dev[i].v = dalloc(8 * (size_t)std::max<int64_t>(bnd, 1));
+            dev[i].h = (i == 2 && cls_alias) ? dev[0].h : dalloc(8 * (size_t)std::max<int64_t>(bnd, 1));
+            if (!dev[i].off || !dev[i].v || !dev[i].h) {
+                free_scratch();
+                return fail(EUCALC_E_NOMEM, "device scratch for host outputs");
+            }
+        } else {
+            dev[i].off = o->offsets;
+            dev[i].h = (i == 2 && cls_alias) ? nullptr : o->height;
+            dev[i].v = o->value;
+        }
+    }
+    double *d_xi = (double *)dalloc(sizeof(double) * D * n);
+    int32_t *d_q = (int32_t *)dalloc(sizeof(int32_t) * D), *d_sw = (int32_t *)dalloc(sizeof(int32_t) * D);
+    unsigned long long *flags = (unsigned long long *)dalloc(sizeof(unsigned long long) * S);
+    unsigned int *ticket = (unsigned int *)dalloc(sizeof(unsigned int) * 4);
+    int *cnts = (int *)dalloc(sizeof(int) * 2 * S);
+    if (!d_xi || !d_q || !d_sw || !flags || !ticket || !cnts) {
+        free_scratch();
+        return fail(EUCALC_E_NOMEM, "scratch");
+    }
+    cudaError_t e = cudaMemcpyAsync(d_xi, h.data(), sizeof(double) * D * n, cudaMemcpyHostToDevice, st);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(d_q, hq.data(), sizeof(int32_t) * D, cudaMemcpyHostToDevice, st);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(d_sw, hsw.data(), sizeof(int32_t) * D, cudaMemcpyHostToDevice, st);
+    if (e == cudaSuccess) e = cudaMemsetAsync(flags, 0, sizeof(unsigned long long) * S, st);
+    if (e == cudaSuccess) e = cudaMemsetAsync(ticket, 0, sizeof(unsigned int) * 4, st);
+    if (e == cudaSuccess) {
+        K5Args a{};
+        a.rec = cr->d_rec;
+        a.wide = cr->wide;
+        a.vcap = cr->vcap;
+        a.count = cr->d_count;
+        a.Q = cr->Q;
+        a.ndim = n;
+        for (int k = 0; k < n; ++k) {
+            a.sh[k] = cx->sh[k];
+            a.msk[k] = cx->msk[k];
+            a.M[k] = (int)cx->M[k];
+        }
+        a.xi = d_xi;
+        a.q = d_q;
+        a.swap = d_sw;
+        a.D = D;
+        a.batch = cx->batch;
+        int np2 = 32;
+        while (np2 < cr->max_count) np2 <<= 1;
+        a.npow2 = np2;
+        a.cnt_c = cnts;
+        a.cnt_o = cnts + S;
+        a.do_ect = ect != nullptr;
+        a.do_ord = ordinary != nullptr;
+        a.do_cls = classical != nullptr;
+        a.cls_alias = cls_alias;
+        a.ect = dev[0];
+        a.ord = dev[1];
+        a.cls = dev[2];
+        a.scan.do_ect = a.do_ect;
+        a.scan.do_ord = a.do_ord;
+        a.scan.do_cls = a.do_cls;
+        a.scan.ect = dev[0];
+        a.scan.ord = dev[1];
+        a.scan.cls = dev[2];
+        a.scan.flags = flags;
+        a.scan.ticket = ticket;
+        ProfScope ps("k5_real", st);
+        e = launch_k5(a, st, num_sms());
+    }
+    if (e == cudaSuccess && host_out) {
+        for (int i = 0; i < 3 && e == cudaSuccess; ++i) {
+            eucalc_steps *o = outs[i];
+            if (!o) continue;
+            e = cudaMemcpyAsync(o->offsets, dev[i].off, sizeof(int64_t) * (S + 1), cudaMemcpyDeviceToHost, st);
+        }
+        if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+        for (int i = 0; i < 3 && e == cudaSuccess; ++i) {
+            eucalc_steps *o = outs[i];
+            if (!o) continue;
+            const size_t nbytes = 8 * (size_t)o->offsets[S];
+            if (nbytes == 0) continue;
+            e = cudaMemcpyAsync(o->value, dev[i].v, nbytes, cudaMemcpyDeviceToHost, st);
+            if (e == cudaSuccess && o->height && !(i == 2 && cls_alias))
+                e = cudaMemcpyAsync(o->height, dev[i].h, nbytes, cudaMemcpyDeviceToHost, st);
+        }
+    }
+    free_scratch();
+    if (e == cudaSuccess && host_out) e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) return cuda_fail(e, "transforms_real");
+    return EUCALC_OK;
 }
 
 eucalc_status eucalc_ect(const eucalc_critical *cr, const int32_t *dirs, int64_t D, eucalc_steps *ect,

@@ -203,6 +203,34 @@ cudaError_t launch_k4(const K4Args &a, cudaStream_t s, int num_sms);
 // repeated launch is a map lookup instead of two driver calls.
 cudaError_t prepare_kernel(const void *fn, int threads, size_t smem, int *occ);
 
+// CSR offsets from per-segment counts (K2's decoupled-look-back scan): writes
+// a.ect/cls/ord.off[0..S] for the requested streams; a.ticket[2] and a.flags
+// (S entries) must be zeroed.
+cudaError_t launch_csr_scan(const K2Args &a, const int *cnt_c, const int *cnt_o, long long S, cudaStream_t s);
+
+// K5: real-valued directions (NEXT f3)
+struct K5Args {
+    const void *rec;
+    bool wide;
+    int64_t vcap;
+    const int32_t *count;
+    int Q, ndim;
+    int sh[kMaxN];
+    uint32_t msk[kMaxN];
+    int M[kMaxN];
+    const double *xi;     // [D][ndim]
+    const int32_t *q;     // [D] antipodal pair of the direction's orthant
+    const int32_t *swap;  // [D] 1 if the orthant is the pair's non-representative
+    int64_t D, batch;
+    int npow2;            // sort length: power of two >= every list length
+    int *cnt_c, *cnt_o;   // [batch*D]
+    bool do_ect, do_ord, do_cls, cls_alias;
+    StepsOut ect, ord, cls;  // heights double, values int64
+    K2Args scan;          // offsets / ticket / flags for launch_csr_scan
+};
+cudaError_t launch_k5(const K5Args &a, cudaStream_t s, int num_sms);
+size_t k5_smem(int npow2);
+
 // thread-local launch counter (eucalc_launch_count)
 void count_launch(int n = 1);
 

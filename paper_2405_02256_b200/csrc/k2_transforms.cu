@@ -861,6 +861,13 @@ cudaError_t launch_o(const K2Args &a, cudaStream_t s, int num_sms) {
 
 }  // namespace
 
+cudaError_t launch_csr_scan(const K2Args &a, const int *cnt_c, const int *cnt_o, long long S, cudaStream_t s) {
+    const long long ntiles = (S + 1 + kScanTile - 1) / kScanTile;
+    k2_scan<<<(unsigned)ntiles, kScanThreads, 0, s>>>(a, cnt_c, cnt_o, S, a.flags);
+    count_launch();
+    return cudaGetLastError();
+}
+
 cudaError_t launch_k2(const K2Args &a, cudaStream_t s, int num_sms) {
     return a.wide ? launch_o<Rec32>(a, s, num_sms) : launch_o<Rec16>(a, s, num_sms);
 }

@@ -136,8 +136,39 @@ def exp_levels(eu, torch):
                        classical_frac=float(cnt[:, 0].mean() / V), ordinary_frac=float(cnt[:, 1].mean() / V))
 
 
+def exp_real(eu, torch):
+    """Real-valued directions (K5, NEXT f3): config-2 images x 100 directions uniform in
+    [0,1]^2, the paper's Table 1 setting (6e6 image-directions in 117 s
+    for the ECT on an i7-4770)."""
+    for variant in ("gray", "binary"):
+        c = synth.config_inputs(2, variant)
+        dev = torch.from_numpy(c["images"]).cuda()
+        dirs = np.random.default_rng(3).uniform(1e-3, 1.0, size=(100, 2))
+
+        def run():
+            cr = eu.critical_points(eu.build_complex(dev, "vertex"))
+            eu.profile_enable(True)
+            eu.transforms_real(cr, dirs, share_heights=True)
+
+        for _ in range(2):
+            run()
+        torch.cuda.synchronize()
+        ts = []
+        for _ in range(5):
+            cr = eu.critical_points(eu.build_complex(dev, "vertex"))
+            torch.cuda.synchronize()
+            eu.profile_enable(True)
+            eu.transforms_real(cr, dirs, share_heights=True)
+            torch.cuda.synchronize()
+            ts.append(eu.profile_read("k5_real")[0])
+            eu.profile_enable(False)
+        ms = float(np.median(ts))
+        yield dict(experiment="real", variant=variant, images=int(dev.shape[0]), directions=100, k5_real_ms=ms,
+                   image_directions_per_s=dev.shape[0] * 100 / (ms / 1e3))
+
+
 EXPS = {"size": exp_size, "critical": exp_critical, "directions": exp_directions, "vectorize": exp_vectorize,
-        "levels": exp_levels}
+        "levels": exp_levels, "real": exp_real}
 
 
 def main():
