@@ -77,7 +77,7 @@ class Clocks:
              "clocks_event_reasons.sw_power_cap")
         try:
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={q}",
-                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                          "--format=csv,noheader,nounits", "-lms", "25"],
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
@@ -239,6 +239,10 @@ def gpu_arm(args):
     k2_bytes /= 2  # per launch (two variants per step)
     peak, peak_src = peaks()
     achieved = k2_bytes / (k2_launch_ms / 1e3) / 1e9
+    traffic = None  # measured DRAM bytes per K2 call, from the committed ncu capture (tools/traffic.py)
+    tp = os.path.join(ROOT, "profiles", "r1", "k2_traffic.json")
+    if os.path.exists(tp):
+        traffic = json.load(open(tp)).get("dram_bytes_per_launch")
 
     # ---- e2e through the ABI with host buffers
     torch.cuda.synchronize()
@@ -277,8 +281,9 @@ def gpu_arm(args):
                 "output": "CSR, int32 heights/values, classical heights shared with ECT",
             },
             "stages_ms_per_step": {k: v / args.steps for k, v in stage_ms.items()},
-            "roofline": {"bound": "hbm", "kernel": "k2_transforms (k2_warp)", "achieved": achieved,
-                         "peak": peak, "unit": "GB/s", "frac": achieved / peak, "traffic": None,
+            "roofline": {"bound": "hbm", "kernel": "k2_transforms (k2w_count+k2_scan+k2w_emit, fused HT)",
+                         "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                         "traffic": traffic, "traffic_source": "profiles/r1/k2_traffic.json (ncu, per K2 call)",
                          "peak_source": peak_src, "algorithmic_bytes_per_launch": k2_bytes,
                          "launch_ms": k2_launch_ms},
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
@@ -364,7 +369,7 @@ def reference_arm(args):
 def main(argv=None):
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=30)
+    ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cpu-sample", type=int, default=96, help="images per variant in the oracle sample")
