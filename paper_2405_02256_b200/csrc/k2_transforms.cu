@@ -201,6 +201,24 @@ __device__ __forceinline__ int warp_incl_scan(int v) {
     return v;
 }
 
+// Three inclusive warp scans at once: the shuffle chains are independent, so
+// interleaving them hides the shuffle latency (the emit pass was short-
+// scoreboard bound on three back-to-back dependent chains).
+__device__ __forceinline__ void warp_incl_scan3(int &x, int &y, int &z) {
+    const int lane = threadIdx.x & 31;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const int tx = __shfl_up_sync(0xffffffffu, x, d);
+        const int ty = __shfl_up_sync(0xffffffffu, y, d);
+        const int tz = __shfl_up_sync(0xffffffffu, z, d);
+        if (lane >= d) {
+            x += tx;
+            y += ty;
+            z += tz;
+        }
+    }
+}
+
 // Count the nonzero bins of one 128-bin group (lane <-> 4 consecutive bins).
 template <bool PACK, bool SWZ>
 __device__ __forceinline__ void count_group(const Hist<PACK, SWZ> &hs, int base, int &c, int &o, bool clear) {
@@ -285,7 +303,8 @@ __device__ __forceinline__ void emit_group(const OutPtrs<OutT> &o, const Hist<PA
         sj += wj[s];
     }
     const int cnt = lc | (lo << 16);
-    const int ic = warp_incl_scan(cnt), isc = warp_incl_scan(sc), isj = warp_incl_scan(sj);
+    int ic = cnt, isc = sc, isj = sj;
+    warp_incl_scan3(ic, isc, isj);
     const int ec = ic - cnt;
     int p_c = pc + (ec & 0xffff), p_o = po + (ec >> 16);
     int e = e_run + (isc - sc), r = r_run + (isj - sj);
@@ -339,15 +358,28 @@ constexpr int kGroup = 128;  // bins per warp step (4 per lane)
 // (A single pass with a segment look-back was measured to lose ~1/3 of the
 // time to look-back spinning when ~9k warps start at once.)
 template <typename RecT, bool PACK>
-__device__ __forceinline__ void fill_segment(const K2Args &a, const Hist<PACK> &hs, long long b, const DirInfo &di) {
+// Fills the warp's histogram with the segment's records; returns the 128-bin
+// groups [g0, g1) that can hold a nonzero bin (the records' height span,
+// typically ~85% of R: the scans skip the rest).
+__device__ __forceinline__ void fill_segment(const K2Args &a, const Hist<PACK> &hs, long long b, const DirInfo &di,
+                                             int &g0, int &g1) {
     const int lane = threadIdx.x & 31;
     const RecT *list = reinterpret_cast<const RecT *>(a.rec) + (b * a.Q + di.q) * a.vcap;
     const int n = a.count[b * a.Q + di.q];
+    int lo = INT_MAX, hi = -1;
     for (int i = lane; i < n; i += 32) {
         int bin, wc, wj;
         decode(list[i], di, a, bin, wc, wj);
         hs.add(bin, wc, wj);
+        lo = min(lo, bin);
+        hi = max(hi, bin);
     }
+    for (int d = 16; d; d >>= 1) {
+        lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, d));
+        hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, d));
+    }
+    g0 = hi < 0 ? 0 : (lo / kGroup) * kGroup;
+    g1 = hi + 1;
     __syncwarp();
 }
 
@@ -453,8 +485,9 @@ __global__ void __launch_bounds__(kWarpThreads) k2w_count(K2Args a, int rcap, in
                 if ((threadIdx.x & 31) == 0) ht_write(a, s, acc);
             }
         } else {
-            fill_segment<RecT>(a, hs, b, di);
-            for (int base = 0; base < di.R; base += kGroup) count_group(hs, base, c, o, true);
+            int g0, g1;
+            fill_segment<RecT>(a, hs, b, di, g0, g1);
+            for (int base = g0; base < g1; base += kGroup) count_group(hs, base, c, o, true);
             c = warp_sum(c);
             o = warp_sum(o);
         }
@@ -498,11 +531,12 @@ __global__ void __launch_bounds__(kWarpThreads) k2w_emit(K2Args a, int rcap) {
                 if (r.emit_o) put_o<MODE>(o, po + __popc(mo & lt), h, r.pj);
             }
         } else {
-            fill_segment<RecT>(a, hs, b, di);
+            int g0, g1;
+            fill_segment<RecT>(a, hs, b, di, g0, g1);
             int e_run = 0, r_run = 0;
             double ht = 0.0;
             const long long toff = (MODE & kHt) || (MODE == kModeAny && o.tab) ? ht_tab_off(a, d) : 0;
-            for (int base = 0; base < di.R; base += kGroup)
+            for (int base = g0; base < g1; base += kGroup)
                 emit_group<MODE>(o, hs, base, di.hlo, e_run, r_run, pc, po, ht, toff);
             if ((MODE & kHt) || (MODE == kModeAny && o.tab)) {
                 for (int k = 16; k; k >>= 1) ht += __shfl_xor_sync(0xffffffffu, ht, k);
