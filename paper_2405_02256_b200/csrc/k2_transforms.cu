@@ -608,7 +608,7 @@ __global__ void __launch_bounds__(kScanThreads) k2_scan(K2Args a, const int *cnt
 }
 
 // ----------------------------------------------------------------------------- block kernel
-constexpr int kBlockThreads = 512;
+constexpr int kBlockThreads = 1024;
 constexpr int kBlockWarps = kBlockThreads / 32;
 constexpr size_t kBlockSmem = 208 * 1024;
 
