@@ -615,16 +615,16 @@ constexpr size_t kBlockSmem = 208 * 1024;
 // Accumulate the records list[beg, end) whose bin lies in [lo, lo + wbins):
 // the warp's lanes stride the range, four records in flight per lane (the list
 // streams from L2; a lone load per lane leaves the SM latency-bound).
-template <typename RecT, bool PACK, bool SWZ>
+template <int U, typename RecT, bool PACK, bool SWZ>  // U: records in flight per thread
 __device__ __forceinline__ void fill_range(const K2Args &a, const RecT *list, int beg, int end, const DirInfo &di,
                                            int lo, int wbins, const Hist<PACK, SWZ> &hs, int lane, int step) {
     int i = beg + lane;
-    for (; i + 3 * step < end; i += 4 * step) {
-        RecT r[4];
+    for (; i + (U - 1) * step < end; i += U * step) {
+        RecT r[U];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) r[u] = list[i + u * step];
+        for (int u = 0; u < U; ++u) r[u] = list[i + u * step];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
+        for (int u = 0; u < U; ++u) {
             int bin, wc, wj;
             decode(r[u], di, a, bin, wc, wj);
             bin -= lo;
@@ -675,7 +675,7 @@ __device__ void fill_window(const K2Args &a, const RecT *list, const int32_t *to
                             int lo, int wbins, bool cull, const Hist<PACK, SWZ> &hs) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     if (!cull) {
-        fill_range(a, list, 0, n, di, lo, wbins, hs, threadIdx.x, kBlockThreads);
+        fill_range<8>(a, list, 0, n, di, lo, wbins, hs, threadIdx.x, kBlockThreads);
         return;
     }
     for (int t0 = warp * 32; t0 < a.ntiles; t0 += kBlockWarps * 32) {
@@ -690,7 +690,7 @@ __device__ void fill_window(const K2Args &a, const RecT *list, const int32_t *to
         while (m) {
             const int tt = t0 + __ffs(m) - 1;
             m &= m - 1;
-            fill_range(a, list, toff[tt], toff[tt + 1], di, lo, wbins, hs, lane, 32);
+            fill_range<4>(a, list, toff[tt], toff[tt + 1], di, lo, wbins, hs, lane, 32);
         }
     }
 }
