@@ -610,7 +610,7 @@ __global__ void __launch_bounds__(kScanThreads) k2_scan(K2Args a, const int *cnt
 // ----------------------------------------------------------------------------- block kernel
 constexpr int kBlockThreads = 1024;
 constexpr int kBlockWarps = kBlockThreads / 32;
-constexpr size_t kBlockSmem = 208 * 1024;
+constexpr size_t kBlockSmem = 200 * 1024;
 
 // Accumulate the records list[beg, end) whose bin lies in [lo, lo + wbins):
 // the warp's lanes stride the range, four records in flight per lane (the list
@@ -670,12 +670,32 @@ __device__ __forceinline__ void tile_bins(const K2Args &a, const DirInfo &di, in
 // A single window takes the whole list; several windows cull K1 tiles by their
 // height band, so each record is streamed about once over all windows instead
 // of once per window.
+constexpr int kMaxHitTiles = 4096;  // culled-tile list in shared memory
+
 template <typename RecT, bool PACK, bool SWZ>
 __device__ void fill_window(const K2Args &a, const RecT *list, const int32_t *toff, int n, const DirInfo &di,
-                            int lo, int wbins, bool cull, const Hist<PACK, SWZ> &hs) {
+                            int lo, int wbins, bool cull, const Hist<PACK, SWZ> &hs, int *s_hit, int *s_nhit) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     if (!cull) {
         fill_range<8>(a, list, 0, n, di, lo, wbins, hs, threadIdx.x, kBlockThreads);
+        return;
+    }
+    if (a.ntiles <= kMaxHitTiles) {
+        // the tiles whose height band meets the window, compacted (any order: the
+        // histogram sums are integers), then dealt round-robin to the warps
+        if (threadIdx.x == 0) *s_nhit = 0;
+        __syncthreads();
+        for (int t = threadIdx.x; t < a.ntiles; t += kBlockThreads) {
+            int bmin, bmax;
+            tile_bins(a, di, t, bmin, bmax);
+            if (bmax >= lo && bmin < lo + wbins && toff[t + 1] > toff[t]) s_hit[atomicAdd(s_nhit, 1)] = t;
+        }
+        __syncthreads();
+        const int nhit = *s_nhit;
+        for (int k = warp; k < nhit; k += kBlockWarps) {
+            const int tt = s_hit[k];
+            fill_range<4>(a, list, toff[tt], toff[tt + 1], di, lo, wbins, hs, lane, 32);
+        }
         return;
     }
     for (int t0 = warp * 32; t0 < a.ntiles; t0 += kBlockWarps * 32) {
@@ -702,6 +722,8 @@ __global__ void __launch_bounds__(kBlockThreads, 1) k2_block(K2Args a, long long
     __shared__ int s_wsum[kBlockWarps][4];  // per-warp (nc, no, sum wc, sum wj)
     __shared__ long long s_exc[2];
     __shared__ double s_ht[kBlockWarps];
+    __shared__ int s_hit[kMaxHitTiles];
+    __shared__ int s_nhit;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     constexpr int words = PACK ? 1 : 2;
     const OutPtrs<OutT> outp(a);
@@ -729,7 +751,7 @@ __global__ void __launch_bounds__(kBlockThreads, 1) k2_block(K2Args a, long long
         long long nc = 0, no = 0;
         for (int w = 0; w < nwin; ++w) {
             const int lo = w * win, wb = min(win, di.R - lo);
-            fill_window(a, list, toff, n, di, lo, wb, cull, hs);
+            fill_window(a, list, toff, n, di, lo, wb, cull, hs, s_hit, &s_nhit);
             __syncthreads();
             int c = 0, o = 0;
             const int b0 = min(wb, warp * per), b1 = min(wb, b0 + per);
@@ -765,7 +787,7 @@ __global__ void __launch_bounds__(kBlockThreads, 1) k2_block(K2Args a, long long
         for (int w = 0; w < nwin; ++w) {
             const int lo = w * win, wb = min(win, di.R - lo);
             if (nwin > 1) {
-                fill_window(a, list, toff, n, di, lo, wb, cull, hs);
+                fill_window(a, list, toff, n, di, lo, wb, cull, hs, s_hit, &s_nhit);
                 __syncthreads();
             }
             const int b0 = min(wb, warp * per), b1 = min(wb, b0 + per);
