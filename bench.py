@@ -269,17 +269,9 @@ def gpu_arm(args):
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": dev_ms / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "int32 (ECT/Radon), f64 (HT)",
+            "scaling": "weak", "vs_baseline": None, "dtype": "int16 (ECT/Radon outputs), int32 (histogram), f64 (HT)",
             "data": "synthetic (seeded generators, synth/; config-2 recipe of SURVEY.md 8(d))",
-            "config": {
-                "workload": "BASELINE.json configs[1]: 1024 x 28x28 u8 Gaussian-blob images + binary variant "
-                            "(>=128), vertex construction, 256 integer directions in [-16,16]^2; "
-                            "ECT + Radon (all three streams) + HT (kappa=sin, fp64) per image-direction "
-                            "(HT fused into K2, eucalc_transforms_ht)",
-                "images_per_gpu": 2 * IMAGES_PER_SHARD, "directions": NDIRS, "parallelism": f"dp{world}",
-                "l2": "flushed between timed steps (256 MB write, untimed)",
-                "output": "CSR, int32 heights/values, classical heights shared with ECT",
-            },
+            "config": arm_config(world),
             "stages_ms_per_step": {k: v / args.steps for k, v in stage_ms.items()},
             "roofline": {"bound": "hbm", "kernel": "k2_transforms (k2w_count+k2_scan+k2w_emit, fused HT)",
                          "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
@@ -297,6 +289,18 @@ def gpu_arm(args):
         dist.barrier()
         dist.destroy_process_group()
     return line
+
+
+def arm_config(world):
+    return {
+        "workload": "BASELINE.json configs[1]: 1024 x 28x28 u8 Gaussian-blob images + binary variant "
+                    "(>=128), vertex construction, 256 integer directions in [-16,16]^2; "
+                    "ECT + Radon (all three streams) + HT (kappa=sin, fp64) per image-direction "
+                    "(HT fused into K2, eucalc_transforms_ht)",
+        "images_per_gpu": 2 * IMAGES_PER_SHARD, "directions": NDIRS, "parallelism": f"dp{world}",
+        "l2": "flushed between timed steps (256 MB write, untimed)",
+        "output": "CSR, narrowest exact int width (int16 here), classical heights shared with ECT",
+    }
 
 
 def list_bytes(cr, dirs):
@@ -340,7 +344,9 @@ def reference_arm(args):
     if rank != 0:
         return None
     gray, binary, dirs = workload(0)
-    n = args.cpu_sample
+    # each step a bounded sample of the workload: with the default 100 steps the
+    # whole run stays within a couple of minutes on the host cores
+    n = args.ref_sample
     sample = [gray[:n], binary[:n]]
     cores = os.cpu_count() or 1
     for _ in range(args.warmup):
@@ -356,8 +362,8 @@ def reference_arm(args):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3 / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int64 (ECT/Radon), f64 (HT)",
         "data": "synthetic (seeded generators, synth/)", "impl": "reference",
-        "config": {"workload": "config 2 (bounded sample per step), oracle on host cores",
-                   "images_per_step": 2 * n, "directions": len(dirs)},
+        "config": dict(arm_config(int(os.environ.get("WORLD_SIZE", "1"))),
+                       sample=f"oracle on host cores; each step {n} gray + {n} binary images x {len(dirs)} directions"),
         "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle",
                          "sample": f"{n} gray + {n} binary config-2 images x {len(dirs)} directions per step"},
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -372,7 +378,8 @@ def main(argv=None):
     ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--cpu-sample", type=int, default=96, help="images per variant in the oracle sample")
+    ap.add_argument("--cpu-sample", type=int, default=96, help="images per variant in the cpu_baseline sample")
+    ap.add_argument("--ref-sample", type=int, default=8, help="images per variant per --impl reference step")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args(argv)
     if args.warmup < 3:

@@ -348,3 +348,25 @@ def test_config5_sampled():
     for kernel, param in (("gauss", 1.0), ("cos", 64.0)):
         for precision in ("f64", "f32"):
             check_ht(vols, dirs, "vertex", cr, kernel, param, precision, pairs=pairs, algorithms=("direct", "table"))
+
+
+@pytest.mark.parametrize("construction", ["vertex", "top"])
+def test_degenerate_images(construction):
+    """All-zero images (no critical points: empty lists and empty segments), constant
+    images (closed forms) and a 1x1 image, through K1-K4 and the fused HT."""
+    imgs = np.stack([np.zeros((9, 7), np.uint8), np.full((9, 7), 5, np.uint8), np.eye(9, 7, dtype=np.uint8)])
+    dirs = synth.random_directions(6, 2, 4, 17)
+    cx, cr, res = run_gpu(imgs, dirs, construction)
+    check_transforms(imgs, dirs, construction, res)
+    assert cr.list_lengths()[0].tolist() == [0, 0]
+    for s in range(len(dirs)):  # the zero image has empty segments in every stream
+        for k in ("ect", "ordinary", "classical"):
+            assert res[k]["offsets"][s + 1] == res[k]["offsets"][s]
+    check_fused_ht(imgs, dirs, construction, cr, "gauss", 1.0, "f64")
+    check_ht(imgs, dirs, construction, cr, "exp", 1.0, "f64")
+    r = eu.transforms(cr, dirs)
+    v = eu.vectorize(cx, dirs, -1.0, 1.0, 7, ect=r["ect"]).cpu().numpy()
+    assert not v[: len(dirs)].any()  # zero image: ECT identically 0
+    one = np.array([[[3]]], np.uint8)
+    cx1, cr1, r1 = run_gpu(one, np.array([[1, 1]], np.int32), construction)
+    check_transforms(one, np.array([[1, 1]], np.int32), construction, r1)
