@@ -4,6 +4,7 @@
 #include <atomic>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -959,7 +960,9 @@ eucalc_status transforms_impl(const eucalc_critical *ccr, const int32_t *dirs, i
     // need not sort them again
     int64_t min_count = INT64_MAX;
     for (int64_t i = 0; i < cx->batch * cr->Q; ++i) min_count = std::min(min_count, cr->h_count[i]);
-    const bool slab_ok = min_count <= 32 && p.R_max <= 32767 && cr->max_abs_sum < 32768 && cr->max_count <= 32768;
+    int sparse_max = 32;  // EUCALC_K2_SPARSE_MAX (0..32) overrides, for measurements
+    if (const char *v = getenv("EUCALC_K2_SPARSE_MAX")) sparse_max = std::max(0, std::min(32, atoi(v)));
+    const bool slab_ok = min_count <= sparse_max && p.R_max <= 32767 && cr->max_abs_sum < 32768 && cr->max_count <= 32768;
     uint2 *slab = slab_ok ? (uint2 *)dalloc(sizeof(uint2) * 33 * S) : nullptr;
     if (!flags || !ticket || !cnts || (slab_ok && !slab)) {
         free_scratch();
@@ -1029,6 +1032,7 @@ eucalc_status transforms_impl(const eucalc_critical *ccr, const int32_t *dirs, i
         a.cnt_c = cnts;
         a.cnt_o = cnts + S;
         a.slab = slab;
+        a.sparse_max = sparse_max;
         ProfScope ps("k2_transforms", st);
         e = launch_k2(a, st, num_sms());
     }

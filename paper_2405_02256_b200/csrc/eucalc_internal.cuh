@@ -130,7 +130,8 @@ struct K2Args {
     unsigned long long *flags;  // [batch*D] look-back flags (zeroed)
     unsigned int *ticket;       // [4] ticket counters (zeroed)
     int *cnt_c, *cnt_o;         // [batch*D] per-segment counts (warp regime)
-    uint2 *slab;                // [batch*D][33] merged runs of lists <= 32 records, or NULL
+    uint2 *slab;                // [batch*D][33] merged runs of lists <= sparse_max records, or NULL
+    int sparse_max;             // lists of <= sparse_max (<= 32) records: register sort instead of histogram
     // fused HT (NEXT f2): kbar table (fp64) over u in [ht_U0, ...), or NULL
     const double *ht_tab;
     int64_t ht_U0, L;

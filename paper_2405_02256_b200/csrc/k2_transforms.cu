@@ -463,7 +463,7 @@ __global__ void __launch_bounds__(kWarpThreads) k2w_count(K2Args a, int rcap, in
         const DirInfo di = a.dirs[d];
         const int n = a.count[b * a.Q + di.q];
         int c = 0, o = 0;
-        if (n <= 32) {
+        if (n <= a.sparse_max) {
             const SparseRuns r = sparse_runs<RecT>(a, b, di, n);
             const unsigned mc = __ballot_sync(0xffffffffu, r.emit_c), mo = __ballot_sync(0xffffffffu, r.emit_o);
             c = __popc(mc);
@@ -513,7 +513,7 @@ __global__ void __launch_bounds__(kWarpThreads) k2w_emit(K2Args a, int rcap) {
         const DirInfo di = a.dirs[d];
         const int n = a.count[b * a.Q + di.q];
         int pc = any_c ? (int)off_c[s] : 0, po = a.do_ord ? (int)a.ord.off[s] : 0;
-        if (n <= 32) {
+        if (n <= a.sparse_max) {
             const unsigned lt = (1u << (threadIdx.x & 31)) - 1;
             if (a.slab) {
                 const uint2 *sl = a.slab + (long long)s * 33;
