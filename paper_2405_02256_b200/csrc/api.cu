@@ -123,6 +123,42 @@ void keep_pool() {
     done[dev] = true;
 }
 
+// Per-(thread, stream) device scratch arena for the small per-call buffers
+// (look-back flags, tickets, counts, slabs, kbar tables): one allocation that
+// only grows, carved per call. Reuse is stream-ordered: a later call on the same
+// stream runs after the kernels of the earlier one. Never released (bounded by
+// the largest call).
+struct Arena {
+    void *p = nullptr;
+    size_t cap = 0;
+};
+thread_local std::map<cudaStream_t, Arena> g_arenas;
+
+// Carves `sizes` (256-byte aligned) out of the arena of `st`; false on allocation failure.
+bool arena_take(cudaStream_t st, const std::vector<size_t> &sizes, std::vector<void *> &out) {
+    size_t total = 0;
+    for (size_t b : sizes) total += (b + 255) / 256 * 256;
+    Arena &ar = g_arenas[st];
+    if (total > ar.cap) {
+        if (ar.p) cudaFreeAsync(ar.p, st);
+        ar.p = nullptr;
+        ar.cap = 0;
+        const size_t want = std::max<size_t>(total, size_t(1) << 20);
+        if (cudaMallocAsync(&ar.p, want, st) != cudaSuccess) {
+            cudaGetLastError();
+            return false;
+        }
+        ar.cap = want;
+    }
+    out.clear();
+    size_t off = 0;
+    for (size_t b : sizes) {
+        out.push_back(b ? (unsigned char *)ar.p + off : nullptr);
+        off += (b + 255) / 256 * 256;
+    }
+    return true;
+}
+
 int bits_for(int64_t v) {  // bits to hold 0..v
     int b = 1;
     while ((int64_t(1) << b) <= v) ++b;
@@ -952,9 +988,6 @@ eucalc_status transforms_impl(const eucalc_critical *ccr, const int32_t *dirs, i
         }
     }
     const DirInfo *d_info = pe->d_info;
-    unsigned long long *flags = (unsigned long long *)dalloc(sizeof(unsigned long long) * S);
-    unsigned int *ticket = (unsigned int *)dalloc(sizeof(unsigned int) * 4);
-    int *cnts = (int *)dalloc(sizeof(int) * 2 * S);
     // warp regime, lists of <= 32 records: k2w_count keeps the merged runs (16-bit
     // fields: every bin index, value and running sum must fit) so that k2w_emit
     // need not sort them again
@@ -963,27 +996,26 @@ eucalc_status transforms_impl(const eucalc_critical *ccr, const int32_t *dirs, i
     int sparse_max = 32;  // EUCALC_K2_SPARSE_MAX (0..32) overrides, for measurements
     if (const char *v = getenv("EUCALC_K2_SPARSE_MAX")) sparse_max = std::max(0, std::min(32, atoi(v)));
     const bool slab_ok = min_count <= sparse_max && p.R_max <= 32767 && cr->max_abs_sum < 32768 && cr->max_count <= 32768;
-    uint2 *slab = slab_ok ? (uint2 *)dalloc(sizeof(uint2) * 33 * S) : nullptr;
-    if (!flags || !ticket || !cnts || (slab_ok && !slab)) {
+    // fused HT: the kbar table over the directions' u range, and the output
+    const int64_t U = p.U1 - p.U0 + 1;
+    const bool ht_host = ht && !is_device_ptr(ht->out);
+    const size_t ht_osz = ht && ht->precision == EUCALC_F32 ? 4 : 8;
+    // flags + ticket are adjacent (one memset); then counts, slab, table, HT staging
+    std::vector<void *> ar;
+    if (!arena_take(st, {sizeof(unsigned long long) * S + sizeof(unsigned int) * 4, sizeof(int) * 2 * S,
+                         slab_ok ? sizeof(uint2) * 33 * S : 0, ht ? 12 * (size_t)U : 0,
+                         ht_host ? ht_osz * S : 0},
+                    ar)) {
         free_scratch();
         return fail(EUCALC_E_NOMEM, "scratch");
     }
-    // fused HT: the kbar table over the directions' u range, and the output
-    const int64_t U = p.U1 - p.U0 + 1;
-    double *d_tab = nullptr;
-    void *d_ht = nullptr;
-    const bool ht_host = ht && !is_device_ptr(ht->out);
-    const size_t ht_osz = ht && ht->precision == EUCALC_F32 ? 4 : 8;
-    if (ht) {
-        d_tab = (double *)dalloc(12 * (size_t)U);
-        d_ht = ht_host ? dalloc(ht_osz * S) : ht->out;
-        if (!d_tab || !d_ht) {
-            free_scratch();
-            return fail(EUCALC_E_NOMEM, "HT table");
-        }
-    }
-    cudaError_t e = cudaMemsetAsync(flags, 0, sizeof(unsigned long long) * S, st);
-    if (e == cudaSuccess) e = cudaMemsetAsync(ticket, 0, sizeof(unsigned int) * 4, st);
+    unsigned long long *flags = (unsigned long long *)ar[0];
+    unsigned int *ticket = (unsigned int *)(flags + S);
+    int *cnts = (int *)ar[1];
+    uint2 *slab = (uint2 *)ar[2];
+    double *d_tab = (double *)ar[3];
+    void *d_ht = ht ? (ht_host ? ar[4] : ht->out) : nullptr;
+    cudaError_t e = cudaMemsetAsync(flags, 0, sizeof(unsigned long long) * S + sizeof(unsigned int) * 4, st);
     if (e == cudaSuccess && ht)
         e = launch_k3_table_only(ht->kernel, ht->param, cx->L, p.U0, U, d_tab, (float *)(d_tab + U), st);
     if (e == cudaSuccess) {
@@ -1309,9 +1341,16 @@ eucalc_status eucalc_hybrid_ex(const eucalc_critical *ccr, const int32_t *dirs, 
     auto free_scratch = [&]() { for (void *q : scratch) cudaFreeAsync(q, st); };
     const DirInfo *d_info = pe->d_info;
     const int32_t *d_order = pe->d_order, *d_ts = pe->d_ts, *d_tl = pe->d_tl, *d_cs = pe->d_csum;
-    double *d_part = (double *)dalloc(sizeof(double) * cx->batch * nchunks * D);
-    void *d_out = host_out ? dalloc(osz * cx->batch * D) : out;
-    void *d_tab = use_table ? dalloc(12 * (size_t)U) : nullptr;
+    std::vector<void *> ar;
+    if (!arena_take(st, {sizeof(double) * cx->batch * nchunks * D, host_out ? osz * cx->batch * D : 0,
+                         use_table ? 12 * (size_t)U : 0},
+                    ar)) {
+        free_scratch();
+        return fail(EUCALC_E_NOMEM, "scratch");
+    }
+    double *d_part = (double *)ar[0];
+    void *d_out = host_out ? ar[1] : out;
+    void *d_tab = ar[2];
     if (!d_part || !d_out || (use_table && !d_tab)) {
         free_scratch();
         return fail(EUCALC_E_NOMEM, "scratch");
