@@ -125,16 +125,37 @@ class Clocks:
 
 # ----------------------------------------------------------------------------- GPU arm
 
+_STREAMS = []
+
+
 def run_step(eu, torch, imgs_dev, dirs, record=None):
-    """One pass of the whole hot path over both variants. Returns host-free results."""
+    """One pass of the whole hot path over both variants. Returns host-free results.
+
+    The two variants (independent batches) go to two CUDA streams forked from and
+    joined back into the current stream, so one variant's small kernels and
+    launch tails overlap the other's work."""
+    cur = torch.cuda.current_stream()
+    while len(_STREAMS) < len(imgs_dev):
+        _STREAMS.append(torch.cuda.Stream())
+    streams = _STREAMS[:len(imgs_dev)]
+    for st in streams:
+        st.wait_stream(cur)
     # enqueue A0-A2 for both variants before the first call that waits on K1
-    cxs = [eu.build_complex(img, "vertex") for img in imgs_dev]
-    crs = [eu.critical_points(cx) for cx in cxs]
+    cxs, crs = [], []
+    for img, st in zip(imgs_dev, streams):
+        with torch.cuda.stream(st):
+            cx = eu.build_complex(img, "vertex", stream=st)
+            cxs.append(cx)
+            crs.append(eu.critical_points(cx, stream=st))
     out = []
-    for cx, cr in zip(cxs, crs):
-        # ECT + Radon + HT in one pass over the merged histogram (eucalc_transforms_ht)
-        r = eu.transforms(cr, dirs, elem_bytes="auto", share_heights=True, ht=(HT_KERNEL, 1.0, "f64"))
+    for cx, cr, st in zip(cxs, crs, streams):
+        with torch.cuda.stream(st):
+            # ECT + Radon + HT in one pass over the merged histogram (eucalc_transforms_ht)
+            r = eu.transforms(cr, dirs, elem_bytes="auto", share_heights=True, ht=(HT_KERNEL, 1.0, "f64"),
+                              stream=st)
         out.append((cx, cr, r, r["ht"]))
+    for st in streams:
+        cur.wait_stream(st)
     return out
 
 
