@@ -217,6 +217,7 @@ def gpu_arm(args):
     times = []
     k2_ms = 0.0
     stage_ms = {}
+    k2_span = 0.0  # wall span of the step's (concurrent) K2 launches
     launches = 0
     if True:
         barrier()
@@ -234,6 +235,7 @@ def gpu_arm(args):
             times.append(ev0.elapsed_time(ev1))
             for st in ("build", "k1_critical", "k2_transforms", "k3_hybrid"):
                 stage_ms[st] = stage_ms.get(st, 0.0) + eu.profile_read(st)[0]
+            k2_span += eu.profile_span("k2_transforms")
             eu.profile_enable(False)
         barrier()
         clk.end()
@@ -246,8 +248,10 @@ def gpu_arm(args):
     units = 2 * IMAGES_PER_SHARD * NDIRS * world * args.steps
     value = units / (dev_ms / 1e3)
 
-    # ---- roofline of the dominant kernel (K2) from the last step's actual sizes
-    k2_launch_ms = stage_ms["k2_transforms"] / (2 * args.steps)
+    # ---- roofline of the dominant stage (K2, both variants' launches running
+    # concurrently on their streams) from the last step's actual sizes: bytes of
+    # both launches over the wall span from the first K2 start to the last K2 end
+    k2_launch_ms = k2_span / args.steps
     k2_bytes = 0
     for cx, cr, r, ht in res:
         S = cx.batch * NDIRS
@@ -257,13 +261,13 @@ def gpu_arm(args):
         lists = list_bytes(cr, dirs)
         # ECT (h,v) + ordinary (h,v) + classical (v; heights shared) + 3 offset arrays + HT (f64)
         k2_bytes += lists + ne * 2 * eb + no * 2 * eb + ne * eb + 3 * (S + 1) * 8 + S * 8
-    k2_bytes /= 2  # per launch (two variants per step)
     peak, peak_src = peaks()
     achieved = k2_bytes / (k2_launch_ms / 1e3) / 1e9
     traffic = None  # measured DRAM bytes per K2 call, from the committed ncu capture (tools/traffic.py)
     tp = os.path.join(ROOT, "profiles", "r1", "k2_traffic.json")
-    if os.path.exists(tp):
-        traffic = json.load(open(tp)).get("dram_bytes_per_launch")
+    if os.path.exists(tp):  # both variants' K2 calls of one step, as the roofline's bytes
+        tj = json.load(open(tp))
+        traffic = tj.get("dram_bytes_per_step") or 2 * tj.get("dram_bytes_per_launch", 0) or None
 
     # ---- e2e through the ABI with host buffers
     torch.cuda.synchronize()
@@ -294,10 +298,12 @@ def gpu_arm(args):
             "data": "synthetic (seeded generators, synth/; config-2 recipe of SURVEY.md 8(d))",
             "config": arm_config(world),
             "stages_ms_per_step": {k: v / args.steps for k, v in stage_ms.items()},
-            "roofline": {"bound": "hbm", "kernel": "k2_transforms (k2w_count+k2_scan+k2w_emit, fused HT)",
+            "roofline": {"bound": "hbm", "kernel": "k2_transforms (k2w_count+k2_scan+k2w_emit, fused HT; gray and "
+                                                  "binary launches concurrent, bytes and span of both)",
                          "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                         "traffic": traffic, "traffic_source": "profiles/r1/k2_traffic.json (ncu, per K2 call)",
+                         "traffic": traffic, "traffic_source": "profiles/r1/k2_traffic.json (ncu, gray + binary K2 calls)",
                          "peak_source": peak_src, "algorithmic_bytes_per_launch": k2_bytes,
+                         "launch": "one step's K2 stage (gray + binary)",
                          "launch_ms": k2_launch_ms},
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
             "gpu_launches": int(launches),

@@ -240,6 +240,9 @@ eucalc_status eucalc_height_map(const eucalc_complex *cx, const int32_t *dir, in
  * the summed milliseconds and number of recorded launches of `stage`. */
 void eucalc_profile_enable(int on);
 int eucalc_profile_read(const char *stage, double *ms, int64_t *launches);
+/* Wall span (first start to last end, milliseconds) of the recorded launches of
+ * `stage`, which may run concurrently on several streams. Synchronises them. */
+int eucalc_profile_span(const char *stage, double *ms);
 /* Kernel launches issued by this library on the calling thread since the last reset. */
 int64_t eucalc_launch_count(int reset);
 const char *eucalc_status_string(eucalc_status s);

@@ -73,6 +73,7 @@ def lib():
         L.eucalc_profile_enable.argtypes = [I32]
         L.eucalc_profile_enable.restype = None
         L.eucalc_profile_read.argtypes = [ctypes.c_char_p, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(I64)]
+        L.eucalc_profile_span.argtypes = [ctypes.c_char_p, ctypes.POINTER(ctypes.c_double)]
         L.eucalc_launch_count.argtypes = [I32]
         L.eucalc_launch_count.restype = I64
         L.eucalc_status_string.restype = ctypes.c_char_p
@@ -431,6 +432,13 @@ def profile_read(stage=None):
     ms, n = ctypes.c_double(), ctypes.c_int64()
     lib().eucalc_profile_read(stage.encode() if stage else None, ctypes.byref(ms), ctypes.byref(n))
     return ms.value, n.value
+
+
+def profile_span(stage=None):
+    """Milliseconds from the first start to the last end of the recorded `stage` launches."""
+    ms = ctypes.c_double()
+    lib().eucalc_profile_span(stage.encode() if stage else None, ctypes.byref(ms))
+    return ms.value
 
 
 def launch_count(reset=False) -> int:

@@ -555,6 +555,27 @@ int eucalc_profile_read(const char *stage, double *ms, int64_t *launches) {
     if (launches) *launches = n;
     return 0;
 }
+int eucalc_profile_span(const char *stage, double *ms) {
+    // first start to last end over the recorded launches of `stage` (they may sit
+    // on different streams and overlap): event timestamps share one GPU clock
+    bool any = false;
+    float lo = 0, hi = 0;
+    cudaEvent_t ref = nullptr;
+    for (auto &r : g_prof_recs) {
+        if (stage && r.stage != stage) continue;
+        cudaEventSynchronize(r.b);
+        if (!ref) ref = r.a;
+        float a = 0, b = 0;
+        cudaEventElapsedTime(&a, ref, r.a);
+        cudaEventElapsedTime(&b, ref, r.b);
+        lo = any ? std::min(lo, a) : a;
+        hi = any ? std::max(hi, b) : b;
+        any = true;
+    }
+    if (ms) *ms = any ? (double)(hi - lo) : 0.0;
+    return 0;
+}
+
 int64_t eucalc_last_bad_index(void) { return g_bad; }
 int64_t eucalc_launch_count(int reset) {
     int64_t v = g_launches;

@@ -27,7 +27,7 @@ ids = sorted(launch)
 half = ids[len(ids) // 2:]  # second iteration (warm)
 tot = sum(launch[i]["dram__bytes_read.sum"] + launch[i]["dram__bytes_write.sum"] for i in half)
 res = {"stage": "k2_transforms (k2w_count + k2_scan + k2w_emit + k3_table, fused HT)",
-       "dram_bytes_per_launch": tot / 2, "launches_per_stage_call": len(half) / 2,
+       "dram_bytes_per_launch": tot / 2, "dram_bytes_per_step": tot, "launches_per_stage_call": len(half) / 2,
        "source": "ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum (tools/traffic.py), "
                  "second iteration of tools/run_config2_once.py, mean of gray and binary",
        "per_kernel": [{k: launch[i][k] for k in launch[i]} for i in half]}
