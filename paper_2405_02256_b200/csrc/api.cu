@@ -769,6 +769,9 @@ eucalc_status eucalc_critical_points(const eucalc_complex *cx, void *stream, euc
         a.TY = TY;
         a.TZ = TZ;
         a.tile_off = cr->d_tile_off;
+        // TMA-staged persistent K1: opt-in, measured no faster than the plain
+        // kernel (K1 is issue-bound, not load-bound)
+        a.use_tma = getenv("EUCALC_K1_TMA") ? 1 : 0;
         a.tiles_x = tiles_x;
         a.tiles_y = tiles_y;
         a.tiles_z = tiles_z;
@@ -1353,12 +1356,7 @@ eucalc_status eucalc_hybrid_ex(const eucalc_critical *ccr, const int32_t *dirs, 
     const size_t osz = precision == EUCALC_F32 ? 4 : 8;
     const bool host_out = !is_device_ptr(out);
     std::vector<void *> scratch;
-    auto dalloc = [&](size_t bytes) -> void * {
-        void *q = nullptr;
-        if (cudaMallocAsync(&q, bytes, st) != cudaSuccess) return nullptr;
-        scratch.push_back(q);
-        return q;
-    };
+    
     auto free_scratch = [&]() { for (void *q : scratch) cudaFreeAsync(q, st); };
     const DirInfo *d_info = pe->d_info;
     const int32_t *d_order = pe->d_order, *d_ts = pe->d_ts, *d_tl = pe->d_tl, *d_cs = pe->d_csum;

@@ -88,6 +88,7 @@ struct K1Args {
     int64_t *stats;
     int64_t *abs_sum;
     int64_t *max_rec;
+    int use_tma;  // TMA-staged persistent kernel when the image layout allows it
 };
 cudaError_t launch_k1(const K1Args &a, cudaStream_t s);
 

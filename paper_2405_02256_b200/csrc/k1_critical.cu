@@ -28,6 +28,11 @@
 // Tiles are boxes of <= kTileV vertices (the whole image when it fits; else
 // 64 x 32 in 2-D, 16 x 16 x 8 in 3-D), so a tile spans a narrow band of heights
 // in every direction; K1 records each tile's list offset for K2's culling.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+
 #include <climits>
 #include <type_traits>
 
@@ -178,24 +183,30 @@ __device__ __forceinline__ void vertex_dminus(const int *s, int sz, int sy, int 
     });
 }
 
+// Shared state of one tile (per CTA).
+template <int N>
+struct K1Shared {
+    int warp[kThreads / 32][1 << (N - 1)];
+    int run[1 << (N - 1)];
+    long long excl[1 << (N - 1)];
+    int ostat[1 << N][2];
+};
+
+// One tile: stage the image region (from global memory, or from the raw TMA box
+// `raw` of xbox x ybox x zbox elements at image coordinates (x0-xoff, y0-1, z0-1),
+// xoff = 16 bytes of elements: TMA wants 16-byte aligned innermost box starts),
+// run the stencil, compact, look back, copy out. All threads of the CTA call it;
+// `sh.ostat` must be zero on entry (it is left zero on exit).
 template <int N, int CONS, typename TIn, typename RecT>
-__global__ void __launch_bounds__(kThreads) k1_kernel(K1Args a) {
+__device__ __forceinline__ void k1_tile(const K1Args &a, unsigned ticket, const TIn *raw, int xbox, int ybox,
+                                        RecT *stage, int *reg, K1Shared<N> &sh) {
     constexpr int Q = 1 << (N - 1);
     constexpr int FULL = (1 << N) - 1;
-    extern __shared__ __align__(16) unsigned char smem[];
-    RecT *stage = reinterpret_cast<RecT *>(smem);                 // [Q][kTileV]
-    int *reg = reinterpret_cast<int *>(stage + Q * kTileV);        // input region
-    __shared__ int s_warp[kThreads / 32][Q];
-    __shared__ int s_run[Q];
-    __shared__ long long s_excl[Q];
-    __shared__ unsigned s_ticket;
-    __shared__ int s_ostat[1 << N][2];
-
+    auto &s_warp = sh.warp;
+    auto &s_run = sh.run;
+    auto &s_excl = sh.excl;
+    auto &s_ostat = sh.ostat;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    if (tid == 0) s_ticket = atomicAdd(a.ticket, 1u);
-    if (tid < (1 << N) * 2) (&s_ostat[0][0])[tid] = 0;
-    __syncthreads();
-    const unsigned ticket = s_ticket;
     const int tiles_per_img = a.tiles_x * a.tiles_y * a.tiles_z;
     const int64_t b = ticket / tiles_per_img;
     const int t = ticket % tiles_per_img;
@@ -222,11 +233,19 @@ __global__ void __launch_bounds__(kThreads) k1_kernel(K1Args a) {
         const int pz = row / RY, ry = row - pz * RY;
         const int gy = y0 - 1 + ry, gz = (N == 3) ? z0 - 1 + pz : 0;
         const bool rin = gy >= 0 && gy < mY && gz >= 0 && gz < mZ;
-        const TIn *src = img + ((int64_t)gz * mY + gy) * mX;
         int *dst = reg + row * RX;
-        for (int rx = lane; rx < RX; rx += 32) {
-            const int gx = x0 - 1 + rx;
-            dst[rx] = (rin && gx >= 0 && gx < mX) ? load_img(src, gx) : SENT;
+        if (raw) {  // TMA box already in shared memory (out-of-range elements zero-filled)
+            const TIn *src = raw + ((long long)pz * ybox + ry) * xbox + (16 / (int)sizeof(TIn) - 1);
+            for (int rx = lane; rx < RX; rx += 32) {
+                const int gx = x0 - 1 + rx;
+                dst[rx] = (rin && gx >= 0 && gx < mX) ? (int)src[rx] : SENT;
+            }
+        } else {
+            const TIn *src = img + ((int64_t)gz * mY + gy) * mX;
+            for (int rx = lane; rx < RX; rx += 32) {
+                const int gx = x0 - 1 + rx;
+                dst[rx] = (rin && gx >= 0 && gx < mX) ? load_img(src, gx) : SENT;
+            }
         }
     }
     __syncthreads();
@@ -333,6 +352,7 @@ __global__ void __launch_bounds__(kThreads) k1_kernel(K1Args a) {
     if (tid < (1 << N) * 2) {
         int v = (&s_ostat[0][0])[tid];
         if (v) atomicAdd((unsigned long long *)&a.stats[b * (1 << N) * 2 + tid], (unsigned long long)v);
+        (&s_ostat[0][0])[tid] = 0;  // ready for the CTA's next tile
     }
 
     // ---- look-back per pair (warp q), then ordered copy-out
@@ -369,18 +389,183 @@ __global__ void __launch_bounds__(kThreads) k1_kernel(K1Args a) {
         const RecT *src = stage + q * kTileV + warp * kPerWarp;
         for (int i = lane; i < s_warp[warp][q]; i += 32) dst[i] = src[i];
     }
+    __syncthreads();  // staging, region and shared counters are reused by the next tile
+}
+
+template <int N, int CONS, typename TIn, typename RecT>
+__global__ void __launch_bounds__(kThreads) k1_kernel(K1Args a) {
+    constexpr int Q = 1 << (N - 1);
+    extern __shared__ __align__(16) unsigned char smem[];
+    RecT *stage = reinterpret_cast<RecT *>(smem);           // [Q][kTileV]
+    int *reg = reinterpret_cast<int *>(stage + Q * kTileV);  // input region
+    __shared__ K1Shared<N> sh;
+    __shared__ unsigned s_ticket;
+    if (threadIdx.x == 0) s_ticket = atomicAdd(a.ticket, 1u);
+    if (threadIdx.x < (1 << N) * 2) (&sh.ostat[0][0])[threadIdx.x] = 0;
+    __syncthreads();
+    k1_tile<N, CONS, TIn, RecT>(a, s_ticket, nullptr, 0, 0, stage, reg, sh);
+}
+
+// ---- TMA-staged K1 for large images: a persistent CTA keeps the next tile's
+// box (image region + halo) in flight with cp.async.bulk.tensor while it works
+// on the current one (double buffer, one mbarrier per buffer). Requires 16-byte
+// aligned image rows; the tensor map is 3-D (x, y, image) or 4-D (x, y, z, image).
+__device__ __forceinline__ uint32_t smem_addr(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+template <int N>
+__device__ __forceinline__ void tma_box(const CUtensorMap *tm, void *dst, unsigned long long *bar, int x, int y, int z,
+                                        int b) {
+    if (N == 2)
+        asm volatile(
+            "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];"
+            ::"r"(smem_addr(dst)), "l"(tm), "r"(x), "r"(y), "r"(b), "r"(smem_addr(bar))
+            : "memory");
+    else
+        asm volatile(
+            "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], "
+            "[%6];" ::"r"(smem_addr(dst)),
+            "l"(tm), "r"(x), "r"(y), "r"(z), "r"(b), "r"(smem_addr(bar))
+            : "memory");
+}
+
+template <int N, int CONS, typename TIn, typename RecT>
+__global__ void __launch_bounds__(kThreads) k1_tma(const __grid_constant__ CUtensorMap tm, K1Args a, int xbox, int ybox,
+                                                   int zbox) {
+    constexpr int Q = 1 << (N - 1);
+    extern __shared__ __align__(128) unsigned char k1_smem_tma[];
+    const int box_bytes = xbox * ybox * zbox * (int)sizeof(TIn);
+    const int box_pad = (box_bytes + 127) / 128 * 128;
+    TIn *raw[2] = {reinterpret_cast<TIn *>(k1_smem_tma), reinterpret_cast<TIn *>(k1_smem_tma + box_pad)};
+    RecT *stage = reinterpret_cast<RecT *>(k1_smem_tma + 2 * box_pad);  // [Q][kTileV]
+    int *reg = reinterpret_cast<int *>(stage + Q * kTileV);        // input region
+    __shared__ K1Shared<N> sh;
+    __shared__ unsigned long long bar[2];
+    __shared__ unsigned s_next;
+    const int tiles_per_img = a.tiles_x * a.tiles_y * a.tiles_z;
+    const unsigned total = (unsigned)(a.batch * tiles_per_img);
+    auto issue = [&](unsigned tk, int buf) {  // thread 0: TMA of tile tk's box into raw[buf]
+        const int b = (int)(tk / tiles_per_img), t = (int)(tk % tiles_per_img);
+        const int tx = t % a.tiles_x, ty = (t / a.tiles_x) % a.tiles_y, tz = t / (a.tiles_x * a.tiles_y);
+        asm volatile("mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(&bar[buf])),
+                     "r"(box_bytes)
+                     : "memory");
+        tma_box<N>(&tm, raw[buf], &bar[buf], tx * a.TX - 16 / (int)sizeof(TIn), ty * a.TY - 1, N == 3 ? tz * a.TZ - 1 : 0, b);
+    };
+    if (threadIdx.x == 0) {
+        for (int k = 0; k < 2; ++k)
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(&bar[k])) : "memory");
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        s_next = atomicAdd(a.ticket, 1u);
+        if (s_next < total) issue(s_next, 0);
+    }
+    if (threadIdx.x < (1 << N) * 2) (&sh.ostat[0][0])[threadIdx.x] = 0;
+    __syncthreads();
+    unsigned cur = s_next;
+    int buf = 0;
+    unsigned phase[2] = {0, 0};
+    while (cur < total) {
+        __syncthreads();  // every thread has read s_next
+        if (threadIdx.x == 0) {
+            s_next = atomicAdd(a.ticket, 1u);
+            if (s_next < total) issue(s_next, buf ^ 1);  // raw[buf^1] was consumed by the previous tile
+        }
+        // wait for this tile's box
+        asm volatile(
+            "{\n\t.reg .pred p;\nK1W_%=:\n\t"
+            "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%0], %1;\n\t"
+            "@!p bra K1W_%=;\n}" ::"r"(smem_addr(&bar[buf])),
+            "r"(phase[buf])
+            : "memory");
+        phase[buf] ^= 1;
+        k1_tile<N, CONS, TIn, RecT>(a, cur, raw[buf], xbox, ybox, stage, reg, sh);  // ends with __syncthreads
+        cur = s_next;
+        buf ^= 1;
+    }
+}
+
+
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda)
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    static bool tried = false;
+    if (!tried) {
+        tried = true;
+        void *p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+        cudaGetLastError();
+    }
+    return fn;
+}
+
+template <typename TIn>
+CUtensorMapDataType tma_type() {
+    return sizeof(TIn) == 1 ? CU_TENSOR_MAP_DATA_TYPE_UINT8
+                            : sizeof(TIn) == 2 ? CU_TENSOR_MAP_DATA_TYPE_UINT16 : CU_TENSOR_MAP_DATA_TYPE_INT32;
 }
 
 template <int N, int CONS, typename TIn, typename RecT>
 cudaError_t launch_t(const K1Args &a, cudaStream_t s) {
     constexpr int Q = 1 << (N - 1);
     const int planes = (N == 3) ? a.TZ + 2 : 1;
-    size_t smem = sizeof(RecT) * Q * kTileV + sizeof(int) * planes * (a.TY + 2) * (a.TX + 2);
+    const size_t region = sizeof(int) * planes * (a.TY + 2) * (a.TX + 2);
+    const size_t stage = sizeof(RecT) * Q * kTileV;
+    const int64_t ntiles = a.batch * (int64_t)a.tiles_x * a.tiles_y * a.tiles_z;
+    // TMA path: tiled images with 16-byte aligned base, rows and tile origins, boxes
+    // within 256 per dimension. The innermost box start must be 16-byte aligned
+    // (measured: other starts fault), so a box spans cols x0-xoff .. x0+TX rounded
+    // up to xoff, xoff = 16 bytes of elements, instead of the one-column halo.
+    const int e = (int)sizeof(TIn), xoff = 16 / e;
+    const int xbox = (xoff + a.TX + 1 + xoff - 1) / xoff * xoff, ybox = a.TY + 2, zbox = N == 3 ? a.TZ + 2 : 1;
+    const bool tma = ntiles > 1 && ((int64_t)a.m[N - 1] * e) % 16 == 0 && (a.TX * e) % 16 == 0 &&
+                     ((uintptr_t)a.img & 15) == 0 && xbox <= 256 && ybox <= 256 && zbox <= 256 &&
+                     encode_fn() != nullptr && a.use_tma;
+    if (tma) {
+        CUtensorMap tm;
+        cuuint64_t dims[5], strides[4];
+        cuuint32_t box[5], estr[5] = {1, 1, 1, 1, 1};
+        int rank = 0;
+        dims[rank] = (cuuint64_t)a.m[N - 1];
+        box[rank++] = (cuuint32_t)xbox;
+        dims[rank] = (cuuint64_t)a.m[N - 2];
+        box[rank++] = (cuuint32_t)ybox;
+        if (N == 3) {
+            dims[rank] = (cuuint64_t)a.m[0];
+            box[rank++] = (cuuint32_t)zbox;
+        }
+        dims[rank] = (cuuint64_t)a.batch;
+        box[rank++] = 1;
+        cuuint64_t st = (cuuint64_t)a.m[N - 1] * e;
+        for (int k = 0; k < rank - 1; ++k) {
+            strides[k] = st;
+            st *= dims[k + 1];
+        }
+        CUresult r = encode_fn()(&tm, tma_type<TIn>(), (cuuint32_t)rank, const_cast<void *>(a.img), dims, strides, box,
+                                 estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                 CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r == CUDA_SUCCESS) {
+            const size_t box_pad = ((size_t)xbox * ybox * zbox * e + 127) / 128 * 128;
+            const size_t smem = 2 * box_pad + stage + region;
+            auto kern = k1_tma<N, CONS, TIn, RecT>;
+            int occ = 0;
+            cudaError_t err = prepare_kernel((const void *)kern, kThreads, smem, &occ);
+            if (err != cudaSuccess) return err;
+            int dev = 0, sms = 148;
+            cudaGetDevice(&dev);
+            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+            const int64_t grid = std::min<int64_t>(ntiles, (int64_t)std::max(occ, 1) * sms);
+            kern<<<(unsigned)grid, kThreads, smem, s>>>(tm, a, xbox, ybox, zbox);
+            count_launch();
+            return cudaGetLastError();
+        }
+    }
+    const size_t smem = stage + region;
     auto kern = k1_kernel<N, CONS, TIn, RecT>;
-    cudaError_t e = prepare_kernel((const void *)kern, kThreads, smem, nullptr);
-    if (e != cudaSuccess) return e;
-    int64_t nblocks = a.batch * (int64_t)a.tiles_x * a.tiles_y * a.tiles_z;
-    kern<<<(unsigned)nblocks, kThreads, smem, s>>>(a);
+    cudaError_t err = prepare_kernel((const void *)kern, kThreads, smem, nullptr);
+    if (err != cudaSuccess) return err;
+    kern<<<(unsigned)ntiles, kThreads, smem, s>>>(a);
     count_launch();
     return cudaGetLastError();
 }

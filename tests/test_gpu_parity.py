@@ -370,3 +370,30 @@ def test_degenerate_images(construction):
     one = np.array([[[3]]], np.uint8)
     cx1, cr1, r1 = run_gpu(one, np.array([[1, 1]], np.int32), construction)
     check_transforms(one, np.array([[1, 1]], np.int32), construction, r1)
+
+
+K1_TMA_CASES = [((96, 128), np.uint8, "vertex"), ((96, 128), np.uint8, "top"), ((50, 72), np.int16, "vertex"),
+                ((40, 36), np.int32, "top"), ((20, 24, 32), np.uint8, "vertex"), ((19, 23, 16), np.uint8, "top"),
+                ((9, 10, 16), np.int16, "vertex")]
+
+
+@pytest.mark.parametrize("case", K1_TMA_CASES, ids=lambda c: f"{c[0]}-{np.dtype(c[1]).name}-{c[2]}")
+def test_k1_tma_staging(case, monkeypatch):
+    """With EUCALC_K1_TMA set, tiled images with 16-byte aligned rows take the TMA-staged persistent K1
+    (cp.async.bulk.tensor boxes, double-buffered); its lists equal the oracle's and
+    the plain kernel's exactly."""
+    shape, dt, construction = case
+    monkeypatch.setenv("EUCALC_K1_TMA", "1")
+    rng = np.random.default_rng(sum(shape))
+    lo, hi = (0, 256) if dt == np.uint8 else (-300, 300)
+    images = rng.integers(lo, hi, size=(2, *shape)).astype(dt)
+    dirs = synth.random_directions(5, len(shape), 7, 3)
+    cx, cr, res = run_gpu(images, dirs, construction)
+    check_critical(images, construction, cr, imgs_to_check=[1])
+    check_transforms(images, dirs, construction, res, pairs=[(0, 0), (1, 4)])
+    monkeypatch.delenv("EUCALC_K1_TMA")
+    cr2 = eu.critical_points(eu.build_complex(images, construction))
+    for b in range(2):
+        for e in range(1 << len(shape)):
+            for x, y in zip(cr.export(b, e), cr2.export(b, e)):
+                np.testing.assert_array_equal(x, y)

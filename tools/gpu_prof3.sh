@@ -5,5 +5,5 @@ one() { tag=$1; rx=$2; sk=$3; shift 3
   python tools/ncu_summary.py full $OUT/$tag.ncu-rep > $OUT/$tag.full.txt 2>&1
   python tools/ncu_source.py $OUT/$tag.ncu-rep 25 > $OUT/$tag.source.txt 2>&1
   rm -f $OUT/$tag.ncu-rep; }
-one k3t_f32 k3t 4 python tools/bench_configs.py --configs 5 --steps 1 --warmup 0
-#one k1_c4 k1_kernel 1 python tools/bench_configs.py --configs 4 --steps 1 --warmup 1
+#one k3t_f32 k3t 4 python tools/bench_configs.py --configs 5 --steps 1 --warmup 0
+one k1_c4 k1_kernel 1 python tools/bench_configs.py --configs 4 --steps 1 --warmup 1
