@@ -1189,7 +1189,6 @@ eucalc_status eucalc_transforms_real(const eucalc_critical *ccr, const double *d
         if (o->capacity < bnd) return fail(EUCALC_E_CAPACITY, "capacity " + std::to_string(o->capacity) + " < required bound " + std::to_string(bnd));
     }
     if (!ect && !ordinary && !classical) return EUCALC_OK;
-    if (cr->max_count > 4096) return fail(EUCALC_E_ARG, "real-valued directions: critical lists of more than 4096 records are not supported (bitonic sort in shared memory)");
     if (cr->max_abs_sum >= (int64_t(1) << 31)) return fail(EUCALC_E_RANGE, "total |weight| of a critical list exceeds 2^31");
     const int64_t S = cx->batch * D;
     if (S == 0) return EUCALC_OK;
@@ -1224,6 +1223,55 @@ eucalc_status eucalc_transforms_real(const eucalc_critical *ccr, const double *d
             dev[i].v = o->value;
         }
     }
+    // Lists longer than kSmallMax take the bucketed path (K5Big): planned here in
+    // segment order and cut into chunks whose scratch fits a memory budget.
+    // (EUCALC_K5_SMALL_MAX / EUCALC_K5_BUCKET: test hooks that force the bucketed
+    // path, and oversize pieces, on inputs small enough for the oracle)
+    int64_t kSmallMax = 4096, bucket = kK5Bucket;
+    if (const char *v = getenv("EUCALC_K5_SMALL_MAX")) kSmallMax = std::min<int64_t>(4096, std::max<int64_t>(0, atoll(v)));
+    if (const char *v = getenv("EUCALC_K5_BUCKET")) bucket = std::max<int64_t>(1, atoll(v));
+    int64_t small_np = 0;
+    std::vector<int64_t> g_seg, g_pbase, g_sbase;
+    std::vector<int32_t> g_nb;
+    struct Chunk {
+        int64_t i0, i1, npieces, nrec;
+        int nb_max;
+    };
+    std::vector<Chunk> chunks;
+    {
+        size_t fr = 0, tot = 0;
+        if (cudaMemGetInfo(&fr, &tot) != cudaSuccess) fr = size_t(4) << 30;
+        const int64_t budget_rec = std::max<int64_t>(1, (int64_t)(std::min<size_t>(fr / 4, size_t(8) << 30) / 32));
+        Chunk cur{0, 0, 0, 0, 0};
+        for (int64_t b = 0; b < cx->batch; ++b)
+            for (int64_t d = 0; d < D; ++d) {
+                const int64_t nrec = cr->h_count[b * cr->Q + hq[d]];
+                if (nrec <= kSmallMax) {
+                    small_np = std::max(small_np, nrec);
+                    continue;
+                }
+                const int32_t nb = (int32_t)std::min<int64_t>(kK5MaxBuckets, (nrec + bucket - 1) / bucket);
+                if (cur.i1 > cur.i0 && cur.nrec + nrec > budget_rec) {
+                    chunks.push_back(cur);
+                    cur = Chunk{cur.i1, cur.i1, 0, 0, 0};
+                }
+                g_seg.push_back(b * D + d);
+                g_pbase.push_back(cur.npieces);
+                g_sbase.push_back(cur.nrec);
+                g_nb.push_back(nb);
+                cur.i1 += 1;
+                cur.npieces += nb;
+                cur.nrec += nrec;
+                cur.nb_max = std::max(cur.nb_max, (int)nb);
+            }
+        if (cur.i1 > cur.i0) chunks.push_back(cur);
+    }
+    const int64_t nbig = (int64_t)g_seg.size();
+    int64_t max_rec = 0, max_p = 0;
+    for (const Chunk &c : chunks) {
+        max_rec = std::max(max_rec, c.nrec);
+        max_p = std::max(max_p, c.npieces);
+    }
     double *d_xi = (double *)dalloc(sizeof(double) * D * n);
     int32_t *d_q = (int32_t *)dalloc(sizeof(int32_t) * D), *d_sw = (int32_t *)dalloc(sizeof(int32_t) * D);
     unsigned long long *flags = (unsigned long long *)dalloc(sizeof(unsigned long long) * S);
@@ -1233,9 +1281,37 @@ eucalc_status eucalc_transforms_real(const eucalc_critical *ccr, const double *d
         free_scratch();
         return fail(EUCALC_E_NOMEM, "scratch");
     }
+    K5Big big{};
+    int64_t *d_gseg = nullptr, *d_gpbase = nullptr, *d_gsbase = nullptr;
+    int32_t *d_gnb = nullptr;
+    if (nbig > 0) {
+        d_gseg = (int64_t *)dalloc(sizeof(int64_t) * nbig);
+        d_gpbase = (int64_t *)dalloc(sizeof(int64_t) * nbig);
+        d_gsbase = (int64_t *)dalloc(sizeof(int64_t) * nbig);
+        d_gnb = (int32_t *)dalloc(sizeof(int32_t) * nbig);
+        big.scr = (uint4 *)dalloc(16 * (size_t)max_rec);
+        big.tmp = (uint4 *)dalloc(16 * (size_t)max_rec);
+        big.p_start = (int64_t *)dalloc(sizeof(int64_t) * max_p);
+        int32_t *pa = (int32_t *)dalloc(sizeof(int32_t) * max_p * 11);
+        big.over = (unsigned *)dalloc(sizeof(unsigned) * (2 + max_p));
+        if (!d_gseg || !d_gpbase || !d_gsbase || !d_gnb || !big.scr || !big.tmp || !big.p_start || !pa || !big.over) {
+            free_scratch();
+            return fail(EUCALC_E_NOMEM, "scratch for long lists");
+        }
+        int32_t **arr[11] = {&big.p_len, &big.p_seg, &big.p_nc, &big.p_no, &big.p_sc, &big.p_sj,
+                             &big.p_offc, &big.p_offo, &big.p_ic, &big.p_ij, nullptr};
+        for (int k = 0; k < 10; ++k) *arr[k] = pa + (size_t)k * max_p;
+        big.over_cap = max_p;
+    }
     cudaError_t e = cudaMemcpyAsync(d_xi, h.data(), sizeof(double) * D * n, cudaMemcpyHostToDevice, st);
     if (e == cudaSuccess) e = cudaMemcpyAsync(d_q, hq.data(), sizeof(int32_t) * D, cudaMemcpyHostToDevice, st);
     if (e == cudaSuccess) e = cudaMemcpyAsync(d_sw, hsw.data(), sizeof(int32_t) * D, cudaMemcpyHostToDevice, st);
+    if (e == cudaSuccess && nbig > 0) {
+        e = cudaMemcpyAsync(d_gseg, g_seg.data(), sizeof(int64_t) * nbig, cudaMemcpyHostToDevice, st);
+        if (e == cudaSuccess) e = cudaMemcpyAsync(d_gpbase, g_pbase.data(), sizeof(int64_t) * nbig, cudaMemcpyHostToDevice, st);
+        if (e == cudaSuccess) e = cudaMemcpyAsync(d_gsbase, g_sbase.data(), sizeof(int64_t) * nbig, cudaMemcpyHostToDevice, st);
+        if (e == cudaSuccess) e = cudaMemcpyAsync(d_gnb, g_nb.data(), sizeof(int32_t) * nbig, cudaMemcpyHostToDevice, st);
+    }
     if (e == cudaSuccess) e = cudaMemsetAsync(flags, 0, sizeof(unsigned long long) * S, st);
     if (e == cudaSuccess) e = cudaMemsetAsync(ticket, 0, sizeof(unsigned int) * 4, st);
     if (e == cudaSuccess) {
@@ -1257,8 +1333,9 @@ eucalc_status eucalc_transforms_real(const eucalc_critical *ccr, const double *d
         a.D = D;
         a.batch = cx->batch;
         int np2 = 32;
-        while (np2 < cr->max_count) np2 <<= 1;
+        while (np2 < small_np) np2 <<= 1;
         a.npow2 = np2;
+        a.small_max = (int)kSmallMax;
         a.cnt_c = cnts;
         a.cnt_o = cnts + S;
         a.do_ect = ect != nullptr;
@@ -1277,7 +1354,28 @@ eucalc_status eucalc_transforms_real(const eucalc_critical *ccr, const double *d
         a.scan.flags = flags;
         a.scan.ticket = ticket;
         ProfScope ps("k5_real", st);
-        e = launch_k5(a, st, num_sms());
+        const int sms = num_sms();
+        auto chunk_big = [&](const Chunk &c) {
+            K5Big g = big;
+            g.seg = d_gseg + c.i0;
+            g.pbase = d_gpbase + c.i0;
+            g.sbase = d_gsbase + c.i0;
+            g.nb = d_gnb + c.i0;
+            g.nseg = c.i1 - c.i0;
+            g.npieces = c.npieces;
+            return g;
+        };
+        // one chunk: its sorted pieces stay in scratch for the emit pass; several
+        // chunks: counts in a first round, everything redone per chunk to emit
+        for (size_t c = 0; c < chunks.size() && e == cudaSuccess; ++c)
+            e = launch_k5b_prepare(a, chunk_big(chunks[c]), chunks[c].nb_max, st, sms);
+        if (e == cudaSuccess) e = launch_k5(a, 0, st, sms);
+        if (e == cudaSuccess) e = launch_k5_scan(a, st);
+        if (e == cudaSuccess) e = launch_k5(a, 1, st, sms);
+        for (size_t c = 0; c < chunks.size() && e == cudaSuccess; ++c) {
+            if (chunks.size() > 1) e = launch_k5b_prepare(a, chunk_big(chunks[c]), chunks[c].nb_max, st, sms);
+            if (e == cudaSuccess) e = launch_k5b_emit(a, chunk_big(chunks[c]), st, sms);
+        }
     }
     if (e == cudaSuccess && host_out) {
         for (int i = 0; i < 3 && e == cudaSuccess; ++i) {

@@ -224,13 +224,40 @@ struct K5Args {
     const int32_t *q;     // [D] antipodal pair of the direction's orthant
     const int32_t *swap;  // [D] 1 if the orthant is the pair's non-representative
     int64_t D, batch;
-    int npow2;            // sort length: power of two >= every list length
+    int npow2;            // sort length: power of two >= every small list length
+    int small_max;        // lists longer than this take the bucketed path (K5Big)
     int *cnt_c, *cnt_o;   // [batch*D]
     bool do_ect, do_ord, do_cls, cls_alias;
     StepsOut ect, ord, cls;  // heights double, values int64
     K2Args scan;          // offsets / ticket / flags for launch_csr_scan
 };
-cudaError_t launch_k5(const K5Args &a, cudaStream_t s, int num_sms);
+// Bucketed path for lists longer than small_max (one chunk of big segments):
+// value buckets -> pieces (contiguous in scratch, equal heights never split),
+// each piece sorted (warp bitonic, or a CTA sort for oversize pieces) and
+// run-length merged with the running sums of the pieces before it.
+struct K5Big {
+    const int64_t *seg;    // [nseg] segment ids s = b*D + d, ascending
+    const int64_t *pbase;  // [nseg] first piece (chunk-local)
+    const int32_t *nb;     // [nseg] buckets (= pieces) of the segment
+    const int64_t *sbase;  // [nseg] first scratch record
+    int64_t nseg, npieces;
+    uint4 *scr, *tmp;      // records {key lo, key hi, Delta^-, J}, and merge-sort ping-pong
+    int64_t *p_start;      // [npieces] first scratch record
+    int32_t *p_len, *p_seg;
+    int32_t *p_nc, *p_no, *p_sc, *p_sj;      // run counts and sums per piece
+    int32_t *p_offc, *p_offo, *p_ic, *p_ij;  // exclusive within the segment
+    unsigned *over;        // [0] oversize pieces, [1] ticket, then the list from over+2
+    int64_t over_cap;
+};
+constexpr int kK5PieceMax = 512;    // pieces up to this many records: warp sort in smem
+constexpr int kK5Bucket = 128;      // target records per bucket
+constexpr int kK5MaxBuckets = 32768;
+// phase 0: counts, 1: emit (small lists only; big segments are skipped)
+cudaError_t launch_k5(const K5Args &a, int phase, cudaStream_t s, int num_sms);
+cudaError_t launch_k5_scan(const K5Args &a, cudaStream_t s);
+// bucket + sort + per-piece counts + segment scan (writes cnt_c/cnt_o of its segments)
+cudaError_t launch_k5b_prepare(const K5Args &a, const K5Big &g, int nb_max, cudaStream_t s, int num_sms);
+cudaError_t launch_k5b_emit(const K5Args &a, const K5Big &g, cudaStream_t s, int num_sms);
 size_t k5_smem(int npow2);
 
 // thread-local launch counter (eucalc_launch_count)

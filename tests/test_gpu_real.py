@@ -88,7 +88,56 @@ def test_real_errors():
     with pytest.raises(eu.EucalcError) as ei:
         eu.transforms_real(cr, np.array([[0.5, 0.25], [0.0, 1.0]]))
     assert ei.value.status == eu.E_NONGENERIC and ei.value.bad_index == 1
-    big = eu.critical_points(eu.build_complex(synth.uniform_image((128, 128), 256, 3)[None], "vertex"))
-    with pytest.raises(eu.EucalcError) as ei:
-        eu.transforms_real(big, np.array([[0.5, 0.25]]))  # list > 4096 records
-    assert ei.value.status == eu.E_ARG
+
+
+# Bucketed path for long lists (> 4096 records; forced on smaller ones through the
+# EUCALC_K5_SMALL_MAX / EUCALC_K5_BUCKET hooks): value buckets -> pieces, warp
+# sorts, CTA sorts of oversize pieces (bitonic tiles of 8192 + merge passes).
+BIG_CASES = [
+    # (shape, levels, construction, dirs kind, bucket target)
+    ((40, 40), 256, "vertex", "unit", 4),        # many small pieces, empty buckets
+    ((40, 40), 256, "top", "signed", 128),       # default bucket target
+    ((40, 40), 256, "vertex", "unit", 100000),   # one oversize piece (CTA bitonic)
+    ((160, 160), 256, "vertex", "unit", 100000),  # oversize > 8192: merge passes
+    ((65, 65), 7, "vertex", "ties", 1),          # dyadic spacing: exact ties across records
+    ((65, 65), 7, "vertex", "ties", 100000),
+    ((17, 17, 17), 5, "vertex", "ties", 16),
+    ((9, 11, 13), 256, "top", "signed", 3),
+]
+
+
+@pytest.mark.parametrize("case", BIG_CASES, ids=lambda c: f"{c[0]}-{c[2]}-{c[3]}-b{c[4]}")
+def test_real_bucketed_forced(case, monkeypatch):
+    shape, levels, construction, kind, bucket = case
+    monkeypatch.setenv("EUCALC_K5_SMALL_MAX", "0")
+    monkeypatch.setenv("EUCALC_K5_BUCKET", str(bucket))
+    rng = np.random.default_rng(sum(shape) + bucket)
+    images = rng.integers(0, levels, size=(2, *shape)).astype(np.uint8)
+    n = len(shape)
+    if kind == "unit":
+        dirs = rng.uniform(1e-3, 1.0, size=(4, n))
+    elif kind == "signed":
+        dirs = rng.uniform(-2.0, 2.0, size=(4, n))
+        dirs[np.abs(dirs) < 1e-3] = 0.5
+    else:  # exact ties: dyadic coordinates x = p/64 - 1/2 (or 1/16) and small dyadic directions
+        dirs = np.array([[1.0] * n, [0.5] + [0.25] * (n - 1), [-1.0] + [2.0] * (n - 1), [0.75] * n])
+    pairs = [(b, d) for b in range(2) for d in range(len(dirs))]
+    if shape == (160, 160):
+        pairs = [(0, 0), (1, 3)]
+    check(images, dirs, construction, pairs=pairs)
+
+
+def test_real_long_lists_default():
+    """Lists over 4096 records take the bucketed path by default."""
+    img = synth.uniform_image((128, 128), 256, 3)[None]
+    cr = eu.critical_points(eu.build_complex(img, "vertex"))
+    assert int(cr.counts().max()) > 4096
+    check(img, np.array([[0.5, 0.25], [-0.3, 0.9]]), "vertex")
+
+
+def test_real_config3_sampled():
+    """Config 3 (2048^2 GRF, 1.75 M-record lists) with real directions: sampled pairs vs the oracle."""
+    c = synth.config_inputs(3, "gray")
+    img = c["images"]
+    dirs = np.array([[0.61, 0.23], [-0.17, 0.94], [0.5, -0.5]])
+    check(img, dirs, "vertex", pairs=[(0, 0), (0, 2)])

@@ -167,8 +167,35 @@ def exp_real(eu, torch):
                    image_directions_per_s=dev.shape[0] * 100 / (ms / 1e3))
 
 
+def exp_real_large(eu, torch):
+    """Real-valued directions on long lists (K5 bucketed path): config 3 (2048^2 GRF) and
+    config 4 (256^3) with directions uniform in [0,1]^n; and the paper's §5 size
+    experiment shape (1000 x 1000 image) with 100 such directions."""
+    cases = [("config3", synth.config_inputs(3, "gray")["images"], 2, 256),
+             ("config4", synth.config_inputs(4, "gray")["images"], 3, 64),
+             ("squares1000", synth.squares_image(1000, 250, 2)[None], 2, 100)]
+    for name, img, n, D in cases:
+        dev = torch.from_numpy(img).cuda()
+        dirs = np.random.default_rng(5).uniform(1e-3, 1.0, size=(D, n))
+        cr = eu.critical_points(eu.build_complex(dev, "vertex"))
+        recs = int(cr.counts().max())
+        ts = []
+        for it in range(4):
+            torch.cuda.synchronize()
+            eu.profile_enable(True)
+            eu.transforms_real(cr, dirs, share_heights=True)
+            torch.cuda.synchronize()
+            if it:
+                ts.append(eu.profile_read("k5_real")[0])
+            eu.profile_enable(False)
+        ms = float(np.median(ts))
+        yield dict(experiment="real_large", input=name, directions=D, max_list=recs, k5_real_ms=ms,
+                   directions_per_s=img.shape[0] * D / (ms / 1e3), records_per_s=recs * D / (ms / 1e3))
+
+
 EXPS = {"size": exp_size, "critical": exp_critical, "directions": exp_directions, "vectorize": exp_vectorize,
-        "levels": exp_levels, "real": exp_real}
+        "levels": exp_levels, "real": exp_real,
+        "real_large": exp_real_large}
 
 
 def main():
