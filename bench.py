@@ -132,24 +132,21 @@ def run_step(eu, torch, imgs_dev, dirs, record=None):
     """One pass of the whole hot path over both variants. Returns host-free results.
 
     The two variants (independent batches) go to two CUDA streams forked from and
-    joined back into the current stream, so one variant's small kernels and
-    launch tails overlap the other's work."""
+    joined back into the current stream. The gray variant's calls are issued
+    first and in full (its K2 is the step's longest stage, so its launch should
+    leave the host as early as possible); the binary variant's calls are issued
+    while gray's K2 runs and overlap it on the second stream."""
     cur = torch.cuda.current_stream()
     while len(_STREAMS) < len(imgs_dev):
         _STREAMS.append(torch.cuda.Stream())
     streams = _STREAMS[:len(imgs_dev)]
     for st in streams:
         st.wait_stream(cur)
-    # enqueue A0-A2 for both variants before the first call that waits on K1
-    cxs, crs = [], []
+    out = []
     for img, st in zip(imgs_dev, streams):
         with torch.cuda.stream(st):
             cx = eu.build_complex(img, "vertex", stream=st)
-            cxs.append(cx)
-            crs.append(eu.critical_points(cx, stream=st))
-    out = []
-    for cx, cr, st in zip(cxs, crs, streams):
-        with torch.cuda.stream(st):
+            cr = eu.critical_points(cx, stream=st)
             # ECT + Radon + HT in one pass over the merged histogram (eucalc_transforms_ht)
             r = eu.transforms(cr, dirs, elem_bytes="auto", share_heights=True, ht=(HT_KERNEL, 1.0, "f64"),
                               stream=st)

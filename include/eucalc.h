@@ -128,7 +128,8 @@ eucalc_status eucalc_output_bound(const eucalc_critical *cr, const int32_t *dirs
  * (ect/classical: bound_ect, ordinary: bound_ordinary), else E_CAPACITY with
  * *required_out (if non-NULL) = that bound and nothing written. Element widths
  * 2 and 4 are accepted when every height and value provably fits int16 / int32
- * (host-checked bounds from K1's statistics), else E_RANGE.
+ * (host-checked bounds from K1's statistics), else E_RANGE; E_RANGE also when
+ * batch * D >= 2^31 segments or the total output exceeds 2^31 entries.
  * The exact total of segment s is offsets[s+1] - offsets[s].
  * Device outputs: asynchronous except the first bound query. Host outputs:
  * computed into library scratch and copied back, then `stream` is synchronised.

@@ -237,9 +237,11 @@ def _alloc_steps(torch, S, cap, elem_bytes, device, with_height=True):
     return dict(offsets=off, height=h, value=v), st
 
 
-def _alloc_all(torch, S, cap, elem_bytes, device, names, share):
+def _alloc_all(torch, S, cap, elem_bytes, device, names, share, extra=None):
     """All requested CSR streams carved out of ONE allocation (one allocator call
-    instead of up to nine): offsets first (8-byte aligned), then heights/values."""
+    instead of up to nine): offsets first (8-byte aligned), then heights/values.
+    extra=(shape, dtype) appends one more tensor (the fused HT output), returned
+    as res["_extra"]."""
     dt = {2: torch.int16, 4: torch.int32, 8: torch.int64}[elem_bytes]
     pin = device == "cpu" and torch.cuda.is_available()
     cap1 = max(cap, 1)
@@ -252,6 +254,11 @@ def _alloc_all(torch, S, cap, elem_bytes, device, names, share):
         has_h = not (name == "classical" and share)
         plan.append((name, total, has_h))
         total += offb + arr * (2 if has_h else 1)
+    xoff = total
+    if extra is not None:
+        xshape, xdt = extra
+        xn = int(np.prod(xshape)) * torch.empty(0, dtype=xdt).element_size()
+        total += (xn + 255) // 256 * 256
     buf = torch.empty(total, dtype=torch.uint8, device=device, pin_memory=pin)
     res, sts = {}, {}
     for name, o, has_h in plan:
@@ -264,6 +271,8 @@ def _alloc_all(torch, S, cap, elem_bytes, device, names, share):
         v = buf[p:p + cap1 * elem_bytes].view(dt)
         res[name] = dict(offsets=off, height=h, value=v)
         sts[name] = _Steps(off.data_ptr(), h.data_ptr() if h is not None else 0, v.data_ptr(), cap, elem_bytes, 0)
+    if extra is not None:
+        res["_extra"] = buf[xoff:xoff + xn].view(xdt).view(xshape)
     return res, sts
 
 
@@ -298,7 +307,10 @@ def transforms(cr: Critical, dirs, ect=True, ordinary=True, classical=True, elem
     bound = be.value
     names = [n for n, want in (("ect", ect), ("ordinary", ordinary), ("classical", classical)) if want]
     share = share_heights and ect and classical
-    res, sts = _alloc_all(torch, S, bound, elem_bytes, device, names, share)
+    extra = None
+    if ht is not None:  # the HT output shares the CSR allocation
+        extra = ((cr.cx.batch, D), torch.float32 if ht[2] == "f32" else torch.float64)
+    res, sts = _alloc_all(torch, S, bound, elem_bytes, device, names, share, extra)
     if share:
         res["classical"]["height"] = res["ect"]["height"]
         sts["classical"].height = sts["ect"].height
@@ -308,9 +320,7 @@ def transforms(cr: Critical, dirs, ect=True, ordinary=True, classical=True, elem
         _check(lib().eucalc_transforms(cr._h, p, D, refs[0], refs[1], refs[2], ctypes.byref(req), st), req.value)
     else:
         kern, param, prec = ht
-        pin = device == "cpu" and torch.cuda.is_available()
-        out = torch.empty((cr.cx.batch, D), dtype=torch.float32 if prec == "f32" else torch.float64, device=device,
-                          pin_memory=pin)
+        out = res.pop("_extra")
         _check(lib().eucalc_transforms_ht(cr._h, p, D, refs[0], refs[1], refs[2], KERNELS[kern], float(param),
                                           PRECISIONS[prec], ctypes.c_void_p(out.data_ptr()), ctypes.byref(req), st),
                req.value)

@@ -977,6 +977,7 @@ eucalc_status transforms_impl(const eucalc_critical *ccr, const int32_t *dirs, i
     }
     const int64_t S = cx->batch * D;
     if (S == 0) return EUCALC_OK;
+    if (S >= (int64_t(1) << 31)) return fail(EUCALC_E_RANGE, "more than 2^31 (image, direction) segments in one call");
     const bool cls_alias = classical && ect && (classical->height == ect->height || !classical->height);
     if (classical && !classical->height && !ect) return fail(EUCALC_E_ARG, "classical height is NULL");
     // host outputs -> device scratch
@@ -1019,6 +1020,7 @@ eucalc_status transforms_impl(const eucalc_critical *ccr, const int32_t *dirs, i
     for (int64_t i = 0; i < cx->batch * cr->Q; ++i) min_count = std::min(min_count, cr->h_count[i]);
     int sparse_max = 32;  // EUCALC_K2_SPARSE_MAX (0..32) overrides, for measurements
     if (const char *v = getenv("EUCALC_K2_SPARSE_MAX")) sparse_max = std::max(0, std::min(32, atoi(v)));
+    if (p.R_max >= (1 << 25)) sparse_max = 0;  // the register sort keys are bin << 5 | lane
     const bool slab_ok = min_count <= sparse_max && p.R_max <= 32767 && cr->max_abs_sum < 32768 && cr->max_count <= 32768;
     // fused HT: the kbar table over the directions' u range, and the output
     const int64_t U = p.U1 - p.U0 + 1;
@@ -1089,6 +1091,7 @@ eucalc_status transforms_impl(const eucalc_critical *ccr, const int32_t *dirs, i
         a.cnt_o = cnts + S;
         a.slab = slab;
         a.sparse_max = sparse_max;
+        a.sum16 = cr->max_abs_sum < 32768;
         ProfScope ps("k2_transforms", st);
         e = launch_k2(a, st, num_sms());
     }
@@ -1192,6 +1195,7 @@ eucalc_status eucalc_transforms_real(const eucalc_critical *ccr, const double *d
     if (cr->max_abs_sum >= (int64_t(1) << 31)) return fail(EUCALC_E_RANGE, "total |weight| of a critical list exceeds 2^31");
     const int64_t S = cx->batch * D;
     if (S == 0) return EUCALC_OK;
+    if (S >= (int64_t(1) << 31)) return fail(EUCALC_E_RANGE, "more than 2^31 (image, direction) segments in one call");
     const bool cls_alias = classical && ect && (classical->height == ect->height || !classical->height);
     if (classical && !classical->height && !ect) return fail(EUCALC_E_ARG, "classical height is NULL");
     bool host_out = false;

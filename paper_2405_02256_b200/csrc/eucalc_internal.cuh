@@ -133,6 +133,7 @@ struct K2Args {
     int *cnt_c, *cnt_o;         // [batch*D] per-segment counts (warp regime)
     uint2 *slab;                // [batch*D][33] merged runs of lists <= sparse_max records, or NULL
     int sparse_max;             // lists of <= sparse_max (<= 32) records: register sort instead of histogram
+    bool sum16;                 // every list's sum |a|+|b| < 2^15: (wj, wc) prefix sums fit packed 16+16 bits
     // fused HT (NEXT f2): kbar table (fp64) over u in [ht_U0, ...), or NULL
     const double *ht_tab;
     int64_t ht_U0, L;

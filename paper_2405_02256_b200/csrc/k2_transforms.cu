@@ -130,10 +130,29 @@ struct Hist {
     __device__ __forceinline__ void add(int bin, int wc, int wj) const {
         const int w = SWZ ? swz(bin) : bin;
         if (PACK) {
-            if (wc | wj) atomicAdd(c + w, (unsigned)(wj * 65536 + wc));
+            // a kept record has Delta^-(eps) != 0 or Delta^-(-eps) != 0, so (wc, wj) != (0, 0)
+            atomicAdd(c + w, (unsigned)(wj * 65536 + wc));
         } else {
             if (wc) atomicAdd(c + w, (unsigned)wc);
             if (wj) atomicAdd(j + w, (unsigned)wj);
+        }
+    }
+    // PACK only: the raw packed words of bins b0..b0+3 (b0 % 4 == 0), optionally cleared
+    __device__ __forceinline__ void load4raw(int b0, unsigned (&u)[4], bool clear) const {
+        if constexpr (SWZ) {
+#pragma unroll
+            for (int s = 0; s < 4; ++s) {
+                const int w = swz(b0 + s);
+                u[s] = c[w];
+                if (clear) c[w] = 0;
+            }
+        } else {
+            const uint4 v = *reinterpret_cast<const uint4 *>(c + b0);
+            if (clear) *reinterpret_cast<uint4 *>(c + b0) = make_uint4(0, 0, 0, 0);
+            u[0] = v.x;
+            u[1] = v.y;
+            u[2] = v.z;
+            u[3] = v.w;
         }
     }
     // bins b0..b0+3 (b0 % 4 == 0), optionally cleared
@@ -222,12 +241,23 @@ __device__ __forceinline__ void warp_incl_scan3(int &x, int &y, int &z) {
 // Count the nonzero bins of one 128-bin group (lane <-> 4 consecutive bins).
 template <bool PACK, bool SWZ>
 __device__ __forceinline__ void count_group(const Hist<PACK, SWZ> &hs, int base, int &c, int &o, bool clear) {
-    int wc[4], wj[4];
-    hs.load4(base + 4 * (threadIdx.x & 31), wc, wj, clear);
+    if constexpr (PACK) {
+        // packed word u = wj * 2^16 + wc: wc != 0 <=> low half != 0; wj != 0 <=> u != sext16(u)
+        unsigned u[4];
+        hs.load4raw(base + 4 * (threadIdx.x & 31), u, clear);
 #pragma unroll
-    for (int s = 0; s < 4; ++s) {
-        c += wc[s] != 0;
-        o += wj[s] != 0;
+        for (int s = 0; s < 4; ++s) {
+            c += (u[s] & 0xffffu) != 0;
+            o += (int)u[s] != (int)(short)(u[s] & 0xffffu);
+        }
+    } else {
+        int wc[4], wj[4];
+        hs.load4(base + 4 * (threadIdx.x & 31), wc, wj, clear);
+#pragma unroll
+        for (int s = 0; s < 4; ++s) {
+            c += wc[s] != 0;
+            o += wj[s] != 0;
+        }
     }
 }
 
@@ -287,10 +317,82 @@ __device__ __forceinline__ void put_o(const OutPtrs<OutT> &o, int p, int h, int 
 // order: local sums per lane, one warp scan of (counts, sum Delta^-, sum J),
 // then up to 4 entries per stream per lane. Running values are warp-uniform;
 // positions are int32 (< 2^31 entries per call, host-checked).
+// Two inclusive warp scans at once (see warp_incl_scan3).
+__device__ __forceinline__ void warp_incl_scan2(int &x, int &y) {
+    const int lane = threadIdx.x & 31;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const int tx = __shfl_up_sync(0xffffffffu, x, d);
+        const int ty = __shfl_up_sync(0xffffffffu, y, d);
+        if (lane >= d) {
+            x += tx;
+            y += ty;
+        }
+    }
+}
+
+// emit_group for packed bins whose running sums fit 16 bits (every |E|, |Radon|
+// <= the list's sum |a|+|b| < 2^15, host-checked; always true for int16 outputs):
+// the running pair (E, Radon) is carried as ONE packed int P = Radon * 2^16 + E
+// (linear, exact in int32), so the warp scans two chains instead of three, and
+// E = sext16(P), Radon = (P + 2^15) >> 16. The kbar table values of the lane's
+// bins are loaded before the scan so their latency overlaps it.
+template <int MODE, typename OutT, bool SWZ>
+__device__ __forceinline__ void emit_group16(const OutPtrs<OutT> &o, const Hist<true, SWZ> &hs, int base, int h0,
+                                             int &e_run, int &r_run, int &pc, int &po, double &ht,
+                                             long long tab_off) {
+    const int lane = threadIdx.x & 31;
+    const bool do_ht = (MODE == kModeAny) ? (o.tab != nullptr) : ((MODE & kHt) != 0);
+    unsigned u[4];
+    hs.load4raw(base + 4 * lane, u, true);
+    const int hb = h0 + base + 4 * lane;
+    int wc[4], lc = 0, lo = 0, sum = 0;
+    bool nzc[4], nzo[4];
+#pragma unroll
+    for (int s = 0; s < 4; ++s) {
+        wc[s] = (int)(short)(u[s] & 0xffffu);
+        nzc[s] = wc[s] != 0;
+        nzo[s] = (int)u[s] != wc[s];
+        lc += nzc[s];
+        lo += nzo[s];
+        sum += (int)u[s];
+    }
+    double tv[4];
+    if (do_ht) {
+#pragma unroll
+        for (int s = 0; s < 4; ++s) tv[s] = nzo[s] ? __ldg(o.tab + 2 * (long long)(hb + s) + tab_off) : 0.0;
+    }
+    const int cnt = lc | (lo << 16);
+    int ic = cnt, isum = sum;
+    warp_incl_scan2(ic, isum);
+    const int ec = ic - cnt;
+    int p_c = pc + (ec & 0xffff), p_o = po + (ec >> 16);
+    const int prun = r_run * 65536 + e_run;
+    int P = prun + (isum - sum);
+#pragma unroll
+    for (int s = 0; s < 4; ++s) {
+        const int Pb = P;
+        P += (int)u[s];
+        if (nzc[s]) put_c<MODE>(o, p_c++, hb + s, (int)(short)(P & 0xffff), ((Pb + 0x8000) >> 16) + wc[s]);
+        if (nzo[s]) put_o<MODE>(o, p_o++, hb + s, (P + 0x8000) >> 16);
+        if (do_ht && nzo[s]) ht = fma((double)(((int)u[s] - wc[s]) >> 16), tv[s], ht);
+    }
+    const int tc = __shfl_sync(0xffffffffu, ic, 31);
+    pc += tc & 0xffff;
+    po += tc >> 16;
+    const int pend = prun + __shfl_sync(0xffffffffu, isum, 31);
+    e_run = (int)(short)(pend & 0xffff);
+    r_run = (pend + 0x8000) >> 16;
+}
+
 template <int MODE, typename OutT, bool PACK, bool SWZ>
 __device__ __forceinline__ void emit_group(const OutPtrs<OutT> &o, const Hist<PACK, SWZ> &hs, int base, int h0,
                                            int &e_run, int &r_run, int &pc, int &po, double &ht,
                                            long long tab_off) {
+    if constexpr (PACK && sizeof(OutT) == 2) {
+        emit_group16<MODE>(o, hs, base, h0, e_run, r_run, pc, po, ht, tab_off);
+        return;
+    }
     const int lane = threadIdx.x & 31;
     int wc[4], wj[4];
     hs.load4(base + 4 * lane, wc, wj, true);
@@ -367,7 +469,18 @@ __device__ __forceinline__ void fill_segment(const K2Args &a, const Hist<PACK> &
     const RecT *list = reinterpret_cast<const RecT *>(a.rec) + (b * a.Q + di.q) * a.vcap;
     const int n = a.count[b * a.Q + di.q];
     int lo = INT_MAX, hi = -1;
-    for (int i = lane; i < n; i += 32) {
+    int i = lane;
+    for (; i + 32 < n; i += 64) {  // two records in flight per lane
+        const RecT r0 = list[i], r1 = list[i + 32];
+        int bin0, wc0, wj0, bin1, wc1, wj1;
+        decode(r0, di, a, bin0, wc0, wj0);
+        decode(r1, di, a, bin1, wc1, wj1);
+        hs.add(bin0, wc0, wj0);
+        hs.add(bin1, wc1, wj1);
+        lo = min(lo, min(bin0, bin1));
+        hi = max(hi, max(bin0, bin1));
+    }
+    if (i < n) {
         int bin, wc, wj;
         decode(list[i], di, a, bin, wc, wj);
         hs.add(bin, wc, wj);
@@ -398,44 +511,53 @@ template <typename RecT>
 __device__ __forceinline__ SparseRuns sparse_runs(const K2Args &a, long long b, const DirInfo &di, int n) {
     const int lane = threadIdx.x & 31;
     const RecT *list = reinterpret_cast<const RecT *>(a.rec) + (b * a.Q + di.q) * a.vcap;
-    int h = INT_MAX, wc = 0, wj = 0;
+    int h = 0, wc = 0, wj = 0;
     if (lane < n) decode(list[lane], di, a, h, wc, wj);
+    // Sort the keys (bin << 5 | lane) — unique, so one shuffle and one min/max per
+    // network step; padding lanes hold keys above every record's. A list of
+    // <= 16 (8) records is sorted by the 16 (8)-lane network (the padding lanes
+    // above it are already in order).
+    int key = lane < n ? (h << 5) | lane : (0x7fffffe0 | lane);
+    const int kmax = n <= 8 ? 8 : n <= 16 ? 16 : 32;
 #pragma unroll
     for (int k = 2; k <= 32; k <<= 1) {
+        if (k > kmax) break;
 #pragma unroll
         for (int j = k >> 1; j > 0; j >>= 1) {
-            const int oh = __shfl_xor_sync(0xffffffffu, h, j);
-            const int oc = __shfl_xor_sync(0xffffffffu, wc, j);
-            const int oj = __shfl_xor_sync(0xffffffffu, wj, j);
-            const bool asc = (lane & k) == 0, lower = (lane & j) == 0;
-            if (lower == asc ? (oh < h) : (oh > h)) {
-                h = oh;
-                wc = oc;
-                wj = oj;
-            }
+            const int ok = __shfl_xor_sync(0xffffffffu, key, j);
+            const bool takemin = ((lane & j) == 0) == ((lane & k) == 0);
+            key = takemin ? min(key, ok) : max(key, ok);
         }
     }
+    const int src = key & 31;
+    const bool valid = key < 0x7fffffe0;
     SparseRuns r;
-    r.h = h;
-    r.pc = warp_incl_scan(wc);
-    r.pj = warp_incl_scan(wj);
-    const int hn = __shfl_down_sync(0xffffffffu, h, 1);
-    const int hp = __shfl_up_sync(0xffffffffu, h, 1);
-    const bool end = lane == 31 || hn != h;
-    const bool head = lane == 0 || hp != h;
-    int st = head ? lane : 0;
-#pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-        const int t = __shfl_up_sync(0xffffffffu, st, d);
-        if (lane >= d) st = max(st, t);
+    r.h = valid ? key >> 5 : INT_MAX;
+    if (a.sum16) {
+        // one scan of the packed pair (|prefix sums| <= list sum |a|+|b| < 2^15)
+        const int w = __shfl_sync(0xffffffffu, wj * 65536 + wc, src);
+        const int pw = warp_incl_scan(valid ? w : 0);
+        r.pc = (int)(short)(pw & 0xffff);
+        r.pj = (pw + 0x8000) >> 16;
+    } else {
+        wc = __shfl_sync(0xffffffffu, wc, src);
+        wj = __shfl_sync(0xffffffffu, wj, src);
+        r.pc = warp_incl_scan(valid ? wc : 0);
+        r.pj = warp_incl_scan(valid ? wj : 0);
     }
-    const int src = st > 0 ? st - 1 : 0;
-    const int bc = __shfl_sync(0xffffffffu, r.pc, src), bj = __shfl_sync(0xffffffffu, r.pj, src);
+    const int hn = __shfl_down_sync(0xffffffffu, r.h, 1);
+    const int hp = __shfl_up_sync(0xffffffffu, r.h, 1);
+    const bool end = lane == 31 || hn != r.h;
+    const bool head = lane == 0 || hp != r.h;
+    // run start: the highest head lane <= this lane
+    const unsigned heads = __ballot_sync(0xffffffffu, head);
+    const int st = 31 - __clz(heads & (0xffffffffu >> (31 - lane)));
+    const int bsrc = st > 0 ? st - 1 : 0;
+    const int bc = __shfl_sync(0xffffffffu, r.pc, bsrc), bj = __shfl_sync(0xffffffffu, r.pj, bsrc);
     r.run_c = r.pc - (st > 0 ? bc : 0);
     r.run_j = r.pj - (st > 0 ? bj : 0);
-    const bool valid = end && h != INT_MAX;
-    r.emit_c = valid && r.run_c != 0;
-    r.emit_o = valid && r.run_j != 0;
+    r.emit_c = end && valid && r.run_c != 0;
+    r.emit_o = end && valid && r.run_j != 0;
     return r;
 }
 
@@ -456,10 +578,17 @@ template <typename RecT, bool PACK>
 __global__ void __launch_bounds__(kWarpThreads) k2w_count(K2Args a, int rcap, int *cnt_c, int *cnt_o) {
     extern __shared__ __align__(16) unsigned hist_all[];
     const Hist<PACK> hs = warp_hist<PACK>(hist_all, rcap);
-    const long long S = a.batch * a.D;
-    const long long nw = (long long)gridDim.x * (blockDim.x >> 5);
-    for (long long s = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); s < S; s += nw) {
-        const long long b = s / a.D, d = s % a.D;
+    // segment indices are int32 (< 2^31 segments per call, host-checked): no 64-bit division
+    const int S = (int)(a.batch * a.D), D = (int)a.D;
+    const int nw = gridDim.x * (blockDim.x >> 5);
+    const int s0 = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    const int nb = nw / D, nd = nw - nb * D;  // (image, direction) advance per step
+    int b = s0 / D, d = s0 - b * D;
+    for (int s = s0; s < S; s += nw, b += nb, d += nd) {
+        if (d >= D) {
+            d -= D;
+            ++b;
+        }
         const DirInfo di = a.dirs[d];
         const int n = a.count[b * a.Q + di.q];
         int c = 0, o = 0;
@@ -472,7 +601,7 @@ __global__ void __launch_bounds__(kWarpThreads) k2w_count(K2Args a, int rcap, in
                 // keep the merged runs for k2w_emit (16-bit fields, host-checked):
                 // bin | E << 16, E_c | E' << 16; the emission masks in slot 32
                 const int ec = r.pj - r.run_j + r.run_c;
-                uint2 *sl = a.slab + s * 33;
+                uint2 *sl = a.slab + (long long)s * 33;
                 sl[threadIdx.x & 31] = make_uint2((unsigned)(r.h & 0xffff) | ((unsigned)r.pc << 16),
                                                   (unsigned)(ec & 0xffff) | ((unsigned)r.pj << 16));
                 if ((threadIdx.x & 31) == 0) sl[32] = make_uint2(mc, mo);
@@ -508,8 +637,14 @@ __global__ void __launch_bounds__(kWarpThreads) k2w_emit(K2Args a, int rcap) {
     const int64_t *off_c = a.do_ect ? a.ect.off : a.cls.off;
     const bool any_c = a.do_ect || a.do_cls;
     const int nw = gridDim.x * (blockDim.x >> 5);
-    for (int s = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); s < S; s += nw) {
-        const int b = s / D, d = s - b * D;
+    const int s0 = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    const int nb = nw / D, nd = nw - nb * D;  // (image, direction) advance per step
+    int b = s0 / D, d = s0 - b * D;
+    for (int s = s0; s < S; s += nw, b += nb, d += nd) {
+        if (d >= D) {
+            d -= D;
+            ++b;
+        }
         const DirInfo di = a.dirs[d];
         const int n = a.count[b * a.Q + di.q];
         int pc = any_c ? (int)off_c[s] : 0, po = a.do_ord ? (int)a.ord.off[s] : 0;

@@ -324,6 +324,54 @@ def test_config2_full_size_sampled():
     check_fused_ht(imgs, dirs, "vertex", cr, "sin", 1.0, "f64", pairs=pairs[:40], elem_bytes=4)
 
 
+def _squares_image(m, k, rng, value=255):
+    img = np.zeros((m, m), np.uint8)
+    for _ in range(k):
+        y, x = rng.integers(1, m - 4, 2)
+        img[y:y + 3, x:x + 3] = value
+    return img
+
+
+@pytest.mark.parametrize("with_gray", [False, True])
+def test_sparse_lists_register_sort(with_gray):
+    """K2's register sort path (lists of <= 32 records: 8-, 16- and 32-lane
+    networks) next to histogram segments, with the packed 16+16 prefix sums
+    (every list's sum |a|+|b| < 2^15) and without (a uniform gray image in the
+    batch lifts the bound)."""
+    rng = np.random.default_rng(77)
+    imgs = [_squares_image(40, k, rng) for k in (0, 1, 2, 3, 5, 8, 12, 30)]
+    if with_gray:
+        imgs.append(rng.integers(0, 256, (40, 40)).astype(np.uint8))
+    imgs = np.stack(imgs)
+    dirs = synth.random_directions(48, 2, 16, 78)
+    cx, cr, res = run_gpu(imgs, dirs, "vertex")
+    L = cr.list_lengths()
+    assert (L <= 8).any() and ((L > 8) & (L <= 16)).any() and ((L > 16) & (L <= 32)).any() and (L > 32).any(), L
+    check_transforms(imgs, dirs, "vertex", res)
+    check_fused_ht(imgs, dirs, "vertex", cr, "gauss", 1.0, "f64", elem_bytes=8)
+
+
+def test_config2_binary_full_size_bench_launch():
+    """Full config-2 binary batch in bench.py's launch (narrowest width, shared
+    heights, fused HT): sampled segments vs the oracle."""
+    c = synth.config_inputs(2, "binary")
+    imgs, dirs = c["images"], c["dirs"]
+    cx = eu.build_complex(imgs, "vertex")
+    cr = eu.critical_points(cx)
+    r = eu.transforms(cr, dirs, elem_bytes="auto", share_heights=True, ht=("sin", 1.0, "f64"))
+    torch.cuda.synchronize()
+    assert r["ect"]["value"].element_size() == 2
+    ht = r.pop("ht").cpu().numpy()
+    res = {k: to_np(v) for k, v in r.items()}
+    rng = np.random.default_rng(5)
+    pairs = [(int(b), int(d)) for b, d in zip(rng.integers(0, 1024, 300), rng.integers(0, 256, 300))]
+    pairs += [(0, 0), (1023, 255)]
+    check_transforms(imgs, dirs, "vertex", res, pairs=pairs)
+    ref = oracle.ht_batch(imgs, dirs, "vertex", "sin", 1.0, pairs=pairs[:60])
+    for (b, d), want in ref.items():
+        assert abs(float(ht[b, d]) - want) <= 1e-9 * max(abs(want), 1.0), (b, d)
+
+
 def test_config3_sampled():
     c = synth.config_inputs(3)
     img, dirs = c["images"], c["dirs"][:64]
