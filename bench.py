@@ -75,6 +75,8 @@ class Clocks:
         q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
              "clocks_event_reasons.sw_power_cap")
+        if os.environ.get("BENCH_NO_CLOCKS") == "1":  # diagnostics: measure without the sampler
+            return self
         try:
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={q}",
                                           "--format=csv,noheader,nounits", "-lms", "25"],
@@ -295,6 +297,8 @@ def gpu_arm(args):
             "data": "synthetic (seeded generators, synth/; config-2 recipe of SURVEY.md 8(d))",
             "config": arm_config(world),
             "stages_ms_per_step": {k: v / args.steps for k, v in stage_ms.items()},
+            "step_ms_spread": {"min": float(np.min(times)), "median": float(np.median(times)),
+                               "max": float(np.max(times))},
             "roofline": {"bound": "hbm", "kernel": "k2_transforms (k2w_count+k2_scan+k2w_emit, fused HT; gray and "
                                                   "binary launches concurrent, bytes and span of both)",
                          "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,

@@ -193,6 +193,23 @@ struct DirPlan {
     uint64_t id = 0;         // unique per plan (bound cache key)
 };
 
+// Max number of vertices on one lattice height level {p : sum xs_k p_k = h}:
+// along two axes j, k the solutions step by (xs_k, -xs_j) / gcd, so a line holds
+// at most min((M_j-1) / |xs_k/g|, (M_k-1) / |xs_j/g|) + 1 points; in 3-D a level
+// set is at most (extent of the third axis) lines. Bounds every histogram bin's
+// record count (K2's packed-bin test per direction).
+int64_t level_points(const Complex *cx, const DirInfo &di) {
+    const int n = cx->ndim;
+    auto line2 = [&](int j, int k) -> int64_t {
+        const int64_t a = std::llabs((int64_t)di.xs[j]), b = std::llabs((int64_t)di.xs[k]);
+        if (a == 0 || b == 0) return int64_t(1);  // an extent-1 axis (scale 0): one point per height
+        const int64_t g = std::gcd(a, b);
+        return std::min((cx->M[j] - 1) / (b / g), (cx->M[k] - 1) / (a / g)) + 1;
+    };
+    if (n == 2) return line2(0, 1);
+    return std::min({cx->M[0] * line2(1, 2), cx->M[1] * line2(0, 2), cx->M[2] * line2(0, 1)});
+}
+
 eucalc_status plan_dirs(const Complex *cx, const int32_t *dirs, int64_t D, cudaStream_t st, DirPlan &p) {
     if (D < 0) return fail(EUCALC_E_ARG, "D < 0");
     if (D > 0 && !dirs) return fail(EUCALC_E_ARG, "dirs is NULL");
@@ -250,6 +267,7 @@ eucalc_status plan_dirs(const Complex *cx, const int32_t *dirs, int64_t D, cudaS
             x8 |= (uint32_t)(di.xs[k] & 0xff) << (8 * (n - 1 - k));
         }
         p.info[d].xs8 = (int)x8;
+        p.info[d].line = (int)std::min<int64_t>(level_points(cx, p.info[d]), INT32_MAX);
         if (d == 0) p.dp = cx->aligned;
         if (!fits8) p.dp = 0;
     }
@@ -1092,6 +1110,8 @@ eucalc_status transforms_impl(const eucalc_critical *ccr, const int32_t *dirs, i
         a.slab = slab;
         a.sparse_max = sparse_max;
         a.sum16 = cr->max_abs_sum < 32768;
+        a.max_rec = cr->max_rec;
+        a.max_abs_sum = cr->max_abs_sum;
         ProfScope ps("k2_transforms", st);
         e = launch_k2(a, st, num_sms());
     }

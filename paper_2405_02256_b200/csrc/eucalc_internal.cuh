@@ -100,6 +100,7 @@ struct DirInfo {
     int q;          // antipodal pair of the orthant
     int swap;       // 1 if the orthant is the pair's non-representative
     int xs8;        // xs as packed int8 (byte j <-> axis n-1-j) when every |xs_i| <= 127
+    int line;       // max vertices on one lattice height level (bounds every bin's record count)
 };
 
 struct StepsOut {
@@ -134,6 +135,7 @@ struct K2Args {
     uint2 *slab;                // [batch*D][33] merged runs of lists <= sparse_max records, or NULL
     int sparse_max;             // lists of <= sparse_max (<= 32) records: register sort instead of histogram
     bool sum16;                 // every list's sum |a|+|b| < 2^15: (wj, wc) prefix sums fit packed 16+16 bits
+    int64_t max_rec, max_abs_sum;  // K1 statistics: max |a|+|b| of a record, max list sum of |a|+|b|
     // fused HT (NEXT f2): kbar table (fp64) over u in [ht_U0, ...), or NULL
     const double *ht_tab;
     int64_t ht_U0, L;

@@ -850,139 +850,157 @@ __device__ void fill_window(const K2Args &a, const RecT *list, const int32_t *to
     }
 }
 
-template <typename RecT, typename OutT, bool PACK>
-__global__ void __launch_bounds__(kBlockThreads, 1) k2_block(K2Args a, long long nseg, int win) {
-    extern __shared__ __align__(16) unsigned hist[];
-    __shared__ long long s_seg;
-    __shared__ int s_wsum[kBlockWarps][4];  // per-warp (nc, no, sum wc, sum wj)
-    __shared__ long long s_exc[2];
-    __shared__ double s_ht[kBlockWarps];
-    __shared__ int s_hit[kMaxHitTiles];
-    __shared__ int s_nhit;
+struct BlockShared {
+    long long seg;
+    int wsum[kBlockWarps][4];  // per-warp (nc, no, sum wc, sum wj)
+    long long exc[2];
+    double ht[kBlockWarps];
+    int hit[kMaxHitTiles];
+    int nhit;
+};
+
+// One segment (image b, direction d) of the block regime with histogram bins of
+// kind PACK over windows of `win` bins (`hist` holds win words per array).
+template <bool PACK, typename RecT, typename OutT>
+__device__ __forceinline__ void block_segment(const K2Args &a, const OutPtrs<OutT> &outp, unsigned *hist, int win,
+                                              long long s, long long b, long long d, BlockShared &sh) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    constexpr int words = PACK ? 1 : 2;
-    const OutPtrs<OutT> outp(a);
     Hist<PACK, true> hs;
     hs.c = hist;
     hs.j = hist + win;
-    for (int i = threadIdx.x; i < win * words; i += kBlockThreads) hist[i] = 0;
     const RecT *recs = reinterpret_cast<const RecT *>(a.rec);
+    const DirInfo di = a.dirs[d];
+    const RecT *list = recs + (b * a.Q + di.q) * a.vcap;
+    const int32_t *toff = a.tile_off + (b * a.Q + di.q) * (long long)(a.ntiles + 1);
+    const int n = a.count[b * a.Q + di.q];
+    const int nwin = (di.R + win - 1) / win;
+    const bool cull = nwin > 1 && a.ntiles > 1;
+    // each warp owns a contiguous, 128-aligned range of the window
+    const int per = ((win / kBlockWarps) + kGroup - 1) / kGroup * kGroup;
+    // phase A: counts over all windows
+    long long nc = 0, no = 0;
+    for (int w = 0; w < nwin; ++w) {
+        const int lo = w * win, wb = min(win, di.R - lo);
+        fill_window(a, list, toff, n, di, lo, wb, cull, hs, sh.hit, &sh.nhit);
+        __syncthreads();
+        int c = 0, o = 0;
+        const int b0 = min(wb, warp * per), b1 = min(wb, b0 + per);
+        for (int base = b0; base < b1; base += kGroup) count_group(hs, base, c, o, nwin > 1);
+        c = warp_sum(c);
+        o = warp_sum(o);
+        if (lane == 0) {
+            sh.wsum[warp][0] = c;
+            sh.wsum[warp][1] = o;
+        }
+        __syncthreads();
+        for (int k = 0; k < kBlockWarps; ++k) {
+            nc += sh.wsum[k][0];
+            no += sh.wsum[k][1];
+        }
+        __syncthreads();
+    }
+    if (warp == 0) {
+        long long ec, eo;
+        seg_lookback(a.flags, s, nc, no, ec, eo);
+        if (lane == 0) {
+            sh.exc[0] = ec;
+            sh.exc[1] = eo;
+            write_offsets(a, s, ec, eo, nc, no);
+        }
+    }
+    __syncthreads();
+    // phase B: emit window by window
+    long long pc_carry = sh.exc[0], po_carry = sh.exc[1];
+    int e_carry = 0, r_carry = 0;
+    double ht = 0.0;
+    const long long ht_off = outp.tab ? ht_tab_off(a, d) : 0;
+    for (int w = 0; w < nwin; ++w) {
+        const int lo = w * win, wb = min(win, di.R - lo);
+        if (nwin > 1) {
+            fill_window(a, list, toff, n, di, lo, wb, cull, hs, sh.hit, &sh.nhit);
+            __syncthreads();
+        }
+        const int b0 = min(wb, warp * per), b1 = min(wb, b0 + per);
+        int c = 0, o = 0, sc = 0, sj = 0;
+        for (int base = b0; base < b1; base += kGroup) {
+            int wc[4], wj[4];
+            hs.load4(base + 4 * lane, wc, wj, false);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                c += wc[q] != 0;
+                o += wj[q] != 0;
+                sc += wc[q];
+                sj += wj[q];
+            }
+        }
+        c = warp_sum(c);
+        o = warp_sum(o);
+        sc = warp_sum(sc);
+        sj = warp_sum(sj);
+        if (lane == 0) {
+            sh.wsum[warp][0] = c;
+            sh.wsum[warp][1] = o;
+            sh.wsum[warp][2] = sc;
+            sh.wsum[warp][3] = sj;
+        }
+        __syncthreads();
+        int pc = (int)pc_carry, po = (int)po_carry;
+        int er = e_carry, rr = r_carry;
+        long long tc = 0, to = 0;
+        int tsc = 0, tsj = 0;
+        for (int k = 0; k < kBlockWarps; ++k) {
+            if (k < warp) {
+                pc += sh.wsum[k][0];
+                po += sh.wsum[k][1];
+                er += sh.wsum[k][2];
+                rr += sh.wsum[k][3];
+            }
+            tc += sh.wsum[k][0];
+            to += sh.wsum[k][1];
+            tsc += sh.wsum[k][2];
+            tsj += sh.wsum[k][3];
+        }
+        for (int base = b0; base < b1; base += kGroup)
+            emit_group<kModeAny>(outp, hs, base, di.hlo + lo, er, rr, pc, po, ht, ht_off);
+        pc_carry += tc;
+        po_carry += to;
+        e_carry += tsc;
+        r_carry += tsj;
+        __syncthreads();
+    }
+    if (outp.tab) {  // fused HT: warp partials, then a fixed-order sum over warps
+        for (int k = 16; k; k >>= 1) ht += __shfl_xor_sync(0xffffffffu, ht, k);
+        if (lane == 0) sh.ht[warp] = ht;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            double t = 0.0;
+            for (int k = 0; k < kBlockWarps; ++k) t += sh.ht[k];
+            ht_write(a, s, t);
+        }
+    }
+}
+
+// Block regime. A segment uses packed 16+16 bins (one atomic per record, windows
+// of 2*win bins) when its bins provably stay below 2^15: every bin holds at most
+// di.line records (the vertices of one height level) of |a|+|b| <= max_rec, and
+// no more than the list's sum |a|+|b|; else split bins (two int32 arrays, windows
+// of win bins). `hist` is cleared on entry and left cleared by every segment.
+template <typename RecT, typename OutT>
+__global__ void __launch_bounds__(kBlockThreads, 1) k2_block(K2Args a, long long nseg, int win) {
+    extern __shared__ __align__(16) unsigned hist[];
+    __shared__ BlockShared sh;
+    const OutPtrs<OutT> outp(a);
+    for (int i = threadIdx.x; i < 2 * win; i += kBlockThreads) hist[i] = 0;
     while (true) {
         __syncthreads();
-        if (threadIdx.x == 0) s_seg = (long long)atomicAdd(a.ticket, 1u);
+        if (threadIdx.x == 0) sh.seg = (long long)atomicAdd(a.ticket, 1u);
         __syncthreads();
-        const long long s = s_seg;
+        const long long s = sh.seg;
         if (s >= nseg) break;
         const long long b = s / a.D, d = s % a.D;
-        const DirInfo di = a.dirs[d];
-        const RecT *list = recs + (b * a.Q + di.q) * a.vcap;
-        const int32_t *toff = a.tile_off + (b * a.Q + di.q) * (long long)(a.ntiles + 1);
-        const int n = a.count[b * a.Q + di.q];
-        const int nwin = (di.R + win - 1) / win;
-        const bool cull = nwin > 1 && a.ntiles > 1;
-        // each warp owns a contiguous, 128-aligned range of the window
-        const int per = ((win / kBlockWarps) + kGroup - 1) / kGroup * kGroup;
-        // phase A: counts over all windows
-        long long nc = 0, no = 0;
-        for (int w = 0; w < nwin; ++w) {
-            const int lo = w * win, wb = min(win, di.R - lo);
-            fill_window(a, list, toff, n, di, lo, wb, cull, hs, s_hit, &s_nhit);
-            __syncthreads();
-            int c = 0, o = 0;
-            const int b0 = min(wb, warp * per), b1 = min(wb, b0 + per);
-            for (int base = b0; base < b1; base += kGroup) count_group(hs, base, c, o, nwin > 1);
-            c = warp_sum(c);
-            o = warp_sum(o);
-            if (lane == 0) {
-                s_wsum[warp][0] = c;
-                s_wsum[warp][1] = o;
-            }
-            __syncthreads();
-            for (int k = 0; k < kBlockWarps; ++k) {
-                nc += s_wsum[k][0];
-                no += s_wsum[k][1];
-            }
-            __syncthreads();
-        }
-        if (warp == 0) {
-            long long ec, eo;
-            seg_lookback(a.flags, s, nc, no, ec, eo);
-            if (lane == 0) {
-                s_exc[0] = ec;
-                s_exc[1] = eo;
-                write_offsets(a, s, ec, eo, nc, no);
-            }
-        }
-        __syncthreads();
-        // phase B: emit window by window
-        long long pc_carry = s_exc[0], po_carry = s_exc[1];
-        int e_carry = 0, r_carry = 0;
-        double ht = 0.0;
-        const long long ht_off = outp.tab ? ht_tab_off(a, d) : 0;
-        for (int w = 0; w < nwin; ++w) {
-            const int lo = w * win, wb = min(win, di.R - lo);
-            if (nwin > 1) {
-                fill_window(a, list, toff, n, di, lo, wb, cull, hs, s_hit, &s_nhit);
-                __syncthreads();
-            }
-            const int b0 = min(wb, warp * per), b1 = min(wb, b0 + per);
-            int c = 0, o = 0, sc = 0, sj = 0;
-            for (int base = b0; base < b1; base += kGroup) {
-                int wc[4], wj[4];
-                hs.load4(base + 4 * lane, wc, wj, false);
-#pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                    c += wc[q] != 0;
-                    o += wj[q] != 0;
-                    sc += wc[q];
-                    sj += wj[q];
-                }
-            }
-            c = warp_sum(c);
-            o = warp_sum(o);
-            sc = warp_sum(sc);
-            sj = warp_sum(sj);
-            if (lane == 0) {
-                s_wsum[warp][0] = c;
-                s_wsum[warp][1] = o;
-                s_wsum[warp][2] = sc;
-                s_wsum[warp][3] = sj;
-            }
-            __syncthreads();
-            int pc = (int)pc_carry, po = (int)po_carry;
-            int er = e_carry, rr = r_carry;
-            long long tc = 0, to = 0;
-            int tsc = 0, tsj = 0;
-            for (int k = 0; k < kBlockWarps; ++k) {
-                if (k < warp) {
-                    pc += s_wsum[k][0];
-                    po += s_wsum[k][1];
-                    er += s_wsum[k][2];
-                    rr += s_wsum[k][3];
-                }
-                tc += s_wsum[k][0];
-                to += s_wsum[k][1];
-                tsc += s_wsum[k][2];
-                tsj += s_wsum[k][3];
-            }
-            for (int base = b0; base < b1; base += kGroup)
-                emit_group<kModeAny>(outp, hs, base, di.hlo + lo, er, rr, pc, po, ht, ht_off);
-            pc_carry += tc;
-            po_carry += to;
-            e_carry += tsc;
-            r_carry += tsj;
-            __syncthreads();
-        }
-        if (outp.tab) {  // fused HT: warp partials, then a fixed-order sum over warps
-            for (int k = 16; k; k >>= 1) ht += __shfl_xor_sync(0xffffffffu, ht, k);
-            if (lane == 0) s_ht[warp] = ht;
-            __syncthreads();
-            if (threadIdx.x == 0) {
-                double t = 0.0;
-                for (int k = 0; k < kBlockWarps; ++k) t += s_ht[k];
-                ht_write(a, s, t);
-            }
-        }
+        const long long bin_bound = min((long long)a.dirs[d].line * (long long)a.max_rec, (long long)a.max_abs_sum);
+        if (bin_bound < 32768) block_segment<true, RecT, OutT>(a, outp, hist, 2 * win, s, b, d, sh);
+        else block_segment<false, RecT, OutT>(a, outp, hist, win, s, b, d, sh);
     }
 }
 
@@ -1027,8 +1045,8 @@ cudaError_t launch_t(const K2Args &a, cudaStream_t s, int num_sms) {
         count_launch(3);
         return cudaGetLastError();
     }
-    const int win = (int)(kBlockSmem / (4 * words)) / kGroup * kGroup;
-    auto kern = k2_block<RecT, OutT, PACK>;
+    const int win = (int)(kBlockSmem / 8) / kGroup * kGroup;  // split bins; packed segments use 2 * win
+    auto kern = k2_block<RecT, OutT>;
     cudaError_t e = prepare_kernel((const void *)kern, kBlockThreads, kBlockSmem, nullptr);
     if (e != cudaSuccess) return e;
     long long grid = std::min<long long>(nseg, num_sms);
