@@ -1112,6 +1112,13 @@ eucalc_status transforms_impl(const eucalc_critical *ccr, const int32_t *dirs, i
         a.sum16 = cr->max_abs_sum < 32768;
         a.max_rec = cr->max_rec;
         a.max_abs_sum = cr->max_abs_sum;
+        int64_t scap = 0;
+        const size_t sbytes = k2_stage_bytes(a, num_sms(), &scap);
+        if (sbytes) {
+            a.stage = dalloc(sbytes);
+            a.stage_cap = a.stage ? scap : 0;
+            if (!a.stage) cudaGetLastError();  // no staging: the block regime fills twice
+        }
         ProfScope ps("k2_transforms", st);
         e = launch_k2(a, st, num_sms());
     }

@@ -136,6 +136,8 @@ struct K2Args {
     int sparse_max;             // lists of <= sparse_max (<= 32) records: register sort instead of histogram
     bool sum16;                 // every list's sum |a|+|b| < 2^15: (wj, wc) prefix sums fit packed 16+16 bits
     int64_t max_rec, max_abs_sum;  // K1 statistics: max |a|+|b| of a record, max list sum of |a|+|b|
+    void *stage;                // block regime: per-CTA output staging (k2_stage_bytes), or NULL
+    int64_t stage_cap;          // entries per staged array per CTA
     // fused HT (NEXT f2): kbar table (fp64) over u in [ht_U0, ...), or NULL
     const double *ht_tab;
     int64_t ht_U0, L;
@@ -145,6 +147,9 @@ struct K2Args {
     void *ht_out;               // [batch][D]
 };
 cudaError_t launch_k2(const K2Args &a, cudaStream_t s, int num_sms);
+// Block regime only: bytes of per-CTA output staging that let each segment fill
+// its histogram once (0 = warp regime, or staging too large: two fills).
+size_t k2_stage_bytes(const K2Args &a, int num_sms, int64_t *cap);
 
 struct K3Args {
     const void *rec;

@@ -87,15 +87,19 @@ __device__ void seg_lookback(unsigned long long *flags, long long s, long long n
     exc_o = eo;
 }
 
-template <typename RecT>
+// Height bin and weights of a record for direction di. DP = 2 / 3: coordinates
+// are byte-aligned fields, the height is one dp2a / dp4a; DP = 0: shifts and
+// masks; DP = -1: a.dp chosen at run time.
+template <int DP = -1, typename RecT>
 __device__ __forceinline__ void decode(const RecT &r, const DirInfo &di, const K2Args &a, int &bin, int &wc,
                                        int &wj) {
     int h = 0;
-    if (a.dp == 2) {
+    const int dp = DP >= 0 ? DP : a.dp;
+    if (dp == 2) {
         // h = sum of 16-bit unsigned coordinate halves x signed int8 direction bytes
         asm("dp2a.lo.u32.s32 %0, %1, %2, %3;" : "=r"(h) : "r"(r.c), "r"(di.xs8), "r"(-di.hlo));
         bin = h;
-    } else if (a.dp == 3) {
+    } else if (dp == 3) {
         asm("dp4a.u32.s32 %0, %1, %2, %3;" : "=r"(h) : "r"(r.c), "r"(di.xs8), "r"(-di.hlo));
         bin = h;
     } else {
@@ -750,9 +754,11 @@ constexpr size_t kBlockSmem = 200 * 1024;
 // Accumulate the records list[beg, end) whose bin lies in [lo, lo + wbins):
 // the warp's lanes stride the range, four records in flight per lane (the list
 // streams from L2; a lone load per lane leaves the SM latency-bound).
-template <int U, typename RecT, bool PACK, bool SWZ>  // U: records in flight per thread
-__device__ __forceinline__ void fill_range(const K2Args &a, const RecT *list, int beg, int end, const DirInfo &di,
-                                           int lo, int wbins, const Hist<PACK, SWZ> &hs, int lane, int step) {
+// U: records in flight per thread; DP as decode; CHECK: skip records outside
+// the window (false when the window covers the whole height range).
+template <int U, int DP, bool CHECK, typename RecT, bool PACK, bool SWZ>
+__device__ __forceinline__ void fill_range_t(const K2Args &a, const RecT *list, int beg, int end, const DirInfo &di,
+                                             int lo, int wbins, const Hist<PACK, SWZ> &hs, int lane, int step) {
     int i = beg + lane;
     for (; i + (U - 1) * step < end; i += U * step) {
         RecT r[U];
@@ -761,17 +767,24 @@ __device__ __forceinline__ void fill_range(const K2Args &a, const RecT *list, in
 #pragma unroll
         for (int u = 0; u < U; ++u) {
             int bin, wc, wj;
-            decode(r[u], di, a, bin, wc, wj);
+            decode<DP>(r[u], di, a, bin, wc, wj);
             bin -= lo;
-            if ((unsigned)bin < (unsigned)wbins) hs.add(bin, wc, wj);
+            if (!CHECK || (unsigned)bin < (unsigned)wbins) hs.add(bin, wc, wj);
         }
     }
     for (; i < end; i += step) {
         int bin, wc, wj;
-        decode(list[i], di, a, bin, wc, wj);
+        decode<DP>(list[i], di, a, bin, wc, wj);
         bin -= lo;
-        if ((unsigned)bin < (unsigned)wbins) hs.add(bin, wc, wj);
+        if (!CHECK || (unsigned)bin < (unsigned)wbins) hs.add(bin, wc, wj);
     }
+}
+
+template <int U, int DP, typename RecT, bool PACK, bool SWZ>
+__device__ __forceinline__ void fill_range(const K2Args &a, const RecT *list, int beg, int end, const DirInfo &di,
+                                           int lo, int wbins, const Hist<PACK, SWZ> &hs, int lane, int step) {
+    if (lo == 0 && wbins >= di.R) fill_range_t<U, DP, false>(a, list, beg, end, di, lo, wbins, hs, lane, step);
+    else fill_range_t<U, DP, true>(a, list, beg, end, di, lo, wbins, hs, lane, step);
 }
 
 // Height range (bins relative to hlo) of K1 tile t: a TZ x TY x TX box of
@@ -807,12 +820,12 @@ __device__ __forceinline__ void tile_bins(const K2Args &a, const DirInfo &di, in
 // of once per window.
 constexpr int kMaxHitTiles = 4096;  // culled-tile list in shared memory
 
-template <typename RecT, bool PACK, bool SWZ>
+template <int DP, typename RecT, bool PACK, bool SWZ>
 __device__ void fill_window(const K2Args &a, const RecT *list, const int32_t *toff, int n, const DirInfo &di,
                             int lo, int wbins, bool cull, const Hist<PACK, SWZ> &hs, int *s_hit, int *s_nhit) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     if (!cull) {
-        fill_range<8>(a, list, 0, n, di, lo, wbins, hs, threadIdx.x, kBlockThreads);
+        fill_range<8, DP>(a, list, 0, n, di, lo, wbins, hs, threadIdx.x, kBlockThreads);
         return;
     }
     if (a.ntiles <= kMaxHitTiles) {
@@ -829,7 +842,7 @@ __device__ void fill_window(const K2Args &a, const RecT *list, const int32_t *to
         const int nhit = *s_nhit;
         for (int k = warp; k < nhit; k += kBlockWarps) {
             const int tt = s_hit[k];
-            fill_range<4>(a, list, toff[tt], toff[tt + 1], di, lo, wbins, hs, lane, 32);
+            fill_range<4, DP>(a, list, toff[tt], toff[tt + 1], di, lo, wbins, hs, lane, 32);
         }
         return;
     }
@@ -845,7 +858,7 @@ __device__ void fill_window(const K2Args &a, const RecT *list, const int32_t *to
         while (m) {
             const int tt = t0 + __ffs(m) - 1;
             m &= m - 1;
-            fill_range<4>(a, list, toff[tt], toff[tt + 1], di, lo, wbins, hs, lane, 32);
+            fill_range<4, DP>(a, list, toff[tt], toff[tt + 1], di, lo, wbins, hs, lane, 32);
         }
     }
 }
@@ -861,7 +874,7 @@ struct BlockShared {
 
 // One segment (image b, direction d) of the block regime with histogram bins of
 // kind PACK over windows of `win` bins (`hist` holds win words per array).
-template <bool PACK, typename RecT, typename OutT>
+template <bool PACK, int DP, typename RecT, typename OutT>
 __device__ __forceinline__ void block_segment(const K2Args &a, const OutPtrs<OutT> &outp, unsigned *hist, int win,
                                               long long s, long long b, long long d, BlockShared &sh) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -877,11 +890,114 @@ __device__ __forceinline__ void block_segment(const K2Args &a, const OutPtrs<Out
     const bool cull = nwin > 1 && a.ntiles > 1;
     // each warp owns a contiguous, 128-aligned range of the window
     const int per = ((win / kBlockWarps) + kGroup - 1) / kGroup * kGroup;
+    if (a.stage && nwin > 1) {
+        // ONE fill per window: the window's entries go to this CTA's staging at
+        // segment-local positions; after the look-back they are copied to the CSR.
+        OutPtrs<OutT> scr = outp;
+        OutT *base = reinterpret_cast<OutT *>(a.stage) + (long long)blockIdx.x * 6 * a.stage_cap;
+        scr.eh = base;
+        scr.ev = base + a.stage_cap;
+        scr.cv = base + 2 * a.stage_cap;
+        scr.ch = base + 3 * a.stage_cap;
+        scr.oh = base + 4 * a.stage_cap;
+        scr.ov = base + 5 * a.stage_cap;
+        int pc_carry = 0, po_carry = 0, e_carry = 0, r_carry = 0;
+        double ht = 0.0;
+        const long long ht_off = outp.tab ? ht_tab_off(a, d) : 0;
+        for (int w = 0; w < nwin; ++w) {
+            const int lo = w * win, wb = min(win, di.R - lo);
+            fill_window<DP>(a, list, toff, n, di, lo, wb, cull, hs, sh.hit, &sh.nhit);
+            __syncthreads();
+            const int b0 = min(wb, warp * per), b1 = min(wb, b0 + per);
+            int c = 0, o = 0, sc = 0, sj = 0;
+            for (int base = b0; base < b1; base += kGroup) {
+                int wc[4], wj[4];
+                hs.load4(base + 4 * lane, wc, wj, false);
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    c += wc[q] != 0;
+                    o += wj[q] != 0;
+                    sc += wc[q];
+                    sj += wj[q];
+                }
+            }
+            c = warp_sum(c);
+            o = warp_sum(o);
+            sc = warp_sum(sc);
+            sj = warp_sum(sj);
+            if (lane == 0) {
+                sh.wsum[warp][0] = c;
+                sh.wsum[warp][1] = o;
+                sh.wsum[warp][2] = sc;
+                sh.wsum[warp][3] = sj;
+            }
+            __syncthreads();
+            int pc = pc_carry, po = po_carry, er = e_carry, rr = r_carry;
+            int tc = 0, to = 0, tsc = 0, tsj = 0;
+            for (int k = 0; k < kBlockWarps; ++k) {
+                if (k < warp) {
+                    pc += sh.wsum[k][0];
+                    po += sh.wsum[k][1];
+                    er += sh.wsum[k][2];
+                    rr += sh.wsum[k][3];
+                }
+                tc += sh.wsum[k][0];
+                to += sh.wsum[k][1];
+                tsc += sh.wsum[k][2];
+                tsj += sh.wsum[k][3];
+            }
+            for (int base = b0; base < b1; base += kGroup)
+                emit_group<kModeAny>(scr, hs, base, di.hlo + lo, er, rr, pc, po, ht, ht_off);
+            pc_carry += tc;
+            po_carry += to;
+            e_carry += tsc;
+            r_carry += tsj;
+            __syncthreads();
+        }
+        if (warp == 0) {
+            long long ec, eo;
+            seg_lookback(a.flags, s, pc_carry, po_carry, ec, eo);
+            if (lane == 0) {
+                sh.exc[0] = ec;
+                sh.exc[1] = eo;
+                write_offsets(a, s, ec, eo, pc_carry, po_carry);
+            }
+        }
+        __syncthreads();
+        const long long ec = sh.exc[0], eo = sh.exc[1];
+        for (int i = threadIdx.x; i < pc_carry; i += kBlockThreads) {
+            if (outp.ect) {
+                outp.eh[ec + i] = scr.eh[i];
+                outp.ev[ec + i] = scr.ev[i];
+            }
+            if (outp.cls) {
+                if (!outp.alias) outp.ch[ec + i] = scr.ch[i];
+                outp.cv[ec + i] = scr.cv[i];
+            }
+        }
+        if (outp.ord) {
+            for (int i = threadIdx.x; i < po_carry; i += kBlockThreads) {
+                outp.oh[eo + i] = scr.oh[i];
+                outp.ov[eo + i] = scr.ov[i];
+            }
+        }
+        if (outp.tab) {
+            for (int k = 16; k; k >>= 1) ht += __shfl_xor_sync(0xffffffffu, ht, k);
+            if (lane == 0) sh.ht[warp] = ht;
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                double t = 0.0;
+                for (int k = 0; k < kBlockWarps; ++k) t += sh.ht[k];
+                ht_write(a, s, t);
+            }
+        }
+        return;
+    }
     // phase A: counts over all windows
     long long nc = 0, no = 0;
     for (int w = 0; w < nwin; ++w) {
         const int lo = w * win, wb = min(win, di.R - lo);
-        fill_window(a, list, toff, n, di, lo, wb, cull, hs, sh.hit, &sh.nhit);
+        fill_window<DP>(a, list, toff, n, di, lo, wb, cull, hs, sh.hit, &sh.nhit);
         __syncthreads();
         int c = 0, o = 0;
         const int b0 = min(wb, warp * per), b1 = min(wb, b0 + per);
@@ -917,7 +1033,7 @@ __device__ __forceinline__ void block_segment(const K2Args &a, const OutPtrs<Out
     for (int w = 0; w < nwin; ++w) {
         const int lo = w * win, wb = min(win, di.R - lo);
         if (nwin > 1) {
-            fill_window(a, list, toff, n, di, lo, wb, cull, hs, sh.hit, &sh.nhit);
+            fill_window<DP>(a, list, toff, n, di, lo, wb, cull, hs, sh.hit, &sh.nhit);
             __syncthreads();
         }
         const int b0 = min(wb, warp * per), b1 = min(wb, b0 + per);
@@ -985,7 +1101,7 @@ __device__ __forceinline__ void block_segment(const K2Args &a, const OutPtrs<Out
 // di.line records (the vertices of one height level) of |a|+|b| <= max_rec, and
 // no more than the list's sum |a|+|b|; else split bins (two int32 arrays, windows
 // of win bins). `hist` is cleared on entry and left cleared by every segment.
-template <typename RecT, typename OutT>
+template <typename RecT, typename OutT, int DP>
 __global__ void __launch_bounds__(kBlockThreads, 1) k2_block(K2Args a, long long nseg, int win) {
     extern __shared__ __align__(16) unsigned hist[];
     __shared__ BlockShared sh;
@@ -999,8 +1115,8 @@ __global__ void __launch_bounds__(kBlockThreads, 1) k2_block(K2Args a, long long
         if (s >= nseg) break;
         const long long b = s / a.D, d = s % a.D;
         const long long bin_bound = min((long long)a.dirs[d].line * (long long)a.max_rec, (long long)a.max_abs_sum);
-        if (bin_bound < 32768) block_segment<true, RecT, OutT>(a, outp, hist, 2 * win, s, b, d, sh);
-        else block_segment<false, RecT, OutT>(a, outp, hist, win, s, b, d, sh);
+        if (bin_bound < 32768) block_segment<true, DP, RecT, OutT>(a, outp, hist, 2 * win, s, b, d, sh);
+        else block_segment<false, DP, RecT, OutT>(a, outp, hist, win, s, b, d, sh);
     }
 }
 
@@ -1046,7 +1162,7 @@ cudaError_t launch_t(const K2Args &a, cudaStream_t s, int num_sms) {
         return cudaGetLastError();
     }
     const int win = (int)(kBlockSmem / 8) / kGroup * kGroup;  // split bins; packed segments use 2 * win
-    auto kern = k2_block<RecT, OutT>;
+    auto kern = a.dp == 3 ? k2_block<RecT, OutT, 3> : a.dp == 2 ? k2_block<RecT, OutT, 2> : k2_block<RecT, OutT, 0>;
     cudaError_t e = prepare_kernel((const void *)kern, kBlockThreads, kBlockSmem, nullptr);
     if (e != cudaSuccess) return e;
     long long grid = std::min<long long>(nseg, num_sms);
@@ -1075,6 +1191,23 @@ cudaError_t launch_csr_scan(const K2Args &a, const int *cnt_c, const int *cnt_o,
     k2_scan<<<(unsigned)ntiles, kScanThreads, 0, s>>>(a, cnt_c, cnt_o, S, a.flags);
     count_launch();
     return cudaGetLastError();
+}
+
+size_t k2_stage_bytes(const K2Args &a, int num_sms, int64_t *cap) {
+    *cap = 0;
+    const long long nseg = a.batch * a.D;
+    const int words = a.pack16 ? 1 : 2;
+    const int rcap = (a.R_max + kGroup - 1) / kGroup * kGroup;
+    const size_t per_warp = (size_t)rcap * 4 * words;
+    const int warps = (int)std::min<size_t>(8, (200 * 1024) / per_warp);
+    if (nseg == 0 || (warps >= 2 && a.max_count <= 32768)) return 0;  // warp regime
+    // per stream and segment: at most min(list length, R) entries
+    const int64_t c = std::max<int64_t>(1, std::min<int64_t>(a.max_count, a.R_max));
+    const long long grid = std::min<long long>(nseg, num_sms);
+    const size_t bytes = (size_t)grid * 6 * (size_t)c * (size_t)a.elem_bytes;
+    if (bytes > (size_t(4) << 30)) return 0;
+    *cap = c;
+    return bytes;
 }
 
 cudaError_t launch_k2(const K2Args &a, cudaStream_t s, int num_sms) {
