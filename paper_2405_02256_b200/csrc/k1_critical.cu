@@ -228,24 +228,47 @@ __device__ __forceinline__ void k1_tile(const K1Args &a, unsigned ticket, const 
     // cols x0-1 .. x0+TXe; one warp per region row, lanes along the row
     const TIn *img = reinterpret_cast<const TIn *>(a.img) + b * a.npix;
     const int SENT = (CONS == EUCALC_VERTEX) ? INT_MIN : INT_MAX;
-#pragma unroll 4
-    for (int row = warp; row < RZ * RY; row += kThreads / 32) {
-        const int pz = row / RY, ry = row - pz * RY;
-        const int gy = y0 - 1 + ry, gz = (N == 3) ? z0 - 1 + pz : 0;
-        const bool rin = gy >= 0 && gy < mY && gz >= 0 && gz < mZ;
-        int *dst = reg + row * RX;
-        if (raw) {  // TMA box already in shared memory (out-of-range elements zero-filled)
+    if (raw) {  // TMA box already in shared memory (out-of-range elements zero-filled)
+        for (int row = warp; row < RZ * RY; row += kThreads / 32) {
+            const int pz = row / RY, ry = row - pz * RY;
+            const int gy = y0 - 1 + ry, gz = (N == 3) ? z0 - 1 + pz : 0;
+            const bool rin = gy >= 0 && gy < mY && gz >= 0 && gz < mZ;
+            int *dst = reg + row * RX;
             const TIn *src = raw + ((long long)pz * ybox + ry) * xbox + (16 / (int)sizeof(TIn) - 1);
             for (int rx = lane; rx < RX; rx += 32) {
                 const int gx = x0 - 1 + rx;
                 dst[rx] = (rin && gx >= 0 && gx < mX) ? (int)src[rx] : SENT;
             }
-        } else {
-            const TIn *src = img + ((int64_t)gz * mY + gy) * mX;
-            for (int rx = lane; rx < RX; rx += 32) {
-                const int gx = x0 - 1 + rx;
-                dst[rx] = (rin && gx >= 0 && gx < mX) ? load_img(src, gx) : SENT;
+        }
+    } else {
+        // flat walk over the region (all lanes busy), element index -> (pz, ry, rx)
+        // advanced incrementally by kThreads (no division per element), four
+        // loads in flight per thread
+        const int RXY = RX * RY, NR = RXY * RZ;
+        const int sz_ = kThreads / RXY, r1 = kThreads - sz_ * RXY, sy_ = r1 / RX, sx_ = r1 - sy_ * RX;
+        int pz = tid / RXY, rem = tid - pz * RXY, ry = rem / RX, rx = rem - ry * RX;
+        for (int i0 = tid; i0 < NR; i0 += 4 * kThreads) {
+            int v[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int gx = x0 - 1 + rx, gy = y0 - 1 + ry, gz = (N == 3) ? z0 - 1 + pz : 0;
+                const bool in = i0 + u * kThreads < NR && gx >= 0 && gx < mX && gy >= 0 && gy < mY && gz >= 0 && gz < mZ;
+                v[u] = in ? load_img(img, ((int64_t)gz * mY + gy) * mX + gx) : SENT;
+                rx += sx_;
+                if (rx >= RX) {
+                    rx -= RX;
+                    ++ry;
+                }
+                ry += sy_;
+                if (ry >= RY) {
+                    ry -= RY;
+                    ++pz;
+                }
+                pz += sz_;
             }
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+                if (i0 + u * kThreads < NR) reg[i0 + u * kThreads] = v[u];
         }
     }
     __syncthreads();
@@ -257,7 +280,9 @@ __device__ __forceinline__ void k1_tile(const K1Args &a, unsigned ticket, const 
     int cnt_o[1 << N][2];
 #pragma unroll
     for (int e = 0; e < (1 << N); ++e) cnt_o[e][0] = cnt_o[e][1] = 0;
-    long long abs_sum[Q];
+    // per thread: at most kTileV / kThreads vertices; 16-bit records keep the sum in int32
+    using AccT = std::conditional_t<std::is_same<RecT, Rec16>::value, int, long long>;
+    AccT abs_sum[Q];
     int max_rec[Q];
 #pragma unroll
     for (int q = 0; q < Q; ++q) {
@@ -268,16 +293,14 @@ __device__ __forceinline__ void k1_tile(const K1Args &a, unsigned ticket, const 
     int wrun[Q];
 #pragma unroll
     for (int q = 0; q < Q; ++q) wrun[q] = 0;
+    // vertex index li = c0 + tid -> (lz, ly, lx), advanced incrementally by kThreads
+    const int vz_ = kThreads / TP, v1 = kThreads - vz_ * TP, vy_ = v1 / TXe, vx_ = v1 - vy_ * TXe;
+    int lz = tid / TP, lrem = tid - lz * TP, ly = lrem / TXe, lx = lrem - ly * TXe;
     for (int c0 = 0; c0 < TV; c0 += kThreads) {
         const int li = c0 + tid;
         const bool valid = li < TV;
         int dm[1 << N];
-        int lz = 0, ly = 0, lx = 0;
         if (valid) {
-            lz = li / TP;
-            const int r = li - lz * TP;
-            ly = r / TXe;
-            lx = r - ly * TXe;
             const int base = ((N == 3) ? (lz + 1) * sz : 0) + (ly + 1) * sy + (lx + 1);
             vertex_dminus<N, CONS>(reg, sz, sy, base, dm);
         } else {
@@ -296,6 +319,17 @@ __device__ __forceinline__ void k1_tile(const K1Args &a, unsigned ticket, const 
             if (N >= 2) coord |= ((uint32_t)gy << a.sh[N - 2]);
             if (N == 3) coord |= ((uint32_t)(z0 + lz) << a.sh[0]);
         }
+        lx += vx_;
+        if (lx >= TXe) {
+            lx -= TXe;
+            ++ly;
+        }
+        ly += vy_;
+        if (ly >= TYe) {
+            ly -= TYe;
+            ++lz;
+        }
+        lz += vz_;
         // warp-private compaction: warp w appends to its own slice of the
         // staging area (no block barrier per vertex batch); the tile's order is
         // (warp, batch, lane) and the slices are concatenated at copy-out
@@ -341,9 +375,9 @@ __device__ __forceinline__ void k1_tile(const K1Args &a, unsigned ticket, const 
     }
 #pragma unroll
     for (int q = 0; q < Q; ++q) {
-        long long v = abs_sum[q];
+        AccT v = abs_sum[q];
         for (int d = 16; d; d >>= 1) v += __shfl_xor_sync(0xffffffffu, v, d);
-        if (lane == 0 && v) atomicAdd((unsigned long long *)&a.abs_sum[b * Q + q], (unsigned long long)v);
+        if (lane == 0 && v) atomicAdd((unsigned long long *)&a.abs_sum[b * Q + q], (unsigned long long)(long long)v);
         int mr = max_rec[q];
         for (int d = 16; d; d >>= 1) mr = max(mr, __shfl_xor_sync(0xffffffffu, mr, d));
         if (lane == 0 && mr) atomicMax((unsigned long long *)&a.max_rec[b * Q + q], (unsigned long long)mr);
