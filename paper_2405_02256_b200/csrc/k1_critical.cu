@@ -117,8 +117,17 @@ __host__ __device__ constexpr bool top_coface(int idx, int c) {
     return true;
 }
 
-template <int N, int CONS>
-__device__ __forceinline__ void vertex_dminus(const int *s, int sz, int sy, int base, int (&dm)[1 << N]) {
+// Staged region element: int16 for 8-bit images (the sentinels -32768 / 32767
+// lie outside 0..255: half the shared memory, more CTAs per SM), else int32.
+template <typename TIn>
+using RegT = std::conditional_t<sizeof(TIn) == 1, short, int>;
+template <typename R>
+__host__ __device__ constexpr int sent_lo() { return sizeof(R) == 2 ? -32768 : INT_MIN; }
+template <typename R>
+__host__ __device__ constexpr int sent_hi() { return sizeof(R) == 2 ? 32767 : INT_MAX; }
+
+template <int N, int CONS, typename R>
+__device__ __forceinline__ void vertex_dminus(const R *s, int sz, int sy, int base, int (&dm)[1 << N]) {
     constexpr int P3 = pow3(N);
     int val[P3];
     auto stride = [&](int k) { return (k == N - 1) ? 1 : ((k == N - 2) ? sy : sz); };
@@ -140,7 +149,9 @@ __device__ __forceinline__ void vertex_dminus(const int *s, int sz, int sy, int 
         });
         static_for<0, P3>([&](auto I) {
             constexpr int idx = decltype(I)::value;
-            val[idx] = (val[idx] == INT_MIN) ? 0 : val[idx];
+            // 8-bit images (int16 region): weights >= 0 > sentinel, so one max masks
+            if constexpr (sizeof(R) == 2) val[idx] = max(val[idx], 0);
+            else val[idx] = (val[idx] == sent_lo<R>()) ? 0 : val[idx];
         });
     } else {
         // 2^n pixels around the vertex (pixel x + c, c in {-1,0}^n); base <-> c = 0
@@ -156,11 +167,11 @@ __device__ __forceinline__ void vertex_dminus(const int *s, int sz, int sy, int 
         });
         static_for<0, P3>([&](auto I) {
             constexpr int idx = decltype(I)::value;
-            int mval = INT_MAX;
+            int mval = sent_hi<R>();
             static_for<0, P2>([&](auto C) {
                 if constexpr (top_coface<N>(idx, decltype(C)::value)) mval = min(mval, pix[decltype(C)::value]);
             });
-            val[idx] = (mval == INT_MAX) ? 0 : mval;
+            val[idx] = (mval == sent_hi<R>()) ? 0 : mval;
         });
     }
     // inclusion-exclusion: along axis k, slot +1 <- z(0) - z(-1) (eps_k=+1), slot -1 <- z(0) - z(+1)
@@ -199,7 +210,7 @@ struct K1Shared {
 // `sh.ostat` must be zero on entry (it is left zero on exit).
 template <int N, int CONS, typename TIn, typename RecT>
 __device__ __forceinline__ void k1_tile(const K1Args &a, unsigned ticket, const TIn *raw, int xbox, int ybox,
-                                        RecT *stage, int *reg, K1Shared<N> &sh) {
+                                        RecT *stage, RegT<TIn> *reg, K1Shared<N> &sh) {
     constexpr int Q = 1 << (N - 1);
     constexpr int FULL = (1 << N) - 1;
     auto &s_warp = sh.warp;
@@ -227,13 +238,13 @@ __device__ __forceinline__ void k1_tile(const K1Args &a, unsigned ticket, const 
     // for TOP) with a one-voxel halo: planes z0-1 .. z0+TZe, rows y0-1 .. y0+TYe,
     // cols x0-1 .. x0+TXe; one warp per region row, lanes along the row
     const TIn *img = reinterpret_cast<const TIn *>(a.img) + b * a.npix;
-    const int SENT = (CONS == EUCALC_VERTEX) ? INT_MIN : INT_MAX;
+    const int SENT = (CONS == EUCALC_VERTEX) ? sent_lo<RegT<TIn>>() : sent_hi<RegT<TIn>>();
     if (raw) {  // TMA box already in shared memory (out-of-range elements zero-filled)
         for (int row = warp; row < RZ * RY; row += kThreads / 32) {
             const int pz = row / RY, ry = row - pz * RY;
             const int gy = y0 - 1 + ry, gz = (N == 3) ? z0 - 1 + pz : 0;
             const bool rin = gy >= 0 && gy < mY && gz >= 0 && gz < mZ;
-            int *dst = reg + row * RX;
+            RegT<TIn> *dst = reg + row * RX;
             const TIn *src = raw + ((long long)pz * ybox + ry) * xbox + (16 / (int)sizeof(TIn) - 1);
             for (int rx = lane; rx < RX; rx += 32) {
                 const int gx = x0 - 1 + rx;
@@ -431,7 +442,7 @@ __global__ void __launch_bounds__(kThreads) k1_kernel(K1Args a) {
     constexpr int Q = 1 << (N - 1);
     extern __shared__ __align__(16) unsigned char smem[];
     RecT *stage = reinterpret_cast<RecT *>(smem);           // [Q][kTileV]
-    int *reg = reinterpret_cast<int *>(stage + Q * kTileV);  // input region
+    RegT<TIn> *reg = reinterpret_cast<RegT<TIn> *>(stage + Q * kTileV);  // input region
     __shared__ K1Shared<N> sh;
     __shared__ unsigned s_ticket;
     if (threadIdx.x == 0) s_ticket = atomicAdd(a.ticket, 1u);
@@ -471,7 +482,7 @@ __global__ void __launch_bounds__(kThreads) k1_tma(const __grid_constant__ CUten
     const int box_pad = (box_bytes + 127) / 128 * 128;
     TIn *raw[2] = {reinterpret_cast<TIn *>(k1_smem_tma), reinterpret_cast<TIn *>(k1_smem_tma + box_pad)};
     RecT *stage = reinterpret_cast<RecT *>(k1_smem_tma + 2 * box_pad);  // [Q][kTileV]
-    int *reg = reinterpret_cast<int *>(stage + Q * kTileV);        // input region
+    RegT<TIn> *reg = reinterpret_cast<RegT<TIn> *>(stage + Q * kTileV);  // input region
     __shared__ K1Shared<N> sh;
     __shared__ unsigned long long bar[2];
     __shared__ unsigned s_next;
@@ -544,7 +555,7 @@ template <int N, int CONS, typename TIn, typename RecT>
 cudaError_t launch_t(const K1Args &a, cudaStream_t s) {
     constexpr int Q = 1 << (N - 1);
     const int planes = (N == 3) ? a.TZ + 2 : 1;
-    const size_t region = sizeof(int) * planes * (a.TY + 2) * (a.TX + 2);
+    const size_t region = sizeof(RegT<TIn>) * planes * (a.TY + 2) * (a.TX + 2);
     const size_t stage = sizeof(RecT) * Q * kTileV;
     const int64_t ntiles = a.batch * (int64_t)a.tiles_x * a.tiles_y * a.tiles_z;
     // TMA path: tiled images with 16-byte aligned base, rows and tile origins, boxes
