@@ -237,43 +237,58 @@ def _alloc_steps(torch, S, cap, elem_bytes, device, with_height=True):
     return dict(offsets=off, height=h, value=v), st
 
 
+class _CsrBlock:
+    """All requested CSR streams (and optionally one extra tensor, the fused HT
+    output) carved out of ONE allocation: one allocator call instead of up to
+    nine. Offsets first (8-byte aligned), then heights/values. The C structs
+    (`sts`) are built from raw addresses, so the library call can be issued
+    before any tensor view is created (views(): after the launch, off the
+    device's critical path)."""
+
+    def __init__(self, torch, S, cap, elem_bytes, device, names, share, extra=None):
+        self.torch, self.S, self.cap, self.eb = torch, S, max(cap, 1), elem_bytes
+        self.dt = {2: torch.int16, 4: torch.int32, 8: torch.int64}[elem_bytes]
+        pin = device == "cpu" and torch.cuda.is_available()
+        arr = (self.cap * elem_bytes + 255) // 256 * 256
+        offb = ((S + 1) * 8 + 255) // 256 * 256
+        self.plan = []
+        total = 0
+        for name in names:
+            has_h = not (name == "classical" and share)
+            h = total + offb if has_h else None
+            v = total + offb + (arr if has_h else 0)
+            self.plan.append((name, total, h, v))
+            total = v + arr
+        self.extra = extra
+        self.xoff = total
+        if extra is not None:
+            xshape, xdt = extra
+            self.xn = int(np.prod(xshape)) * (4 if xdt == torch.float32 else 8)
+            total += (self.xn + 255) // 256 * 256
+        self.buf = torch.empty(total, dtype=torch.uint8, device=device, pin_memory=pin)
+        base = self.buf.data_ptr()
+        self.sts = {}
+        for name, o, h, v in self.plan:
+            self.sts[name] = _Steps(base + o, base + h if h is not None else 0, base + v, cap, elem_bytes, 0)
+        self.extra_ptr = base + self.xoff
+
+    def views(self):
+        torch, buf, n = self.torch, self.buf, self.cap * self.eb
+        res = {}
+        for name, o, h, v in self.plan:
+            res[name] = dict(offsets=buf[o:o + (self.S + 1) * 8].view(torch.int64),
+                             height=buf[h:h + n].view(self.dt) if h is not None else None,
+                             value=buf[v:v + n].view(self.dt))
+        if self.extra is not None:
+            xshape, xdt = self.extra
+            res["_extra"] = buf[self.xoff:self.xoff + self.xn].view(xdt).view(xshape)
+        return res
+
+
 def _alloc_all(torch, S, cap, elem_bytes, device, names, share, extra=None):
-    """All requested CSR streams carved out of ONE allocation (one allocator call
-    instead of up to nine): offsets first (8-byte aligned), then heights/values.
-    extra=(shape, dtype) appends one more tensor (the fused HT output), returned
-    as res["_extra"]."""
-    dt = {2: torch.int16, 4: torch.int32, 8: torch.int64}[elem_bytes]
-    pin = device == "cpu" and torch.cuda.is_available()
-    cap1 = max(cap, 1)
-    arr = cap1 * elem_bytes
-    arr = (arr + 255) // 256 * 256
-    offb = ((S + 1) * 8 + 255) // 256 * 256
-    plan = []
-    total = 0
-    for name in names:
-        has_h = not (name == "classical" and share)
-        plan.append((name, total, has_h))
-        total += offb + arr * (2 if has_h else 1)
-    xoff = total
-    if extra is not None:
-        xshape, xdt = extra
-        xn = int(np.prod(xshape)) * torch.empty(0, dtype=xdt).element_size()
-        total += (xn + 255) // 256 * 256
-    buf = torch.empty(total, dtype=torch.uint8, device=device, pin_memory=pin)
-    res, sts = {}, {}
-    for name, o, has_h in plan:
-        off = buf[o:o + (S + 1) * 8].view(torch.int64)
-        p = o + offb
-        h = None
-        if has_h:
-            h = buf[p:p + cap1 * elem_bytes].view(dt)
-            p += arr
-        v = buf[p:p + cap1 * elem_bytes].view(dt)
-        res[name] = dict(offsets=off, height=h, value=v)
-        sts[name] = _Steps(off.data_ptr(), h.data_ptr() if h is not None else 0, v.data_ptr(), cap, elem_bytes, 0)
-    if extra is not None:
-        res["_extra"] = buf[xoff:xoff + xn].view(xdt).view(xshape)
-    return res, sts
+    """(views dict, C structs) of a _CsrBlock (callers that need the views first)."""
+    blk = _CsrBlock(torch, S, cap, elem_bytes, device, names, share, extra)
+    return blk.views(), blk.sts
 
 
 def transforms(cr: Critical, dirs, ect=True, ordinary=True, classical=True, elem_bytes=8, device="cuda",
@@ -310,9 +325,9 @@ def transforms(cr: Critical, dirs, ect=True, ordinary=True, classical=True, elem
     extra = None
     if ht is not None:  # the HT output shares the CSR allocation
         extra = ((cr.cx.batch, D), torch.float32 if ht[2] == "f32" else torch.float64)
-    res, sts = _alloc_all(torch, S, bound, elem_bytes, device, names, share, extra)
+    blk = _CsrBlock(torch, S, bound, elem_bytes, device, names, share, extra)
+    sts = blk.sts
     if share:
-        res["classical"]["height"] = res["ect"]["height"]
         sts["classical"].height = sts["ect"].height
     req = ctypes.c_int64()
     refs = [ctypes.byref(sts[n]) if n in sts else None for n in ("ect", "ordinary", "classical")]
@@ -320,11 +335,14 @@ def transforms(cr: Critical, dirs, ect=True, ordinary=True, classical=True, elem
         _check(lib().eucalc_transforms(cr._h, p, D, refs[0], refs[1], refs[2], ctypes.byref(req), st), req.value)
     else:
         kern, param, prec = ht
-        out = res.pop("_extra")
         _check(lib().eucalc_transforms_ht(cr._h, p, D, refs[0], refs[1], refs[2], KERNELS[kern], float(param),
-                                          PRECISIONS[prec], ctypes.c_void_p(out.data_ptr()), ctypes.byref(req), st),
+                                          PRECISIONS[prec], ctypes.c_void_p(blk.extra_ptr), ctypes.byref(req), st),
                req.value)
-        res["ht"] = out
+    res = blk.views()  # tensor views after the launch (the kernels already run)
+    if share:
+        res["classical"]["height"] = res["ect"]["height"]
+    if ht is not None:
+        res["ht"] = res.pop("_extra")
     return res
 
 

@@ -46,7 +46,7 @@ def timed_empty(*a, **k):
 
 torch.empty = timed_empty
 gray, binary, dirs = bench.workload(0)
-imgs = [torch.from_numpy(gray).cuda(), torch.from_numpy(binary).cuda()]
+imgs = [torch.from_numpy(x).cuda() for x in bench.step_batches(gray, binary)]
 N = 30
 tot = 0.0
 for it in range(N + 5):
@@ -62,3 +62,34 @@ for it in range(N + 5):
 print(f"run_step host total {tot / N:8.1f} us")
 for k, v in sorted(T.items(), key=lambda x: -x[1]):
     print(f"{k:34s} {v / N:8.1f} us")
+
+# one step's call sequence: (call, start, end) in us since run_step entry
+SEQ = []
+T0 = [0.0]
+
+
+class Seq(Timed):
+    def __getattr__(self, name):
+        f = getattr(self._L, name)
+        if not callable(f):
+            return f
+
+        def g(*a):
+            t0 = time.perf_counter()
+            r = f(*a)
+            SEQ.append((name, (t0 - T0[0]) * 1e6, (time.perf_counter() - T0[0]) * 1e6))
+            return r
+        return g
+
+
+eu._lib = Seq(real)
+for it in range(3):
+    SEQ.clear()
+    torch.cuda.synchronize()
+    T0[0] = time.perf_counter()
+    out = bench.run_step(eu, torch, imgs, dirs)
+    SEQ.append(("run_step returned", (time.perf_counter() - T0[0]) * 1e6, 0.0))
+    torch.cuda.synchronize()
+    del out
+for name, a, b in SEQ:
+    print(f"{name:34s} {a:8.1f} {b:8.1f}")

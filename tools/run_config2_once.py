@@ -1,5 +1,5 @@
-"""One bench step (config 2 gray then binary, as bench.py's run_step) per
-iteration, for ncu captures (diagnostics, not product code)."""
+"""One bench step (config 2 gray + binary as bench.py's step batches and
+run_step) per iteration, for ncu captures (diagnostics, not product code)."""
 import os
 import sys
 
@@ -10,7 +10,7 @@ import bench  # noqa: E402
 import paper_2405_02256_b200 as eu  # noqa: E402
 
 gray, binary, dirs = bench.workload(0)
-imgs = [torch.from_numpy(gray).cuda(), torch.from_numpy(binary).cuda()]
+imgs = [torch.from_numpy(x).cuda() for x in bench.step_batches(gray, binary)]
 for it in range(int(os.environ.get("ITERS", "2"))):
     bench.run_step(eu, torch, imgs, dirs)
     torch.cuda.synchronize()

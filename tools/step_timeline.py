@@ -14,7 +14,7 @@ import bench  # noqa: E402
 import paper_2405_02256_b200 as eu  # noqa: E402
 
 gray, binary, dirs = bench.workload(0)
-imgs = [torch.from_numpy(gray).cuda(), torch.from_numpy(binary).cuda()]
+imgs = [torch.from_numpy(x).cuda() for x in bench.step_batches(gray, binary)]
 flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
 cur = torch.cuda.current_stream()
 streams = [torch.cuda.Stream(), torch.cuda.Stream()]

@@ -1,6 +1,6 @@
 """DRAM traffic of the bench's dominant stage (K2: k2w_count + k2_scan + k2w_emit,
-fused HT) from an ncu capture of tools/run_config2_once.py, averaged over the
-gray and binary launches of the second iteration -> profiles/<round>/k2_traffic.json.
+fused HT) from an ncu capture of tools/run_config2_once.py: the launches of the
+second iteration (one bench step) -> profiles/<round>/k2_traffic.json.
 Run on the GPU box:  python tools/traffic.py profiles/r1"""
 import csv
 import io
@@ -27,9 +27,9 @@ ids = sorted(launch)
 half = ids[len(ids) // 2:]  # second iteration (warm)
 tot = sum(launch[i]["dram__bytes_read.sum"] + launch[i]["dram__bytes_write.sum"] for i in half)
 res = {"stage": "k2_transforms (k2w_count + k2_scan + k2w_emit + k3_table, fused HT)",
-       "dram_bytes_per_launch": tot / 2, "dram_bytes_per_step": tot, "launches_per_stage_call": len(half) / 2,
+       "dram_bytes_per_step": tot, "launches_per_step": len(half),
        "source": "ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum (tools/traffic.py), "
-                 "second iteration of tools/run_config2_once.py, mean of gray and binary",
+                 "second iteration (one bench step) of tools/run_config2_once.py",
        "per_kernel": [{k: launch[i][k] for k in launch[i]} for i in half]}
 os.makedirs(out_dir, exist_ok=True)
 json.dump(res, open(os.path.join(out_dir, "k2_traffic.json"), "w"), indent=1)
