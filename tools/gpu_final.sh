@@ -10,7 +10,7 @@ timeout 900 python bench.py --impl reference --steps 2 --warmup 3 > $OUT/bench_r
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/launches.csv python bench.py --steps 2 --warmup 3 --no-cpu-baseline > $OUT/ncu_launches.log 2>&1; echo "launches rc=$?"
 python tools/ncu_summary.py launches $OUT/launches.csv > $OUT/launches.txt 2>&1
 timeout 900 python tools/traffic.py $OUT > $OUT/traffic.log 2>&1; echo "traffic rc=$?"; cat $OUT/traffic.log
-ITERS=2 timeout 900 ncu --set full --clock-control none --import-source on -k "regex:k2w_emit" -s 2 -c 1 -o $OUT/top python tools/run_config2_once.py > $OUT/ncu_full.log 2>&1; echo "ncu full rc=$?"
+ITERS=2 timeout 900 ncu --set full --clock-control none --import-source on -k "regex:k2w_emit" -s 1 -c 1 -o $OUT/top python tools/run_config2_once.py > $OUT/ncu_full.log 2>&1; echo "ncu full rc=$?"
 python tools/ncu_summary.py full $OUT/top.ncu-rep > $OUT/top.full.txt 2>&1
 python tools/ncu_source.py $OUT/top.ncu-rep 30 > $OUT/top.source.txt 2>&1
 rm -f $OUT/top.ncu-rep
