@@ -317,6 +317,47 @@ __device__ __forceinline__ void put_o(const OutPtrs<OutT> &o, int p, int h, int 
     }
 }
 
+// Predicated global store (no branch: every lane computes the address; a
+// divergent `if` around the store costs a reconvergence stack push/pop and the
+// base pointers' reload on each side).
+template <typename OutT>
+__device__ __forceinline__ void st_if(OutT *p, int v, bool pred) {
+    if constexpr (sizeof(OutT) == 2)
+        asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q st.global.b16 [%0], %1;\n\t}" ::"l"(p),
+                     "h"((unsigned short)v), "r"((unsigned)pred)
+                     : "memory");
+    else if constexpr (sizeof(OutT) == 4)
+        asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q st.global.b32 [%0], %1;\n\t}" ::"l"(p),
+                     "r"(v), "r"((unsigned)pred)
+                     : "memory");
+    else
+        asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q st.global.b64 [%0], %1;\n\t}" ::"l"(p),
+                     "l"((long long)v), "r"((unsigned)pred)
+                     : "memory");
+}
+template <int MODE, typename OutT>
+__device__ __forceinline__ void put_c_if(const OutPtrs<OutT> &o, int p, int h, int e, int cv, bool pred) {
+    const bool ect = MODE == kModeAny ? o.ect : (MODE & kEct);
+    const bool cls = MODE == kModeAny ? o.cls : (MODE & kCls);
+    const bool alias = MODE == kModeAny ? o.alias : (MODE & kAlias);
+    if (ect) {
+        st_if(o.eh + p, h, pred);
+        st_if(o.ev + p, e, pred);
+    }
+    if (cls) {
+        if (!alias) st_if(o.ch + p, h, pred);
+        st_if(o.cv + p, cv, pred);
+    }
+}
+template <int MODE, typename OutT>
+__device__ __forceinline__ void put_o_if(const OutPtrs<OutT> &o, int p, int h, int r, bool pred) {
+    const bool ord = MODE == kModeAny ? o.ord : (MODE & kOrd);
+    if (ord) {
+        st_if(o.oh + p, h, pred);
+        st_if(o.ov + p, r, pred);
+    }
+}
+
 // Emit one 128-bin group held by a warp (lane <-> 4 consecutive bins) in height
 // order: local sums per lane, one warp scan of (counts, sum Delta^-, sum J),
 // then up to 4 entries per stream per lane. Running values are warp-uniform;
@@ -377,8 +418,10 @@ __device__ __forceinline__ void emit_group16(const OutPtrs<OutT> &o, const Hist<
     for (int s = 0; s < 4; ++s) {
         const int Pb = P;
         P += (int)u[s];
-        if (nzc[s]) put_c<MODE>(o, p_c++, hb + s, (int)(short)(P & 0xffff), ((Pb + 0x8000) >> 16) + wc[s]);
-        if (nzo[s]) put_o<MODE>(o, p_o++, hb + s, (P + 0x8000) >> 16);
+        put_c_if<MODE>(o, p_c, hb + s, (int)(short)(P & 0xffff), ((Pb + 0x8000) >> 16) + wc[s], nzc[s]);
+        put_o_if<MODE>(o, p_o, hb + s, (P + 0x8000) >> 16, nzo[s]);
+        p_c += nzc[s];
+        p_o += nzo[s];
         if (do_ht && nzo[s]) ht = fma((double)(((int)u[s] - wc[s]) >> 16), tv[s], ht);
     }
     const int tc = __shfl_sync(0xffffffffu, ic, 31);
@@ -633,7 +676,7 @@ __global__ void __launch_bounds__(kWarpThreads) k2w_count(K2Args a, int rcap, in
 }
 
 template <typename RecT, typename OutT, bool PACK, int MODE>
-__global__ void __launch_bounds__(kWarpThreads) k2w_emit(K2Args a, int rcap) {
+__global__ void __launch_bounds__(kWarpThreads, 5) k2w_emit(K2Args a, int rcap) {
     extern __shared__ __align__(16) unsigned hist_all[];
     const Hist<PACK> hs = warp_hist<PACK>(hist_all, rcap);
     const OutPtrs<OutT> o(a);
