@@ -506,33 +506,68 @@ constexpr int kGroup = 128;  // bins per warp step (4 per lane)
 //   k2w_emit : per segment histogram again + ordered emission at its offset.
 // (A single pass with a segment look-back was measured to lose ~1/3 of the
 // time to look-back spinning when ~9k warps start at once.)
-template <typename RecT, bool PACK>
-// Fills the warp's histogram with the segment's records; returns the 128-bin
-// groups [g0, g1) that can hold a nonzero bin (the records' height span,
-// typically ~85% of R: the scans skip the rest).
-__device__ __forceinline__ void fill_segment(const K2Args &a, const Hist<PACK> &hs, long long b, const DirInfo &di,
-                                             int &g0, int &g1) {
+// Packed bin word of a 16-bit record for the direction's orthant, from the
+// record's weight word w = a | b << 16: wj * 2^16 + wc with (wc, wj) = (a, a - b)
+// (representative orthant) or (b, b - a) (its antipode, SWAP): one extract, one
+// mask/shift, one multiply-add.
+template <bool SWAP>
+__device__ __forceinline__ unsigned packed_word(unsigned w) {
+    if (SWAP) return (unsigned)(((int)w >> 16) * 65537 - (int)(w << 16));
+    return (unsigned)((int)(short)(w & 0xffffu) * 65537 - (int)(w & 0xffff0000u));
+}
+
+template <int DP, bool SWAP, typename RecT, bool PACK>
+__device__ __forceinline__ void fill_loop(const K2Args &a, const Hist<PACK> &hs, const RecT *list, int n,
+                                          const DirInfo &di, int &lo, int &hi) {
     const int lane = threadIdx.x & 31;
-    const RecT *list = reinterpret_cast<const RecT *>(a.rec) + (b * a.Q + di.q) * a.vcap;
-    const int n = a.count[b * a.Q + di.q];
-    int lo = INT_MAX, hi = -1;
     int i = lane;
     for (; i + 32 < n; i += 64) {  // two records in flight per lane
         const RecT r0 = list[i], r1 = list[i + 32];
         int bin0, wc0, wj0, bin1, wc1, wj1;
-        decode(r0, di, a, bin0, wc0, wj0);
-        decode(r1, di, a, bin1, wc1, wj1);
-        hs.add(bin0, wc0, wj0);
-        hs.add(bin1, wc1, wj1);
+        decode<DP>(r0, di, a, bin0, wc0, wj0);
+        decode<DP>(r1, di, a, bin1, wc1, wj1);
+        if constexpr (PACK && std::is_same<RecT, Rec16>::value) {
+            atomicAdd(hs.c + bin0, packed_word<SWAP>(reinterpret_cast<const uint2 &>(r0).y));
+            atomicAdd(hs.c + bin1, packed_word<SWAP>(reinterpret_cast<const uint2 &>(r1).y));
+        } else {
+            hs.add(bin0, wc0, wj0);
+            hs.add(bin1, wc1, wj1);
+        }
         lo = min(lo, min(bin0, bin1));
         hi = max(hi, max(bin0, bin1));
     }
     if (i < n) {
+        const RecT r = list[i];
         int bin, wc, wj;
-        decode(list[i], di, a, bin, wc, wj);
-        hs.add(bin, wc, wj);
+        decode<DP>(r, di, a, bin, wc, wj);
+        if constexpr (PACK && std::is_same<RecT, Rec16>::value)
+            atomicAdd(hs.c + bin, packed_word<SWAP>(reinterpret_cast<const uint2 &>(r).y));
+        else
+            hs.add(bin, wc, wj);
         lo = min(lo, bin);
         hi = max(hi, bin);
+    }
+}
+
+template <typename RecT, bool PACK>
+// Fills the warp's histogram with the segment's records; returns the 128-bin
+// groups [g0, g1) that can hold a nonzero bin (the records' height span,
+// typically ~85% of R: the scans skip the rest). The loop is specialised on the
+// height decode and the orthant side (both uniform per segment).
+__device__ __forceinline__ void fill_segment(const K2Args &a, const Hist<PACK> &hs, long long b, const DirInfo &di,
+                                             int &g0, int &g1) {
+    const RecT *list = reinterpret_cast<const RecT *>(a.rec) + (b * a.Q + di.q) * a.vcap;
+    const int n = a.count[b * a.Q + di.q];
+    int lo = INT_MAX, hi = -1;
+    if (a.dp == 2) {
+        if (di.swap) fill_loop<2, true>(a, hs, list, n, di, lo, hi);
+        else fill_loop<2, false>(a, hs, list, n, di, lo, hi);
+    } else if (a.dp == 3) {
+        if (di.swap) fill_loop<3, true>(a, hs, list, n, di, lo, hi);
+        else fill_loop<3, false>(a, hs, list, n, di, lo, hi);
+    } else {
+        if (di.swap) fill_loop<0, true>(a, hs, list, n, di, lo, hi);
+        else fill_loop<0, false>(a, hs, list, n, di, lo, hi);
     }
     for (int d = 16; d; d >>= 1) {
         lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, d));
