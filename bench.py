@@ -231,10 +231,11 @@ def gpu_arm(args):
     k2_span = 0.0  # wall span of the step's (concurrent) K2 launches
     launches = 0
     if True:
-        # as timeit: no Python garbage collection pauses inside the timed steps
+        # BENCH_NO_GC=1 (diagnostics): no Python garbage collection inside the timed steps
         gc_was = gc.isenabled()
-        gc.collect()
-        gc.disable()
+        if os.environ.get("BENCH_NO_GC") == "1":
+            gc.collect()
+            gc.disable()
         barrier()
         clk.mark()
         for _ in range(args.steps):
