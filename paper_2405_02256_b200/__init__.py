@@ -373,6 +373,24 @@ def transforms_real(cr: Critical, dirs, ect=True, ordinary=True, classical=True,
     return res
 
 
+def shard_directions(dirs, rank: int, world: int):
+    """Multi-GPU split of ONE image's directions: the directions,
+    stably grouped by antipodal orthant pair (directions of one pair read the
+    same critical list, Lemma 3), cut into `world` contiguous chunks of
+    near-equal size. Returns (indices into dirs, dirs[indices]) for `rank`. Each
+    rank runs K1 on the whole image and K2/K3 on its chunk; outputs stay sharded
+    (no data-path collective). Host logic only."""
+    d = np.ascontiguousarray(np.asarray(dirs).reshape(len(dirs), -1))
+    n = d.shape[1]
+    full = (1 << n) - 1
+    e = ((d > 0).astype(np.int64) << np.arange(n)).sum(1)
+    pair = np.where((e >> (n - 1)) & 1, e ^ full, e)
+    order = np.argsort(pair, kind="stable")
+    per = (len(order) + world - 1) // world
+    idx = order[min(len(order), rank * per):min(len(order), (rank + 1) * per)]
+    return idx, d[idx]
+
+
 def ect(cr: Critical, dirs, **kw):
     return transforms(cr, dirs, ect=True, ordinary=False, classical=False, **kw)["ect"]
 

@@ -86,4 +86,20 @@ def _shard_worker(rank, world):
     t[mine[0]:mine[1]] += 1
     dist.all_reduce(t)
     assert bool((t == 1).all())
+    # single-image configs: directions split by orthant pair into contiguous chunks
+    import numpy as np
+
+    import paper_2405_02256_b200 as eu
+    import synth
+
+    dirs = synth.random_directions(101, 3, 8, 5)
+    idx, sub = eu.shard_directions(dirs, rank, world)
+    assert np.array_equal(sub, dirs[idx])
+    u = torch.zeros(len(dirs), dtype=torch.int64)
+    u[torch.from_numpy(idx)] += 1
+    dist.all_reduce(u)
+    assert bool((u == 1).all())
+    e = ((sub > 0).astype(np.int64) << np.arange(3)).sum(1)
+    pair = np.where((e >> 2) & 1, e ^ 7, e)
+    assert np.all(np.diff(pair) >= 0)  # one orthant pair's directions stay together on a rank
     dist.destroy_process_group()
