@@ -1047,7 +1047,7 @@ eucalc_status transforms_impl(const eucalc_critical *ccr, const int32_t *dirs, i
     // flags + ticket are adjacent (one memset); then counts, slab, table, HT staging
     std::vector<void *> ar;
     if (!arena_take(st, {sizeof(unsigned long long) * S + sizeof(unsigned int) * 4, sizeof(int) * 2 * S,
-                         slab_ok ? sizeof(uint2) * 33 * S : 0, ht ? 12 * (size_t)U : 0,
+                         slab_ok ? sizeof(uint2) * 33 * S : 0, ht ? 8 * (size_t)U : 0,
                          ht_host ? ht_osz * S : 0},
                     ar)) {
         free_scratch();
@@ -1061,10 +1061,11 @@ eucalc_status transforms_impl(const eucalc_critical *ccr, const int32_t *dirs, i
     void *d_ht = ht ? (ht_host ? ar[4] : ht->out) : nullptr;
     cudaError_t e = cudaMemsetAsync(flags, 0, sizeof(unsigned long long) * S + sizeof(unsigned int) * 4, st);
     if (e == cudaSuccess && ht)
-        e = launch_k3_table_only(ht->kernel, ht->param, cx->L, p.U0, U, d_tab, (float *)(d_tab + U), st);
+        e = launch_k3_table_only(ht->kernel, ht->param, cx->L, p.U0, U, d_tab, nullptr, st);
     if (e == cudaSuccess) {
         a.ht_tab = d_tab;
         a.ht_U0 = p.U0;
+        a.ht_U = U;
         a.L = cx->L;
         a.csum = pe->d_csum;
         a.ht_scale = ht ? k3_scale(ht->kernel, ht->param) : 0.0;

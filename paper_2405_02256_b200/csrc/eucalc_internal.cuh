@@ -141,6 +141,7 @@ struct K2Args {
     // fused HT (NEXT f2): kbar table (fp64) over u in [ht_U0, ...), or NULL
     const double *ht_tab;
     int64_t ht_U0, L;
+    int64_t ht_U;               // table length
     const int32_t *csum;        // [D]
     double ht_scale;            // HT = ht_scale * sum_h H_J(h) f(u(h))
     int ht_prec;
@@ -184,7 +185,9 @@ struct K3Args {
 int k3_chunk(bool table);
 size_t k3_table_smem(bool f64, long long U);
 cudaError_t launch_k3(const K3Args &a, cudaStream_t s);
-// kbar table for u in [U0, U0 + U) (fp64 and fp32 copies) and the HT scale of each kernel
+// kbar table for u in [U0, U0 + U) in fp64, parity-split (even u - U0 first, then
+// odd; K2's fused HT), with an optional fp32 copy in natural order; and the HT
+// scale of each kernel
 cudaError_t launch_k3_table_only(int kernel, double param, int64_t L, int64_t U0, int64_t U, double *t64, float *t32,
                                  cudaStream_t s);
 double k3_scale(int kernel, double param);

@@ -284,14 +284,17 @@ struct OutPtrs {
 // height h, H_J(h) = sum of J over the records at h, so
 //   HT(xi) = -sum_x J(x) kbar(t(x)) = -sum_h H_J(h) kbar(t(h))      (Lemma 2)
 // costs one table lookup per nonzero bin instead of one kbar per record.
-// `tab_off` = -L*csum - U0, so the table index of height h is 2h + tab_off.
+// The table is parity-split (k3_table split = 1): u - U0 = 2h - L*csum - U0 has the
+// parity of t = -L*csum - U0 for every height h of a direction, so its entries
+// are contiguous: index(h) = h + tab_off with tab_off = (t & 1) * ceil(U/2) + (t >> 1).
 __device__ __forceinline__ void ht_write(const K2Args &a, long long s, double acc) {
     const double v = a.ht_scale * acc;
     if (a.ht_prec == EUCALC_F32) reinterpret_cast<float *>(a.ht_out)[s] = (float)v;
     else reinterpret_cast<double *>(a.ht_out)[s] = v;
 }
 __device__ __forceinline__ long long ht_tab_off(const K2Args &a, long long d) {
-    return -a.L * (long long)a.csum[d] - a.ht_U0;
+    const long long t = -a.L * (long long)a.csum[d] - a.ht_U0;
+    return (t & 1) * ((a.ht_U + 1) >> 1) + (t >> 1);
 }
 
 template <int MODE, typename OutT>
@@ -405,7 +408,7 @@ __device__ __forceinline__ void emit_group16(const OutPtrs<OutT> &o, const Hist<
     double tv[4];
     if (do_ht) {
 #pragma unroll
-        for (int s = 0; s < 4; ++s) tv[s] = nzo[s] ? __ldg(o.tab + 2 * (long long)(hb + s) + tab_off) : 0.0;
+        for (int s = 0; s < 4; ++s) tv[s] = nzo[s] ? __ldg(o.tab + (long long)(hb + s) + tab_off) : 0.0;
     }
     const int cnt = lc | (lo << 16);
     int ic = cnt, isum = sum;
@@ -466,7 +469,7 @@ __device__ __forceinline__ void emit_group(const OutPtrs<OutT> &o, const Hist<PA
         if (wc[s]) put_c<MODE>(o, p_c++, hb + s, e, rb + wc[s]);
         if (wj[s]) put_o<MODE>(o, p_o++, hb + s, r);
         const bool do_ht = (MODE == kModeAny) ? (o.tab != nullptr) : ((MODE & kHt) != 0);
-        if (do_ht && wj[s]) ht = fma((double)wj[s], __ldg(o.tab + 2 * (long long)(hb + s) + tab_off), ht);
+        if (do_ht && wj[s]) ht = fma((double)wj[s], __ldg(o.tab + (long long)(hb + s) + tab_off), ht);
     }
     const int tc = __shfl_sync(0xffffffffu, ic, 31);
     pc += tc & 0xffff;
@@ -691,7 +694,7 @@ __global__ void __launch_bounds__(kWarpThreads) k2w_count(K2Args a, int rcap, in
             if (a.ht_tab) {
                 // fused HT of a sparse segment: one term per merged run (fixed-order tree sum)
                 double acc = 0.0;
-                if (r.emit_o) acc = (double)r.run_j * __ldg(a.ht_tab + 2 * (long long)(di.hlo + r.h) + ht_tab_off(a, d));
+                if (r.emit_o) acc = (double)r.run_j * __ldg(a.ht_tab + (long long)(di.hlo + r.h) + ht_tab_off(a, d));
                 for (int k = 16; k; k >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, k);
                 if ((threadIdx.x & 31) == 0) ht_write(a, s, acc);
             }

@@ -217,7 +217,11 @@ __global__ void __launch_bounds__(kThreads) k3_f64(K3Args a) {
 // (fp32) or fp64 accumulation — precision-independent kbar cost, no SFU.
 constexpr int kChunkT = 8192;
 
-__global__ void k3_table(int kernel, double param, long long L, long long U0, long long U, double *t64, float *t32) {
+// split = 1 (fused HT in K2): t64 holds the even-offset entries (u - U0 even)
+// first, then the odd ones, so one direction's entries (fixed parity of u) are
+// contiguous in its heights; t32 may be NULL.
+__global__ void k3_table(int kernel, double param, long long L, long long U0, long long U, double *t64, float *t32,
+                         int split = 0) {
     const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= U) return;
     const long long u = U0 + i;
@@ -239,8 +243,8 @@ __global__ void k3_table(int kernel, double param, long long L, long long U0, lo
     } else {
         f = exp((double)u / (2.0 * (double)L));
     }
-    t64[i] = f;
-    t32[i] = (float)f;
+    t64[split ? ((i & 1) ? ((U + 1) >> 1) + (i >> 1) : (i >> 1)) : i] = f;
+    if (t32) t32[i] = (float)f;
 }
 
 template <int DP>
@@ -410,7 +414,7 @@ cudaError_t launch_k3_table(const K3Args &a, cudaStream_t s) {
 
 cudaError_t launch_k3_table_only(int kernel, double param, int64_t L, int64_t U0, int64_t U, double *t64, float *t32,
                                  cudaStream_t s) {
-    k3_table<<<(unsigned)((U + 255) / 256), 256, 0, s>>>(kernel, param, L, U0, U, t64, t32);
+    k3_table<<<(unsigned)((U + 255) / 256), 256, 0, s>>>(kernel, param, L, U0, U, t64, t32, 1);
     count_launch();
     return cudaGetLastError();
 }
