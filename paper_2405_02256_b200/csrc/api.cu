@@ -255,6 +255,7 @@ eucalc_status plan_dirs(const Complex *cx, const int32_t *dirs, int64_t D, cudaS
         di.swap = rep ? 0 : 1;
         p.info[d] = di;
         p.csum[d] = (int32_t)cs;
+        p.info[d].lcsum = cx->L * cs;
         p.orthant[d] = e;
         p.R_max = std::max(p.R_max, di.R);
         const int64_t Lc = cx->L * cs, ulo = 2 * lo - Lc, uhi = 2 * hi - Lc;

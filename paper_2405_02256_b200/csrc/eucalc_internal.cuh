@@ -101,6 +101,7 @@ struct DirInfo {
     int swap;       // 1 if the orthant is the pair's non-representative
     int xs8;        // xs as packed int8 (byte j <-> axis n-1-j) when every |xs_i| <= 127
     int line;       // max vertices on one lattice height level (bounds every bin's record count)
+    long long lcsum;  // L * csum (u = 2H - L*csum, the kbar table argument of the fused HT)
 };
 
 struct StepsOut {

@@ -292,8 +292,8 @@ __device__ __forceinline__ void ht_write(const K2Args &a, long long s, double ac
     if (a.ht_prec == EUCALC_F32) reinterpret_cast<float *>(a.ht_out)[s] = (float)v;
     else reinterpret_cast<double *>(a.ht_out)[s] = v;
 }
-__device__ __forceinline__ long long ht_tab_off(const K2Args &a, long long d) {
-    const long long t = -a.L * (long long)a.csum[d] - a.ht_U0;
+__device__ __forceinline__ long long ht_tab_off(const K2Args &a, const DirInfo &di) {
+    const long long t = -di.lcsum - a.ht_U0;
     return (t & 1) * ((a.ht_U + 1) >> 1) + (t >> 1);
 }
 
@@ -408,7 +408,7 @@ __device__ __forceinline__ void emit_group16(const OutPtrs<OutT> &o, const Hist<
     double tv[4];
     if (do_ht) {
 #pragma unroll
-        for (int s = 0; s < 4; ++s) tv[s] = nzo[s] ? __ldg(o.tab + (long long)(hb + s) + tab_off) : 0.0;
+        for (int s = 0; s < 4; ++s) tv[s] = nzo[s] ? __ldg(o.tab + ((long long)hb + tab_off) + s) : 0.0;
     }
     const int cnt = lc | (lo << 16);
     int ic = cnt, isum = sum;
@@ -694,7 +694,7 @@ __global__ void __launch_bounds__(kWarpThreads) k2w_count(K2Args a, int rcap, in
             if (a.ht_tab) {
                 // fused HT of a sparse segment: one term per merged run (fixed-order tree sum)
                 double acc = 0.0;
-                if (r.emit_o) acc = (double)r.run_j * __ldg(a.ht_tab + (long long)(di.hlo + r.h) + ht_tab_off(a, d));
+                if (r.emit_o) acc = (double)r.run_j * __ldg(a.ht_tab + (long long)(di.hlo + r.h) + ht_tab_off(a, di));
                 for (int k = 16; k; k >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, k);
                 if ((threadIdx.x & 31) == 0) ht_write(a, s, acc);
             }
@@ -755,7 +755,7 @@ __global__ void __launch_bounds__(kWarpThreads, 5) k2w_emit(K2Args a, int rcap) 
             fill_segment<RecT>(a, hs, b, di, g0, g1);
             int e_run = 0, r_run = 0;
             double ht = 0.0;
-            const long long toff = (MODE & kHt) || (MODE == kModeAny && o.tab) ? ht_tab_off(a, d) : 0;
+            const long long toff = (MODE & kHt) || (MODE == kModeAny && o.tab) ? ht_tab_off(a, di) : 0;
             for (int base = g0; base < g1; base += kGroup)
                 emit_group<MODE>(o, hs, base, di.hlo, e_run, r_run, pc, po, ht, toff);
             if ((MODE & kHt) || (MODE == kModeAny && o.tab)) {
@@ -984,7 +984,7 @@ __device__ __forceinline__ void block_segment(const K2Args &a, const OutPtrs<Out
         scr.ov = base + 5 * a.stage_cap;
         int pc_carry = 0, po_carry = 0, e_carry = 0, r_carry = 0;
         double ht = 0.0;
-        const long long ht_off = outp.tab ? ht_tab_off(a, d) : 0;
+        const long long ht_off = outp.tab ? ht_tab_off(a, di) : 0;
         for (int w = 0; w < nwin; ++w) {
             const int lo = w * win, wb = min(win, di.R - lo);
             fill_window<DP>(a, list, toff, n, di, lo, wb, cull, hs, sh.hit, &sh.nhit);
@@ -1110,7 +1110,7 @@ __device__ __forceinline__ void block_segment(const K2Args &a, const OutPtrs<Out
     long long pc_carry = sh.exc[0], po_carry = sh.exc[1];
     int e_carry = 0, r_carry = 0;
     double ht = 0.0;
-    const long long ht_off = outp.tab ? ht_tab_off(a, d) : 0;
+    const long long ht_off = outp.tab ? ht_tab_off(a, di) : 0;
     for (int w = 0; w < nwin; ++w) {
         const int lo = w * win, wb = min(win, di.R - lo);
         if (nwin > 1) {
