@@ -769,7 +769,7 @@ __global__ void __launch_bounds__(kWarpThreads, 5) k2w_emit(K2Args a, int rcap) 
 
 // Single-pass exclusive scan of (cnt_c, cnt_o) into the CSR offset arrays
 // (tiles of 8192 counts, decoupled look-back between the few tiles).
-constexpr int kScanThreads = 1024, kScanPer = 8, kScanTile = kScanThreads * kScanPer;
+constexpr int kScanThreads = 256, kScanPer = 8, kScanTile = kScanThreads * kScanPer;
 
 __global__ void __launch_bounds__(kScanThreads) k2_scan(K2Args a, const int *cnt_c, const int *cnt_o, long long S,
                                                        unsigned long long *flags) {
@@ -799,14 +799,17 @@ __global__ void __launch_bounds__(kScanThreads) k2_scan(K2Args a, const int *cnt
     if (lane == 31) { s_w[warp][0] = ic; s_w[warp][1] = io; }
     __syncthreads();
     if (warp == 0) {
-        long long wc = s_w[lane][0], wo = s_w[lane][1];
+        constexpr int W = kScanThreads / 32;
+        long long wc = lane < W ? s_w[lane][0] : 0, wo = lane < W ? s_w[lane][1] : 0;
         long long xc = wc, xo = wo;
         for (int d = 1; d < 32; d <<= 1) {
             long long x = __shfl_up_sync(0xffffffffu, xc, d), y = __shfl_up_sync(0xffffffffu, xo, d);
             if (lane >= d) { xc += x; xo += y; }
         }
-        s_w[lane][0] = xc - wc;
-        s_w[lane][1] = xo - wo;
+        if (lane < W) {
+            s_w[lane][0] = xc - wc;
+            s_w[lane][1] = xo - wo;
+        }
         const long long aggc = __shfl_sync(0xffffffffu, xc, 31), aggo = __shfl_sync(0xffffffffu, xo, 31);
         long long ec, eo;
         seg_lookback(flags, t, aggc, aggo, ec, eo);
