@@ -592,6 +592,23 @@ struct SparseRuns {
     bool emit_c, emit_o;
 };
 
+// Bitonic network over the first KMAX lanes (fully unrolled: every step a
+// compile-time shuffle distance and a per-lane min/max choice).
+template <int KMAX>
+__device__ __forceinline__ int bitonic_keys(int key) {
+    const int lane = threadIdx.x & 31;
+#pragma unroll
+    for (int k = 2; k <= KMAX; k <<= 1) {
+#pragma unroll
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            const int ok = __shfl_xor_sync(0xffffffffu, key, j);
+            const bool takemin = ((lane & j) == 0) == ((lane & k) == 0);
+            key = takemin ? min(key, ok) : max(key, ok);
+        }
+    }
+    return key;
+}
+
 template <typename RecT>
 __device__ __forceinline__ SparseRuns sparse_runs(const K2Args &a, long long b, const DirInfo &di, int n) {
     const int lane = threadIdx.x & 31;
@@ -603,17 +620,9 @@ __device__ __forceinline__ SparseRuns sparse_runs(const K2Args &a, long long b, 
     // <= 16 (8) records is sorted by the 16 (8)-lane network (the padding lanes
     // above it are already in order).
     int key = lane < n ? (h << 5) | lane : (0x7fffffe0 | lane);
-    const int kmax = n <= 8 ? 8 : n <= 16 ? 16 : 32;
-#pragma unroll
-    for (int k = 2; k <= 32; k <<= 1) {
-        if (k > kmax) break;
-#pragma unroll
-        for (int j = k >> 1; j > 0; j >>= 1) {
-            const int ok = __shfl_xor_sync(0xffffffffu, key, j);
-            const bool takemin = ((lane & j) == 0) == ((lane & k) == 0);
-            key = takemin ? min(key, ok) : max(key, ok);
-        }
-    }
+    if (n <= 8) key = bitonic_keys<8>(key);
+    else if (n <= 16) key = bitonic_keys<16>(key);
+    else key = bitonic_keys<32>(key);
     const int src = key & 31;
     const bool valid = key < 0x7fffffe0;
     SparseRuns r;
