@@ -115,6 +115,14 @@ eucalc_status eucalc_critical_export(const eucalc_critical *cr, int64_t image, i
  * of min(list length, height range R). Synchronises `stream` on first use. */
 eucalc_status eucalc_output_bound(const eucalc_critical *cr, const int32_t *dirs, int64_t D,
                                   int64_t *bound_ect, int64_t *bound_ordinary, void *stream);
+/* A looser bound that needs no K1 result and never synchronises: sum over
+ * (image, direction) of min(vertices, height range R) (a list holds at most one
+ * record per vertex). Any capacity >= eucalc_output_bound() is accepted by
+ * eucalc_transforms, so a caller can allocate with this bound while K1 still
+ * runs. dirs: host pointer (device pointers synchronise to read them).
+ * Errors: E_NONGENERIC, E_ARG. */
+eucalc_status eucalc_output_bound_upper(const eucalc_complex *cx, const int32_t *dirs, int64_t D,
+                                        int64_t *bound, void *stream);
 
 /* ---- exact transforms (Lemma 2) ----
  * For every (image, direction):

@@ -58,6 +58,7 @@ def lib():
         L.eucalc_critical_list_lengths.restype = St
         L.eucalc_critical_export.argtypes = [P, I64, I32, P, P, P, I64, ctypes.POINTER(I64), P]
         L.eucalc_output_bound.argtypes = [P, P, I64, ctypes.POINTER(I64), ctypes.POINTER(I64), P]
+        L.eucalc_output_bound_upper.argtypes = [P, P, I64, ctypes.POINTER(I64), P]
         SP = ctypes.POINTER(_Steps)
         L.eucalc_transforms.argtypes = [P, P, I64, SP, SP, SP, ctypes.POINTER(I64), P]
         L.eucalc_transforms_ht.argtypes = [P, P, I64, SP, SP, SP, I32, ctypes.c_double, I32, P,
@@ -81,7 +82,7 @@ def lib():
         L.eucalc_last_bad_index.restype = I64
         for f in ("eucalc_build_complex", "eucalc_destroy_complex", "eucalc_critical_points",
                   "eucalc_destroy_critical", "eucalc_critical_counts", "eucalc_critical_export",
-                  "eucalc_output_bound", "eucalc_transforms", "eucalc_ect", "eucalc_radon",
+                  "eucalc_output_bound", "eucalc_output_bound_upper", "eucalc_transforms", "eucalc_ect", "eucalc_radon",
                   "eucalc_hybrid", "eucalc_hybrid_ex", "eucalc_height_map", "eucalc_evaluate", "eucalc_transforms_ht",
                   "eucalc_transforms_real",
                   "eucalc_vectorize"):
@@ -291,8 +292,11 @@ def _alloc_all(torch, S, cap, elem_bytes, device, names, share, extra=None):
     return blk.views(), blk.sts
 
 
+_UPPER_MAX_BYTES = 8 << 30  # capacity="auto": the no-sync bound when its outputs fit this
+
+
 def transforms(cr: Critical, dirs, ect=True, ordinary=True, classical=True, elem_bytes=8, device="cuda",
-               share_heights=False, stream=None, ht=None):
+               share_heights=False, stream=None, ht=None, capacity="auto"):
     """eucalc_transforms: canonical ECT (T,E) and Radon (T_o,E'), (T_c,E_c) for every
     (image, direction), as CSR torch tensors on `device` ("cuda" or "cpu").
 
@@ -301,11 +305,16 @@ def transforms(cr: Critical, dirs, ect=True, ordinary=True, classical=True, elem
     share_heights=True lets the classical stream reuse the ECT heights (T_c = T,
     Lemma 6) instead of writing them twice; its "height" is then the ECT tensor.
     ht=(kernel, param, precision) also returns res["ht"] [batch, D], the hybrid
-    transform from the same merged histogram (eucalc_transforms_ht, NEXT f2)."""
+    transform from the same merged histogram (eucalc_transforms_ht, NEXT f2).
+    capacity: "tight" sizes the outputs by eucalc_output_bound (waits for K1's
+    list lengths); "upper" by eucalc_output_bound_upper (no wait: the allocation
+    overlaps K1, the library then waits inside the launch call); "auto" = upper
+    for device outputs of at most 8 GiB, else tight."""
     if elem_bytes == "auto":
         for eb in (2, 4):
             try:
-                return transforms(cr, dirs, ect, ordinary, classical, eb, device, share_heights, stream, ht)
+                return transforms(cr, dirs, ect, ordinary, classical, eb, device, share_heights, stream, ht,
+                                  capacity)
             except EucalcError as e:
                 if e.status != E_RANGE:
                     raise
@@ -317,10 +326,17 @@ def transforms(cr: Critical, dirs, ect=True, ordinary=True, classical=True, elem
     S = cr.cx.batch * D
     st = _stream(stream if stream is not None else cr.stream)
     p, keep = _ptr(d)
-    be, bo = ctypes.c_int64(), ctypes.c_int64()
-    _check(lib().eucalc_output_bound(cr._h, p, D, ctypes.byref(be), ctypes.byref(bo), st))
-    bound = be.value
     names = [n for n, want in (("ect", ect), ("ordinary", ordinary), ("classical", classical)) if want]
+    bound = None
+    if capacity in ("auto", "upper") and device != "cpu":
+        bu = ctypes.c_int64()
+        _check(lib().eucalc_output_bound_upper(cr.cx._h, p, D, ctypes.byref(bu), st))
+        if capacity == "upper" or bu.value * elem_bytes * 2 * len(names) <= _UPPER_MAX_BYTES:
+            bound = bu.value
+    if bound is None:
+        be, bo = ctypes.c_int64(), ctypes.c_int64()
+        _check(lib().eucalc_output_bound(cr._h, p, D, ctypes.byref(be), ctypes.byref(bo), st))
+        bound = be.value
     share = share_heights and ect and classical
     extra = None
     if ht is not None:  # the HT output shares the CSR allocation

@@ -943,6 +943,18 @@ eucalc_status eucalc_output_bound(const eucalc_critical *ccr, const int32_t *dir
     return EUCALC_OK;
 }
 
+eucalc_status eucalc_output_bound_upper(const eucalc_complex *cx, const int32_t *dirs, int64_t D, int64_t *bound,
+                                        void *stream) {
+    if (!cx || !bound) return fail(EUCALC_E_ARG, "NULL argument");
+    std::shared_ptr<PlanEntry> pe;
+    eucalc_status s = get_plan(cx, dirs, D, (cudaStream_t)stream, pe);
+    if (s != EUCALC_OK) return s;
+    int64_t b = 0;
+    for (const DirInfo &di : pe->p.info) b += std::min<int64_t>(cx->nvert, di.R);
+    *bound = b * cx->batch;
+    return EUCALC_OK;
+}
+
 }  // extern "C"
 
 namespace {
