@@ -372,6 +372,37 @@ def test_config2_binary_full_size_bench_launch():
         assert abs(float(ht[b, d]) - want) <= 1e-9 * max(abs(want), 1.0), (b, d)
 
 
+def test_capacity_upper_bound_matches_tight():
+    """eucalc_output_bound_upper (no K1 result needed) bounds eucalc_output_bound,
+    and outputs sized by either are identical."""
+    c = synth.config_inputs(2, "gray", small=True)
+    imgs, dirs = c["images"][:8], c["dirs"][:40]
+    cx = eu.build_complex(imgs, "vertex")
+    cr = eu.critical_points(cx)
+    bu = ctypes_bound_upper(cx, dirs)
+    bt = cr.output_bound(dirs)[0]
+    assert bu >= bt > 0
+    a = eu.transforms(cr, dirs, elem_bytes=2, share_heights=True, capacity="tight", ht=("sin", 1.0, "f64"))
+    b = eu.transforms(cr, dirs, elem_bytes=2, share_heights=True, capacity="upper", ht=("sin", 1.0, "f64"))
+    assert a["ect"]["value"].numel() == max(bt, 1) and b["ect"]["value"].numel() == max(bu, 1)
+    assert torch.equal(a["ht"], b["ht"])
+    for k in ("ect", "ordinary", "classical"):
+        n = int(a[k]["offsets"][-1])
+        assert torch.equal(a[k]["offsets"], b[k]["offsets"])
+        assert torch.equal(a[k]["value"][:n], b[k]["value"][:n])
+        assert torch.equal(a[k]["height"][:n], b[k]["height"][:n])
+
+
+def ctypes_bound_upper(cx, dirs):
+    import ctypes
+
+    d = np.ascontiguousarray(dirs, dtype=np.int32)
+    bu = ctypes.c_int64()
+    assert eu.lib().eucalc_output_bound_upper(cx._h, ctypes.c_void_p(d.ctypes.data), len(d), ctypes.byref(bu),
+                                              None) == 0
+    return bu.value
+
+
 def test_config3_sampled():
     c = synth.config_inputs(3)
     img, dirs = c["images"], c["dirs"][:64]
