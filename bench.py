@@ -325,7 +325,9 @@ def gpu_arm(args):
                          "peak_source": peak_src, "algorithmic_bytes_per_launch": k2_bytes,
                          "launch": "one step's K2 stage (2048 images)",
                          "launch_ms": k2_launch_ms},
-            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                    "step_ms_spread": {"min": 1e3 * float(np.min(e2e_t)), "median": 1e3 * float(np.median(e2e_t)),
+                                       "max": 1e3 * float(np.max(e2e_t))}},
             "gpu_launches": int(launches),
             "clocks": clk.summary(),
         }
