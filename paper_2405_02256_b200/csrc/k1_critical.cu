@@ -68,8 +68,7 @@ constexpr unsigned long long kAgg = 1ull << 62, kIncl = 2ull << 62, kValMask = (
 // consecutive tiles' flag words.
 __device__ long long lookback(unsigned long long *flag_t, int t, int stride, long long agg) {
     const int lane = threadIdx.x & 31;
-    if (lane == 0) st_relaxed(flag_t, kAgg | (unsigned long long)agg);
-    long long excl = 0;
+    long long excl = 0;  // the tile's aggregate is already published (k1_tile)
     int j = t - 1;
     while (true) {
         int idx = j - lane;
@@ -369,6 +368,10 @@ __device__ __forceinline__ void k1_tile(const K1Args &a, unsigned ticket, const 
         int tot = 0;
         for (int w = 0; w < kThreads / 32; ++w) tot += s_warp[w][tid];
         s_run[tid] = tot;
+        // publish this tile's aggregate now, before the statistics below, so that
+        // successors looking back find it sooner (tile 0 publishes its inclusive prefix)
+        unsigned long long *flag_t = a.flags + ((int64_t)b * tiles_per_img + t) * Q + tid;
+        st_relaxed(flag_t, (t == 0 ? kIncl : kAgg) | (unsigned long long)tot);
     }
 
     // ---- per-image statistics (order-independent integer sums: deterministic)
@@ -407,8 +410,7 @@ __device__ __forceinline__ void k1_tile(const K1Args &a, unsigned ticket, const 
         unsigned long long *flag_t = a.flags + ((int64_t)b * tiles_per_img + t) * Q + q;
         long long excl;
         if (t == 0) {
-            if (lane == 0) st_relaxed(flag_t, kIncl | (unsigned long long)agg);
-            excl = 0;
+            excl = 0;  // inclusive prefix published with the aggregate
         } else {
             excl = lookback(flag_t, t, Q, agg);
         }
