@@ -41,8 +41,14 @@ def build(force: bool = False, verbose: bool = False) -> str:
         return LIB
     os.makedirs(OBJ, exist_ok=True)
 
+    headers = glob.glob(os.path.join(CSRC, "*.cuh")) + [os.path.join(INCLUDE, "eucalc.h")]
+
     def compile_one(src):
         obj = os.path.join(OBJ, os.path.basename(src) + ".o")
+        if not force and os.path.exists(obj):  # object newer than its source and every header: reuse
+            t = os.path.getmtime(obj)
+            if all(os.path.getmtime(p) < t for p in [src, *headers]):
+                return obj, subprocess.CompletedProcess([], 0, "", "")
         r = subprocess.run([_nvcc(), *NVCC_FLAGS, "-I", INCLUDE, "-c", "-o", obj, src], capture_output=True, text=True)
         return obj, r
 

@@ -439,8 +439,10 @@ __device__ __forceinline__ void k1_tile(const K1Args &a, unsigned ticket, const 
     __syncthreads();  // staging, region and shared counters are reused by the next tile
 }
 
+// 3-D: at most 80 registers so that three CTAs fit per SM (the 8-bit region +
+// staging of a 16x16x8 tile is 72 KB, three fit in shared memory too)
 template <int N, int CONS, typename TIn, typename RecT>
-__global__ void __launch_bounds__(kThreads) k1_kernel(K1Args a) {
+__global__ void __launch_bounds__(kThreads, N == 3 ? 3 : 1) k1_kernel(K1Args a) {
     constexpr int Q = 1 << (N - 1);
     extern __shared__ __align__(16) unsigned char smem[];
     RecT *stage = reinterpret_cast<RecT *>(smem);           // [Q][kTileV]
