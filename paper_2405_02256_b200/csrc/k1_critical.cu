@@ -193,6 +193,46 @@ __device__ __forceinline__ void vertex_dminus(const R *s, int sz, int sy, int ba
     });
 }
 
+// ---- 3-D VERTEX, 8-bit region: a thread walks one z-column of the tile and
+// carries the planes it shares with the next vertex. The box mins and the
+// inclusion-exclusion above are separable (min and the per-axis difference
+// commute), and max(min(a,b),0) = min(max(a,0),max(b,0)), so per vertex only the
+// new plane z+1 is loaded, min-reduced in-plane and masked; the z pass combines
+// planes. In-plane values p[dy*3+dx], digit 0/1/2 <-> offset -1/0/+1.
+__device__ __forceinline__ void plane_min(const short *s, int sy, int pbase, int (&p)[9]) {
+#pragma unroll
+    for (int dy = 0; dy < 3; ++dy)
+#pragma unroll
+        for (int dx = 0; dx < 3; ++dx) p[dy * 3 + dx] = s[pbase + (dy - 1) * sy + (dx - 1)];
+#pragma unroll
+    for (int dx = 0; dx < 3; ++dx) {  // y pass: cells spanned by x and x + o_y
+        p[dx] = min(p[dx], p[3 + dx]);
+        p[6 + dx] = min(p[6 + dx], p[3 + dx]);
+    }
+#pragma unroll
+    for (int dy = 0; dy < 3; ++dy) {  // x pass
+        p[dy * 3] = min(p[dy * 3], p[dy * 3 + 1]);
+        p[dy * 3 + 2] = min(p[dy * 3 + 2], p[dy * 3 + 1]);
+    }
+#pragma unroll
+    for (int i = 0; i < 9; ++i) p[i] = max(p[i], 0);  // missing cell (sentinel) -> 0
+}
+// in-plane inclusion-exclusion, corner slots t[(dy>>1)*2 + (dx>>1)], dy, dx in {0,2}:
+// slot 2 <- mid - (offset -1), slot 0 <- mid - (offset +1), as in vertex_dminus
+__device__ __forceinline__ void plane_ie(const int (&p)[9], int (&t)[4]) {
+    int r[3][2];
+#pragma unroll
+    for (int dy = 0; dy < 3; ++dy) {
+        r[dy][1] = p[dy * 3 + 1] - p[dy * 3];
+        r[dy][0] = p[dy * 3 + 1] - p[dy * 3 + 2];
+    }
+#pragma unroll
+    for (int xs = 0; xs < 2; ++xs) {
+        t[2 + xs] = r[1][xs] - r[0][xs];
+        t[xs] = r[1][xs] - r[2][xs];
+    }
+}
+
 // Shared state of one tile (per CTA).
 template <int N>
 struct K1Shared {
@@ -306,11 +346,46 @@ __device__ __forceinline__ void k1_tile(const K1Args &a, unsigned ticket, const 
     // vertex index li = c0 + tid -> (lz, ly, lx), advanced incrementally by kThreads
     const int vz_ = kThreads / TP, v1 = kThreads - vz_ * TP, vy_ = v1 / TXe, vx_ = v1 - vy_ * TXe;
     int lz = tid / TP, lrem = tid - lz * TP, ly = lrem / TXe, lx = lrem - ly * TXe;
+    // full-plane tiles (TP == kThreads): vertex li + kThreads is the same (lx, ly) at lz + 1
+    constexpr bool kSlide = N == 3 && CONS == EUCALC_VERTEX && sizeof(RegT<TIn>) == 2;
+    const bool slide = kSlide && TP == kThreads;
+    int sl_pm[9], sl_tlow[4];  // plane lz (masked box mins); corners of min(plane lz-1, plane lz)
+    if constexpr (kSlide) {
+        if (slide) {
+            const int base0 = (lz + 1) * sz + (ly + 1) * sy + (lx + 1);
+            int pp[9];
+            plane_min(reinterpret_cast<const short *>(reg), sy, base0 - sz, pp);
+            plane_min(reinterpret_cast<const short *>(reg), sy, base0, sl_pm);
+#pragma unroll
+            for (int i = 0; i < 9; ++i) pp[i] = min(pp[i], sl_pm[i]);
+            plane_ie(pp, sl_tlow);
+        }
+    }
     for (int c0 = 0; c0 < TV; c0 += kThreads) {
         const int li = c0 + tid;
         const bool valid = li < TV;
         int dm[1 << N];
-        if (valid) {
+        if (kSlide && slide) {
+            if constexpr (kSlide) {
+                const int base = (lz + 1) * sz + (ly + 1) * sy + (lx + 1);
+                int pn[9], cu[9], tup[4], tmid[4];
+                plane_min(reinterpret_cast<const short *>(reg), sy, base + sz, pn);
+#pragma unroll
+                for (int i = 0; i < 9; ++i) cu[i] = min(sl_pm[i], pn[i]);  // cells spanning lz .. lz+1
+                plane_ie(cu, tup);
+                plane_ie(sl_pm, tmid);
+                // z pass: slot 2 (eps_z = +1, bit 0 of e) <- mid - low, slot 0 <- mid - up
+#pragma unroll
+                for (int e = 0; e < (1 << N); ++e) {
+                    const int i = ((e >> 1) & 1) * 2 + ((e >> 2) & 1);
+                    dm[e] = (e & 1) ? tmid[i] - sl_tlow[i] : tmid[i] - tup[i];
+                }
+#pragma unroll
+                for (int i = 0; i < 4; ++i) sl_tlow[i] = tup[i];
+#pragma unroll
+                for (int i = 0; i < 9; ++i) sl_pm[i] = pn[i];
+            }
+        } else if (valid) {
             const int base = ((N == 3) ? (lz + 1) * sz : 0) + (ly + 1) * sy + (lx + 1);
             vertex_dminus<N, CONS>(reg, sz, sy, base, dm);
         } else {

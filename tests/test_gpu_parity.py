@@ -418,6 +418,17 @@ def test_config4_sampled():
     check_transforms(img, dirs, "vertex", res, pairs=[(0, 0), (0, 31)])
 
 
+@pytest.mark.parametrize("construction", ["vertex", "top"])
+def test_k1_3d_full_and_ragged_tiles(construction):
+    """3-D K1 tables on a volume with full 16x16 xy tiles (VERTEX 8-bit: the z-column
+    walk that carries shared planes) and ragged ones (per-vertex stencil), both
+    binary and gray, against the oracle's star sums."""
+    vol = synth.smooth_volume(48, 91)[:37, :40, :48]
+    imgs = np.stack([vol, (vol > np.median(vol)).astype(np.uint8)])
+    _, cr, _ = run_gpu(imgs, synth.random_directions(2, 3, 5, 4), construction)
+    check_critical(imgs, construction, cr)
+
+
 def test_config5_sampled():
     c = synth.config_inputs(5)
     vols, dirs = c["images"][:2], c["dirs"]
