@@ -72,14 +72,22 @@ typedef struct eucalc_steps {
 
 /* ---- build (P:116 top-cell construction, P:140 dual/vertex construction) ----
  * img: `batch` same-shape images, C-order, dtype EUCALC_U8/I16/I32, host or
- * device. ndim 2 or 3; shape[ndim] >= 1. The image is copied (the caller may
- * free it after the call); the handle is library-owned (eucalc_destroy_complex).
- * Synchronises `stream` once (reads back max |weight|, used to pick record width).
+ * device. ndim 2 or 3; shape[ndim] >= 1. The image is copied: a HOST image may
+ * be freed or reused as soon as the call returns (from pinned memory the call
+ * waits for its copy); a DEVICE image must stay unchanged until the copy, which
+ * is enqueued on `stream`, has run. The handle is library-owned
+ * (eucalc_destroy_complex). EUCALC_U8: asynchronous for device images (|w| <= 255
+ * by type); I16/I32: synchronises `stream` once (reads back max |weight|, used to
+ * pick the record width).
  * Errors: E_ARG (dtype/ndim/shape/batch, packed vertex coords need > 32 bits),
  * E_NOMEM, E_CUDA. */
 eucalc_status eucalc_build_complex(const void *img, int dtype, int ndim, const int64_t *shape,
                                    int64_t batch, int construction, void *stream,
                                    eucalc_complex **out);
+/* Destroy calls free device memory stream-ordered on the stream the handle was
+ * created on, after the work that any other stream enqueued with the handle so
+ * far (the library records those streams). Every such stream must still exist
+ * when the handle is destroyed. */
 eucalc_status eucalc_destroy_complex(eucalc_complex *cx);
 
 /* ---- critical points ----
@@ -152,8 +160,10 @@ eucalc_status eucalc_transforms(const eucalc_critical *cr, const int32_t *dirs, 
  * sum with equal heights grouped, so one kbar (tabulated per lattice
  * u, E21) per distinct height instead of one per ordinary point. kernel, param,
  * precision and ht_out ([batch][D], host or device) as for eucalc_hybrid; the
- * ordinary stream must be requested. Deterministic (fixed-order sums). Errors
- * as for eucalc_transforms and eucalc_hybrid. */
+ * ordinary stream must be requested. Deterministic (fixed-order sums). When
+ * the kbar table would exceed 2^24 entries (unequal extents make L, hence the
+ * u range, large) the HT is computed by eucalc_hybrid after the transforms
+ * instead (same tolerance). Errors as for eucalc_transforms and eucalc_hybrid. */
 eucalc_status eucalc_transforms_ht(const eucalc_critical *cr, const int32_t *dirs, int64_t D,
                                    eucalc_steps *ect, eucalc_steps *ordinary, eucalc_steps *classical,
                                    int kernel, double param, int precision, void *ht_out,
@@ -168,8 +178,12 @@ eucalc_status eucalc_transforms_ht(const eucalc_critical *cr, const int32_t *dir
  * sort + merge) per (image, direction). Outputs as for
  * eucalc_transforms, with height[] double and value[] int64: elem_bytes must
  * be 8. Capacity: sum over (image, direction) of the list length (reported in
- * *required_out). Lists of up to 4096 records (E_ARG beyond). Host outputs
- * synchronise `stream`. */
+ * *required_out). Any list length: lists of <= 4096 records are sorted by one
+ * warp in shared memory; longer lists take a bucketed path (value buckets of
+ * ~128 records, each sorted by a warp or, when oversize, by a CTA, then merged
+ * with running sums), processed in chunks whose device scratch (32 B per record)
+ * stays within min(free memory / 4, 8 GiB); E_NOMEM if one segment alone does
+ * not fit. Host outputs synchronise `stream`. */
 eucalc_status eucalc_transforms_real(const eucalc_critical *cr, const double *dirs, int64_t D,
                                      eucalc_steps *ect, eucalc_steps *ordinary, eucalc_steps *classical,
                                      int64_t *required_out, void *stream);

@@ -92,6 +92,30 @@ bool is_device_ptr(const void *p) {
     return at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged;
 }
 
+// Page-locked host memory (cudaHostAlloc / cudaHostRegister): async copies from
+// it are still in flight when cudaMemcpyAsync returns.
+bool is_pinned_host_ptr(const void *p) {
+    if (!p) return false;
+    cudaPointerAttributes at;
+    if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return at.type == cudaMemoryTypeHost;
+}
+
+// Blocks until everything enqueued on `st` so far has completed (one event
+// record + wait; the rest of the stream keeps its asynchrony).
+cudaError_t wait_stream_point(cudaStream_t st) {
+    static thread_local cudaEvent_t ev = nullptr;
+    if (!ev) {
+        cudaError_t e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
+        if (e != cudaSuccess) return e;
+    }
+    cudaError_t e = cudaEventRecord(ev, st);
+    return e == cudaSuccess ? cudaEventSynchronize(ev) : e;
+}
+
 int num_sms() {
     static thread_local int n = 0;
     if (!n) {
@@ -157,6 +181,16 @@ bool arena_take(cudaStream_t st, const std::vector<size_t> &sizes, std::vector<v
         off += (b + 255) / 256 * 256;
     }
     return true;
+}
+
+// Releases (stream-ordered) an arena that one large call pushed past
+// kArenaKeep, so that memory is not held for the life of the stream.
+constexpr size_t kArenaKeep = size_t(256) << 20;
+void arena_trim(cudaStream_t st) {
+    auto it = g_arenas.find(st);
+    if (it == g_arenas.end() || it->second.cap <= kArenaKeep) return;
+    cudaFreeAsync(it->second.p, st);
+    g_arenas.erase(it);
 }
 
 int bits_for(int64_t v) {  // bits to hold 0..v
@@ -665,9 +699,14 @@ eucalc_status eucalc_build_complex(const void *img, int dtype, int ndim, const i
         delete cx;
         return cuda_fail(e, "cudaMallocAsync(image)");
     }
-    e = cudaMemcpyAsync(cx->d_img, img, bytes, is_device_ptr(img) ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st);
+    const bool dev_src = is_device_ptr(img);
+    e = cudaMemcpyAsync(cx->d_img, img, bytes, dev_src ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st);
     if (dtype == EUCALC_U8) {
-        // |w| <= 255 by type: no reduction, no host synchronisation
+        // |w| <= 255 by type: no reduction. A host source may be freed by the
+        // caller when this call returns (eucalc.h): from pageable memory the copy
+        // has consumed the buffer on return, from pinned memory it is still in
+        // flight, so wait for it (the stream's earlier work included).
+        if (e == cudaSuccess && !dev_src && is_pinned_host_ptr(img)) e = wait_stream_point(st);
         if (e != cudaSuccess) {
             cudaFreeAsync(cx->d_img, st);
             delete cx;
@@ -708,7 +747,9 @@ eucalc_status eucalc_build_complex(const void *img, int dtype, int ndim, const i
 
 eucalc_status eucalc_destroy_complex(eucalc_complex *cx) {
     if (!cx) return fail(EUCALC_E_STATE, "NULL handle");
-    // stream-ordered release on the stream the handle was built on (no device sync)
+    // stream-ordered release on the stream the handle was built on (no device
+    // sync), after the work other streams enqueued on it
+    cx->users.join(cx->owner_stream);
     if (cx->d_img) cudaFreeAsync(cx->d_img, cx->owner_stream);
     delete cx;
     return EUCALC_OK;
@@ -719,6 +760,7 @@ eucalc_status eucalc_critical_points(const eucalc_complex *cx, void *stream, euc
     *out = nullptr;
     if (!cx || !cx->d_img) return fail(EUCALC_E_STATE, "invalid complex");
     cudaStream_t st = (cudaStream_t)stream;
+    const_cast<eucalc_complex *>(cx)->users.note(st, cx->owner_stream);
     eucalc_critical *cr = new (std::nothrow) eucalc_critical();
     if (!cr) return fail(EUCALC_E_NOMEM, "host alloc");
     const int n = cx->ndim;
@@ -839,6 +881,7 @@ eucalc_status eucalc_critical_points(const eucalc_complex *cx, void *stream, euc
 
 eucalc_status eucalc_destroy_critical(eucalc_critical *cr) {
     if (!cr) return fail(EUCALC_E_STATE, "NULL handle");
+    cr->users.join(cr->owner_stream);
     cudaFreeAsync(cr->d_rec, cr->owner_stream);
     cudaFreeAsync(cr->d_count, cr->owner_stream);
     cudaFreeAsync(cr->d_tile_off, cr->owner_stream);
@@ -958,6 +1001,8 @@ eucalc_status eucalc_output_bound_upper(const eucalc_complex *cx, const int32_t 
 }  // extern "C"
 
 namespace {
+constexpr int64_t kFusedTabMax = int64_t(1) << 24;  // kbar entries of the fused HT table (128 MB)
+
 struct HtReq {
     int kernel, precision;
     double param;
@@ -979,10 +1024,26 @@ eucalc_status transforms_impl(const eucalc_critical *ccr, const int32_t *dirs, i
     eucalc_critical *cr = const_cast<eucalc_critical *>(ccr);
     const Complex *cx = cr->cx;
     cudaStream_t st = (cudaStream_t)stream;
+    cr->users.note(st, cr->owner_stream);
     std::shared_ptr<PlanEntry> pe;
     eucalc_status s = get_plan(cx, dirs, D, st, pe);
     if (s != EUCALC_OK) return s;
     const DirPlan &p = pe->p;
+    if (ht) {
+        // the fused HT tabulates kbar over the directions' whole u range (8 B per
+        // u); beyond kFusedTabMax entries (unequal extents make L, hence U, large)
+        // the transforms run unfused and the HT comes from K3, which evaluates
+        // kbar per term when its table does not apply (same tolerance, E18).
+        // EUCALC_FUSED_TAB_MAX overrides the limit (test hook).
+        int64_t tab_max = kFusedTabMax;
+        if (const char *v = getenv("EUCALC_FUSED_TAB_MAX")) tab_max = std::max<int64_t>(1, atoll(v));
+        if (p.U1 - p.U0 + 1 > tab_max) {
+            s = transforms_impl(ccr, dirs, D, ect, ordinary, classical, nullptr, required_out, stream);
+            if (s != EUCALC_OK) return s;
+            return eucalc_hybrid_ex(ccr, dirs, D, ht->kernel, ht->param, ht->precision, EUCALC_HT_AUTO, ht->out,
+                                    stream);
+        }
+    }
     int64_t bnd = 0;
     s = bounds(cr, p, st, bnd);
     if (s != EUCALC_OK) return s;
@@ -1008,7 +1069,10 @@ eucalc_status transforms_impl(const eucalc_critical *ccr, const int32_t *dirs, i
     }
     const int64_t S = cx->batch * D;
     if (S == 0) return EUCALC_OK;
-    if (S >= (int64_t(1) << 31)) return fail(EUCALC_E_RANGE, "more than 2^31 (image, direction) segments in one call");
+    // the warp-regime loops step int32 segment indices by the grid's warp count
+    // (< 2^24): keep s + step below 2^31
+    if (S > INT32_MAX - (int64_t(1) << 24))
+        return fail(EUCALC_E_RANGE, "more than 2^31 - 2^24 (image, direction) segments in one call");
     const bool cls_alias = classical && ect && (classical->height == ect->height || !classical->height);
     if (classical && !classical->height && !ect) return fail(EUCALC_E_ARG, "classical height is NULL");
     // host outputs -> device scratch
@@ -1156,6 +1220,7 @@ eucalc_status transforms_impl(const eucalc_critical *ccr, const int32_t *dirs, i
     }
     if (e == cudaSuccess && ht_host) e = cudaMemcpyAsync(ht->out, d_ht, ht_osz * S, cudaMemcpyDeviceToHost, st);
     free_scratch();
+    arena_trim(st);
     if (e == cudaSuccess && (host_out || ht_host)) e = cudaStreamSynchronize(st);
     if (e != cudaSuccess) return cuda_fail(e, "transforms");
     return EUCALC_OK;
@@ -1186,6 +1251,7 @@ eucalc_status eucalc_transforms_real(const eucalc_critical *ccr, const double *d
     const Complex *cx = cr->cx;
     const int n = cx->ndim, full = (1 << n) - 1;
     cudaStream_t st = (cudaStream_t)stream;
+    cr->users.note(st, cr->owner_stream);
     if (D < 0) return fail(EUCALC_E_ARG, "D < 0");
     if (D > 0 && !dirs) return fail(EUCALC_E_ARG, "dirs is NULL");
     std::vector<double> h((size_t)D * n);
@@ -1236,7 +1302,10 @@ eucalc_status eucalc_transforms_real(const eucalc_critical *ccr, const double *d
     if (cr->max_abs_sum >= (int64_t(1) << 31)) return fail(EUCALC_E_RANGE, "total |weight| of a critical list exceeds 2^31");
     const int64_t S = cx->batch * D;
     if (S == 0) return EUCALC_OK;
-    if (S >= (int64_t(1) << 31)) return fail(EUCALC_E_RANGE, "more than 2^31 (image, direction) segments in one call");
+    // the warp-regime loops step int32 segment indices by the grid's warp count
+    // (< 2^24): keep s + step below 2^31
+    if (S > INT32_MAX - (int64_t(1) << 24))
+        return fail(EUCALC_E_RANGE, "more than 2^31 - 2^24 (image, direction) segments in one call");
     const bool cls_alias = classical && ect && (classical->height == ect->height || !classical->height);
     if (classical && !classical->height && !ect) return fail(EUCALC_E_ARG, "classical height is NULL");
     bool host_out = false;
@@ -1474,6 +1543,7 @@ eucalc_status eucalc_hybrid_ex(const eucalc_critical *ccr, const int32_t *dirs, 
     eucalc_critical *cr = const_cast<eucalc_critical *>(ccr);
     const Complex *cx = cr->cx;
     cudaStream_t st = (cudaStream_t)stream;
+    cr->users.note(st, cr->owner_stream);
     std::shared_ptr<PlanEntry> pe;
     eucalc_status s = get_plan(cx, dirs, D, st, pe);
     if (s != EUCALC_OK) return s;
@@ -1559,6 +1629,7 @@ eucalc_status eucalc_hybrid_ex(const eucalc_critical *ccr, const int32_t *dirs, 
     }
     if (e == cudaSuccess && host_out) e = cudaMemcpyAsync(out, d_out, osz * cx->batch * D, cudaMemcpyDeviceToHost, st);
     free_scratch();
+    arena_trim(st);
     if (e == cudaSuccess && host_out) e = cudaStreamSynchronize(st);
     if (e != cudaSuccess) return cuda_fail(e, "hybrid");
     return EUCALC_OK;

@@ -4,8 +4,10 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <algorithm>
 #include <mutex>
 #include <string>
+#include <vector>
 
 #include "../../include/eucalc.h"
 
@@ -25,6 +27,30 @@ struct Rec32 {
 };
 
 // ---- host-side handles -----------------------------------------------------
+// Streams other than the owner stream that enqueued work reading a handle's
+// device memory: the destroy call orders its stream-ordered frees after them.
+struct StreamSet {
+    std::mutex mu;
+    std::vector<cudaStream_t> v;
+    void note(cudaStream_t s, cudaStream_t owner) {
+        if (s == owner) return;
+        std::lock_guard<std::mutex> lk(mu);
+        if (std::find(v.begin(), v.end(), s) == v.end()) v.push_back(s);
+    }
+    // makes `owner` wait for the work enqueued so far on every noted stream
+    void join(cudaStream_t owner) {
+        std::lock_guard<std::mutex> lk(mu);
+        for (cudaStream_t s : v) {
+            cudaEvent_t e;
+            if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) continue;
+            if (cudaEventRecord(e, s) == cudaSuccess) cudaStreamWaitEvent(owner, e, 0);
+            cudaEventDestroy(e);
+        }
+        cudaGetLastError();
+        v.clear();
+    }
+};
+
 struct Complex {
     int ndim = 0, dtype = 0, construction = 0;
     int64_t batch = 0;
@@ -39,6 +65,7 @@ struct Complex {
     int64_t L = 1;                 // lcm of (M_i - 1) > 0
     int64_t scale[kMaxN] = {0, 0, 0};
     cudaStream_t owner_stream = nullptr;
+    StreamSet users;
 };
 
 struct Critical {
@@ -62,6 +89,7 @@ struct Critical {
     uint64_t bound_plan = 0;  // eucalc_output_bound cache: direction plan id -> bound
     int64_t bound_val = 0;
     cudaStream_t owner_stream = nullptr;
+    StreamSet users;
     cudaEvent_t k1_done = nullptr;  // after the async read-back of counts/stats
     void *pinned = nullptr;         // pinned host copy: int32 counts, then int64 stats
     size_t pinned_bytes = 0, pinned_stats_off = 0;
