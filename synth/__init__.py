@@ -55,6 +55,17 @@ def fibonacci_directions(count: int, scale: float) -> np.ndarray:
     return rounded.astype(np.int32), int(zero.any(axis=1).sum())
 
 
+def fibonacci_zero_fixed(count: int, scale: float) -> np.ndarray:
+    """bool [count]: the directions of ``fibonacci_directions(count, scale)`` that
+    had a component rounded to 0 and fixed to +-1 (E12)."""
+    i = np.arange(count, dtype=np.float64)
+    z = 1.0 - (2.0 * i + 1.0) / count
+    r = np.sqrt(np.maximum(0.0, 1.0 - z * z))
+    phi = i * math.pi * (3.0 - math.sqrt(5.0))
+    v = np.stack([r * np.cos(phi), r * np.sin(phi), z], axis=1) * scale
+    return (np.floor(np.abs(v) + 0.5) == 0).any(axis=1)
+
+
 # --------------------------------------------------------------------------- images
 
 def uniform_image(shape, levels: int, seed: int, dtype=np.uint8) -> np.ndarray:

@@ -4,6 +4,7 @@ logic of the binding."""
 import ctypes
 import os
 import re
+import subprocess
 
 import numpy as np
 import pytest
@@ -103,3 +104,23 @@ def _shard_worker(rank, world):
     pair = np.where((e >> 2) & 1, e ^ 7, e)
     assert np.all(np.diff(pair) >= 0)  # one orthant pair's directions stay together on a rank
     dist.destroy_process_group()
+
+
+def test_bench_entry_gloo_world2():
+    """bench.py's own multi-GPU entry (--gpus 2 re-launches itself under
+    torch.distributed.run) on CPU with gloo: two ranks rendezvous on 127.0.0.1,
+    each takes its shard, the time is the max over ranks and rank 0 alone prints
+    one JSON line with n_gpus = 2."""
+    import json
+    import sys
+
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--plumbing-check",
+                          "--steps", "2", "--warmup", "3"], capture_output=True, text=True, timeout=300, cwd=ROOT)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [l for l in out.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1, out.stdout
+    line = json.loads(lines[0])
+    assert line["n_gpus"] == 2 and line["plumbing_check"] and line["value"] > 0
+    shards = sorted(tuple(s) for s in line["shards"])
+    assert [s[0] for s in shards] == [0, 1] and shards[0][2] == shards[1][1] and shards[1][2] == 1024
+    assert shards[0][3] != shards[1][3]  # each rank draws its own images (weak scaling)
