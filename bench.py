@@ -179,6 +179,9 @@ class Clocks:
     def summary(self, name):
         a, b = self.regions.get(name, (0, len(self.samples)))
         s = self.samples[a:max(b, a + 1)]
+        if not s and self.samples:  # a region shorter than the 25 ms sampling period: nearest sample
+            i = min(a, len(self.samples) - 1)
+            s = self.samples[i:i + 1]
         if not s:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
         sm = [float(x[0]) for x in s if x[0].replace(".", "").isdigit()]

@@ -1556,7 +1556,7 @@ eucalc_status eucalc_hybrid_ex(const eucalc_critical *ccr, const int32_t *dirs, 
     // half table of one u-parity fits shared memory; else per-term evaluation
     const int64_t U = p.U1 - p.U0 + 1;
     const bool table_ok = p.dp != 0 && U < (int64_t(1) << 30) &&
-                          k3_table_smem(precision == EUCALC_F64, U) <= 200 * 1024;
+                          k3_table_smem(k3_mode(kernel, precision, cr->wide), U) <= 200 * 1024;
     if (algorithm == EUCALC_HT_TABLE && !table_ok)
         return fail(EUCALC_E_ARG, "tabulated HT needs byte-aligned coordinates, |xs| <= 127 and a table that fits shared memory");
     const bool use_table = algorithm == EUCALC_HT_TABLE || (algorithm == EUCALC_HT_AUTO && table_ok);

@@ -212,7 +212,8 @@ struct K3Args {
     float *tab32;
 };
 int k3_chunk(bool table);
-size_t k3_table_smem(bool f64, long long U);
+int k3_mode(int kernel, int precision, bool wide);
+size_t k3_table_smem(int mode, long long U);
 cudaError_t launch_k3(const K3Args &a, cudaStream_t s);
 // kbar table for u in [U0, U0 + U) in fp64, parity-split (even u - U0 first, then
 // odd; K2's fused HT), with an optional fp32 copy in natural order; and the HT

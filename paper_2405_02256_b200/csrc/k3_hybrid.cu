@@ -10,11 +10,14 @@
 // Work decomposition: directions are grouped by orthant on the host (Lemma 3,
 // same sign vector -> same critical list) into tiles of <= 512; a CTA
 // owns (image, tile, chunk of kChunk records) with one direction per thread in
-// registers and the chunk staged in shared memory (broadcast reads). Per term:
-// 3 FMA for the height, 1 FMA for the kernel argument, kbar (erf / sinpi /
-// cos / exp on the FMA + MUFU pipes), 1 FMUL and a compensated (Kahan) fp32
-// add — or the same in fp64. Chunk partials are combined in a fixed order by
-// a second kernel, so results are bit-identical run to run.
+// registers and the chunk staged in shared memory (broadcast reads). Per term
+// (k3_f64, the per-term "direct" algorithm): the exact integer height, kbar
+// (erf / sinpi with exact integer period reduction / cos / exp) and one FMA,
+// all in fp64 for both output precisions: an fp32 kbar rounds every term by up
+// to an ulp, and on ill-conditioned directions (sum |J kbar| / |HT| up to 1e7
+// in config 5) that alone exceeds the fp32 tolerance (measured 7e-4 absolute).
+// Chunk partials are combined in a fixed order by a second kernel, so results
+// are bit-identical run to run.
 #include <cmath>
 #include <type_traits>
 
@@ -32,100 +35,6 @@ __device__ __forceinline__ void rec_coords(const RecT &r, const K3Args &a, int &
     p0 = (int)((r.c >> a.sh[0]) & a.msk[0]);
     p1 = (int)((r.c >> a.sh[1]) & a.msk[1]);
     p2 = (a.ndim == 3) ? (int)((r.c >> a.sh[2]) & a.msk[2]) : 0;
-}
-
-struct Kahan32 {
-    float s = 0.f, c = 0.f;
-    __device__ __forceinline__ void add(float x) {
-        float y = x - c;
-        float t = s + y;
-        c = (t - s) - y;
-        s = t;
-    }
-};
-
-template <typename RecT>
-__global__ void __launch_bounds__(kThreads) k3_f32(K3Args a) {
-    __shared__ float4 sm[kStage];
-    const int c = blockIdx.x, tile = blockIdx.y;
-    const long long b = blockIdx.z;
-    const int tlen = a.tile_len[tile];
-    const int myd = threadIdx.x < tlen ? a.order[a.tile_start[tile] + threadIdx.x]
-                                       : a.order[a.tile_start[tile]];
-    const DirInfo di = a.dirs[myd];
-    const int d0 = a.order[a.tile_start[tile]];
-    const DirInfo di0 = a.dirs[d0];  // orthant shared by the tile
-    const int n = a.count[b * a.Q + di0.q];
-    const RecT *list = reinterpret_cast<const RecT *>(a.rec) + (b * a.Q + di0.q) * a.vcap;
-    const int beg = c * a.chunk, end = min(n, beg + a.chunk);
-    // per-direction constants
-    const float x0 = (float)di.xs[0], x1 = (float)di.xs[1], x2 = (a.ndim == 3) ? (float)di.xs[2] : 0.f;
-    const double L = (double)a.L;
-    const double cs = (double)a.csum[myd];
-    float c1 = 0.f, c0 = 0.f;
-    float per = 0.f, inv_per = 0.f, inv_half = 0.f;
-    bool int_period = false;
-    if (a.kernel == EUCALC_K_GAUSS) {
-        const double k = 1.0 / (a.param * sqrt(2.0));
-        c1 = (float)(k / L);
-        c0 = (float)(-0.5 * cs * k);
-    } else if (a.kernel == EUCALC_K_COS) {
-        // sin(2 pi t / P) = sinpi(u / (L P)), u = 2H - L csum; period of u is 2LP
-        const double lp = L * a.param;
-        int_period = (a.param == rint(a.param)) && lp < 4.0e6;
-        per = (float)(2.0 * lp);
-        inv_per = (float)(1.0 / (2.0 * lp));
-        inv_half = (float)(1.0 / lp);
-        c0 = (float)(-L * cs);  // u = 2h + c0 (exact integer in fp32)
-        c1 = (float)(2.0 * M_PI / a.param / (2.0 * L));  // fallback: angle = u * c1
-    } else {
-        c1 = (float)(1.0 / L);
-        c0 = (float)(-0.5 * cs);
-    }
-    Kahan32 acc0, acc1;
-    const int sw = di.swap;
-    for (int s0 = beg; s0 < end; s0 += kStage) {
-        const int cnt = min(kStage, end - s0);
-        __syncthreads();
-        for (int i = threadIdx.x; i < cnt; i += blockDim.x) {
-            const RecT r = list[s0 + i];
-            int p0, p1, p2;
-            rec_coords(r, a, p0, p1, p2);
-            const int j = sw ? (r.b - r.a) : (r.a - r.b);
-            sm[i] = make_float4((float)p0, (float)p1, (float)p2, (float)j);
-        }
-        __syncthreads();
-        if (threadIdx.x < tlen) {
-#pragma unroll 2
-            for (int i = 0; i < cnt; ++i) {
-                const float4 r = sm[i];
-                const float h = fmaf(r.x, x0, fmaf(r.y, x1, r.z * x2));  // exact integer
-                float kb;
-                if (a.kernel == EUCALC_K_GAUSS) {
-                    kb = erff(fmaf(h, c1, c0));
-                } else if (a.kernel == EUCALC_K_COS) {
-                    const float u = fmaf(2.f, h, c0);
-                    if (int_period) {
-                        const float q = rintf(u * inv_per);
-                        const float rr = fmaf(-q, per, u);  // exact: integers < 2^24
-                        kb = sinpif(rr * inv_half);
-                    } else {
-                        kb = sinf(u * c1);
-                    }
-                } else if (a.kernel == EUCALC_K_SIN) {
-                    kb = cosf(fmaf(h, c1, c0));
-                } else {
-                    kb = expf(fmaf(h, c1, c0));
-                }
-                if (i & 1) acc1.add(r.w * kb);
-                else acc0.add(r.w * kb);
-            }
-        }
-    }
-    if (threadIdx.x < tlen) {
-        const double tot = ((double)acc0.s - (double)acc0.c) + ((double)acc1.s - (double)acc1.c);
-        a.partial[(b * a.nchunks + c) * a.D + myd] = tot;
-    }
 }
 
 template <typename RecT>
@@ -213,15 +122,29 @@ __global__ void __launch_bounds__(kThreads) k3_f64(K3Args a) {
 //                     directions share the parity of L*csum, hence of u),
 //   acc += J * tab[idx].
 // The half table of the tile's parity sits in shared memory; per term the work
-// is an LDS broadcast of the record, a DP4A, an LDS gather and the compensated
-// (fp32) or fp64 accumulation — precision-independent kbar cost, no SFU.
+// is an LDS broadcast of the record, a DP4A, an LDS gather and the accumulation
+// — precision-independent kbar cost, no SFU. Table element and accumulation per
+// mode (K3Mode):
+//   kF64  : fp64 kbar, DFMA (fp64 output);
+//   kFix32: the bounded kernels' f = erf / sinpi / cos in [-1, 1] as 32-bit fixed
+//           point q = rint(f 2^30) (|error| <= 2^-31), J * q accumulated EXACTLY in
+//           int64 (IMAD.WIDE; |J q| < 2^47, <= 8192 terms per CTA): the fp32
+//           output path. The table's rounding errors are independent per lattice
+//           height, so the HT error is ~2^-31 sqrt(sum_h H_J(h)^2) — 1e-5 on the
+//           worst-conditioned config-5 directions, where fp32 kbar values
+//           (rounded by up to 2^-24) reach 1e-4 (E23);
+//   kF32  : fp32 kbar with Kahan-compensated fp32 accumulation (EXP, whose kbar is
+//           unbounded, and int32-weight records).
 constexpr int kChunkT = 8192;
+constexpr int kFixBits = 30;
+enum K3Mode { kF32 = 0, kF64 = 1, kFix32 = 2 };
 
 // split = 1 (fused HT in K2): t64 holds the even-offset entries (u - U0 even)
 // first, then the odd ones, so one direction's entries (fixed parity of u) are
-// contiguous in its heights; t32 may be NULL.
+// contiguous in its heights; t32 (natural order) may be NULL and holds float
+// values, or int32 fixed-point values when fix32 = 1.
 __global__ void k3_table(int kernel, double param, long long L, long long U0, long long U, double *t64, float *t32,
-                         int split = 0) {
+                         int split = 0, int fix32 = 0) {
     const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= U) return;
     const long long u = U0 + i;
@@ -244,7 +167,10 @@ __global__ void k3_table(int kernel, double param, long long L, long long U0, lo
         f = exp((double)u / (2.0 * (double)L));
     }
     t64[split ? ((i & 1) ? ((U + 1) >> 1) + (i >> 1) : (i >> 1)) : i] = f;
-    if (t32) t32[i] = (float)f;
+    if (t32) {
+        if (fix32) reinterpret_cast<int *>(t32)[i] = (int)rint(f * (double)(1 << kFixBits));
+        else t32[i] = (float)f;
+    }
 }
 
 template <int DP>
@@ -255,10 +181,12 @@ __device__ __forceinline__ int table_index(uint32_t c, int xs8, int off) {
     return r;
 }
 
-template <typename RecT, bool F64, int DP>
+template <typename RecT, int MODE, int DP>
 __global__ void __launch_bounds__(kThreads) k3t(K3Args a) {
-    using T = typename std::conditional<F64, double, float>::type;
-    using S = typename std::conditional<F64, int4, int2>::type;  // staged record: c, J (float bits / double)
+    constexpr bool F64 = MODE == kF64, FIX = MODE == kFix32;
+    using T = typename std::conditional<F64, double, typename std::conditional<FIX, int, float>::type>::type;
+    using S = typename std::conditional<F64, int4, int2>::type;  // staged record: c, J (int / float bits / double)
+    using Acc = typename std::conditional<F64, double, typename std::conditional<FIX, long long, float>::type>::type;
     constexpr int PER = F64 ? 2 : 4;                             // records staged per thread per chunk
     extern __shared__ __align__(16) unsigned char k3t_smem[];
     S *sbuf = reinterpret_cast<S *>(k3t_smem);  // two staging buffers of PER * blockDim records
@@ -305,13 +233,28 @@ __global__ void __launch_bounds__(kThreads) k3t(K3Args a) {
                 if constexpr (F64) {
                     const double jd = (double)j;
                     dst[li] = make_int4((int)pre[k].c, 0, __double2loint(jd), __double2hiint(jd));
+                } else if constexpr (FIX) {
+                    dst[li] = make_int2((int)pre[k].c, j);
                 } else {
                     dst[li] = make_int2((int)pre[k].c, __float_as_int((float)j));
                 }
             }
         }
     };
-    T acc0 = 0, acc1 = 0, cmp0 = 0, cmp1 = 0;
+    Acc acc0 = 0, acc1 = 0;
+    float cmp0 = 0.f, cmp1 = 0.f;  // Kahan compensation (kF32)
+    auto add = [&](Acc &acc, float &cmp, const S &r, T k) {
+        if constexpr (F64) {
+            acc = fma(__hiloint2double(r.w, r.z), k, acc);
+        } else if constexpr (FIX) {
+            acc += (long long)r.y * (long long)k;  // exact (IMAD.WIDE)
+        } else {
+            // Kahan-compensated fp32 (J * kbar formed inside the FMA)
+            const float y = fmaf(__int_as_float(r.y), k, -cmp), t = acc + y;
+            cmp = (t - acc) - y;
+            acc = t;
+        }
+    };
     if (beg < end) {
         load_chunk(beg);
         store_chunk(sbuf, beg);
@@ -324,7 +267,7 @@ __global__ void __launch_bounds__(kThreads) k3t(K3Args a) {
         if (nxt < end) load_chunk(nxt);  // in flight while this chunk is consumed
         const S *srec = sbuf + cur * PER * kThreads;
         if (threadIdx.x < tlen) {
-            // four independent record chains per iteration (LDS -> IDP -> LDS -> FMA)
+            // four independent record chains per iteration (LDS -> IDP -> LDS -> accumulate)
             int i = 0;
             for (; i + 3 < cnt; i += 4) {
                 S r[4];
@@ -345,28 +288,13 @@ __global__ void __launch_bounds__(kThreads) k3t(K3Args a) {
                 for (int u = 0; u < 4; ++u) k[u] = tab[table_index<DP>((uint32_t)r[u].x, di.xs8, off)];
 #pragma unroll
                 for (int u = 0; u < 4; ++u) {
-                    if constexpr (F64) {
-                        if (u & 1) acc1 = fma(__hiloint2double(r[u].w, r[u].z), k[u], acc1);
-                        else acc0 = fma(__hiloint2double(r[u].w, r[u].z), k[u], acc0);
-                    } else {
-                        // Kahan-compensated fp32 (J * kbar formed inside the FMA)
-                        float &acc = (u & 1) ? acc1 : acc0, &cmp = (u & 1) ? cmp1 : cmp0;
-                        const float y = fmaf(__int_as_float(r[u].y), k[u], -cmp), t = acc + y;
-                        cmp = (t - acc) - y;
-                        acc = t;
-                    }
+                    if (u & 1) add(acc1, cmp1, r[u], k[u]);
+                    else add(acc0, cmp0, r[u], k[u]);
                 }
             }
             for (; i < cnt; ++i) {
                 const S r0 = srec[i];
-                const T k0 = tab[table_index<DP>((uint32_t)r0.x, di.xs8, off)];
-                if constexpr (F64) {
-                    acc0 = fma(__hiloint2double(r0.w, r0.z), k0, acc0);
-                } else {
-                    const float y0 = fmaf(__int_as_float(r0.y), k0, -cmp0), t0 = acc0 + y0;
-                    cmp0 = (t0 - acc0) - y0;
-                    acc0 = t0;
-                }
+                add(acc0, cmp0, r0, tab[table_index<DP>((uint32_t)r0.x, di.xs8, off)]);
             }
         }
         if (nxt < end) store_chunk(sbuf + (cur ^ 1) * PER * kThreads, nxt);
@@ -376,6 +304,7 @@ __global__ void __launch_bounds__(kThreads) k3t(K3Args a) {
     if (threadIdx.x < tlen) {
         double tot;
         if constexpr (F64) tot = acc0 + acc1;
+        else if constexpr (FIX) tot = (double)(acc0 + acc1) * (1.0 / (double)(1 << kFixBits));
         else tot = ((double)acc0 - (double)cmp0) + ((double)acc1 - (double)cmp1);
         a.partial[(b * a.nchunks + c) * a.D + myd] = tot;
     }
@@ -397,15 +326,23 @@ __global__ void k3_combine(const K3Args a, double scale) {
 
 int k3_chunk(bool table) { return table ? kChunkT : kChunk; }
 
-size_t k3_table_smem(bool f64, long long U) {
+// Table mode of a K3 call: fp64 output -> kF64; fp32 output -> kFix32 for the
+// bounded kernels over 16-bit-weight records, else kF32.
+int k3_mode(int kernel, int precision, bool wide) {
+    if (precision == EUCALC_F64) return kF64;
+    return (kernel != EUCALC_K_EXP && !wide) ? kFix32 : kF32;
+}
+
+size_t k3_table_smem(int mode, long long U) {
     const long long half = (U + 1) / 2 + 1;
-    // two staging buffers of PER * kThreads records (PER = 2 in fp64, 4 in fp32)
-    return (f64 ? sizeof(int4) * 2 : sizeof(int2) * 4) * 2 * kThreads + (f64 ? 8 : 4) * half;
+    // two staging buffers of PER * kThreads records (PER = 2 in fp64, 4 otherwise)
+    return (mode == kF64 ? sizeof(int4) * 2 : sizeof(int2) * 4) * 2 * kThreads + (mode == kF64 ? 8 : 4) * half;
 }
 
 cudaError_t launch_k3_table(const K3Args &a, cudaStream_t s) {
     // kbar table over u in [U0, U0 + U)
-    k3_table<<<(unsigned)((a.U + 255) / 256), 256, 0, s>>>(a.kernel, a.param, a.L, a.U0, a.U, a.tab64, a.tab32);
+    k3_table<<<(unsigned)((a.U + 255) / 256), 256, 0, s>>>(a.kernel, a.param, a.L, a.U0, a.U, a.tab64, a.tab32, 0,
+                                                           k3_mode(a.kernel, a.precision, a.wide) == kFix32);
     count_launch();
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
@@ -434,23 +371,22 @@ cudaError_t launch_k3(const K3Args &a, cudaStream_t s) {
     if (a.use_table) {
         cudaError_t e = launch_k3_table(a, s);
         if (e != cudaSuccess) return e;
-        const bool f64 = a.precision == EUCALC_F64;
-        const size_t smem = k3_table_smem(f64, a.U);
+        const int mode = k3_mode(a.kernel, a.precision, a.wide);
+        const size_t smem = k3_table_smem(mode, a.U);
         void (*k)(K3Args) = nullptr;
         if (a.wide) {
-            if (f64) k = a.dp == 2 ? k3t<Rec32, true, 2> : k3t<Rec32, true, 3>;
-            else k = a.dp == 2 ? k3t<Rec32, false, 2> : k3t<Rec32, false, 3>;
+            if (mode == kF64) k = a.dp == 2 ? k3t<Rec32, kF64, 2> : k3t<Rec32, kF64, 3>;
+            else k = a.dp == 2 ? k3t<Rec32, kF32, 2> : k3t<Rec32, kF32, 3>;
         } else {
-            if (f64) k = a.dp == 2 ? k3t<Rec16, true, 2> : k3t<Rec16, true, 3>;
-            else k = a.dp == 2 ? k3t<Rec16, false, 2> : k3t<Rec16, false, 3>;
+            if (mode == kF64) k = a.dp == 2 ? k3t<Rec16, kF64, 2> : k3t<Rec16, kF64, 3>;
+            else if (mode == kFix32) k = a.dp == 2 ? k3t<Rec16, kFix32, 2> : k3t<Rec16, kFix32, 3>;
+            else k = a.dp == 2 ? k3t<Rec16, kF32, 2> : k3t<Rec16, kF32, 3>;
         }
         e = prepare_kernel((const void *)k, a.threads, smem, nullptr);
         if (e != cudaSuccess) return e;
         k<<<grid, a.threads, smem, s>>>(a);
-    } else if (a.precision == EUCALC_F32) {
-        if (a.wide) k3_f32<Rec32><<<grid, a.threads, 0, s>>>(a);
-        else k3_f32<Rec16><<<grid, a.threads, 0, s>>>(a);
     } else {
+        // per-term kbar in fp64 for both output precisions (see k3_f64)
         if (a.wide) k3_f64<Rec32><<<grid, a.threads, 0, s>>>(a);
         else k3_f64<Rec16><<<grid, a.threads, 0, s>>>(a);
     }
