@@ -18,7 +18,6 @@
 #include "eucalc_internal.cuh"
 
 namespace eucalc {
-int k1_tile_vertices();
 int k3_chunk();
 
 namespace {
@@ -559,6 +558,44 @@ void pinned_put(void *p, size_t cap) {
     g_pin_free.emplace(cap, p);
 }
 
+// K1 launch arguments of a critical handle (the count/emit passes at creation,
+// the per-orthant statistics on demand).
+K1Args k1_args(const Critical *cr) {
+    const Complex *cx = cr->cx;
+    const int n = cx->ndim;
+    K1Args a{};
+    a.img = cx->d_img;
+    a.dtype = cx->dtype;
+    a.construction = cx->construction;
+    a.ndim = n;
+    a.batch = cx->batch;
+    a.npix = cx->npix;
+    a.vcap = cr->vcap;
+    for (int k = 0; k < n; ++k) {
+        a.m[k] = (int)cx->m[k];
+        a.M[k] = (int)cx->M[k];
+        a.sh[k] = cx->sh[k];
+    }
+    int TX, TY, TZ, W;
+    k1_geometry(n, cx->M, &TX, &TY, &TZ, &W);
+    a.TX = cr->TX;
+    a.TY = cr->TY;
+    a.TZ = cr->TZ;
+    a.W = W;
+    a.tiles_x = cr->tiles_x;
+    a.tiles_y = cr->tiles_y;
+    a.tiles_z = cr->tiles_z;
+    a.rec = cr->d_rec;
+    a.wide = cr->wide;
+    a.count = cr->d_count;
+    a.tile_off = cr->d_tile_off;
+    a.stats = cr->d_stats;
+    a.abs_sum = cr->d_stats + cx->batch * (1 << n) * 2;
+    a.max_rec = a.abs_sum + cx->batch * cr->Q;
+    a.Q = cr->Q;
+    return a;
+}
+
 }  // namespace eucalc
 
 using namespace eucalc;
@@ -773,83 +810,52 @@ eucalc_status eucalc_critical_points(const eucalc_complex *cx, void *stream, euc
     const size_t rsz = cr->wide ? sizeof(Rec32) : sizeof(Rec16);
     const int64_t nlist = cx->batch * cr->Q;
     const int64_t nstats = cx->batch * (1 << n) * 2 + 2 * nlist;
-    // tile shape: the whole image when it fits one tile (list order = row-major
-    // vertex order), else boxes of <= TV vertices (64 x 32 in 2-D, 16 x 16 x 8 in
-    // 3-D) spanning narrow height bands, for K2's tile culling
-    const int TV = k1_tile_vertices();
+    // tiles (K2's culling unit and K1's offset granularity): boxes of TX x TY x TZ
+    // vertices, W pencils (warps) each (k1_critical.cu)
+    int TX, TY, TZ, W;
+    k1_geometry(n, cx->M, &TX, &TY, &TZ, &W);
     const int MX = (int)cx->M[n - 1], MY = (int)cx->M[n - 2], MZ = n == 3 ? (int)cx->M[0] : 1;
-    int TX, TY, TZ = 1;
-    if ((int64_t)MX * MY * MZ <= TV) {
-        TX = MX;
-        TY = MY;
-        TZ = MZ;
-    } else if (n == 2) {
-        TX = std::min(MX, 64);
-        TY = std::max(1, std::min(MY, TV / TX));
-    } else {
-        TX = std::min(MX, 16);
-        TY = std::min(MY, 16);
-        TZ = std::max(1, std::min(MZ, TV / (TX * TY)));
-    }
-    const int tiles_x = (MX + TX - 1) / TX, tiles_y = (MY + TY - 1) / TY;
-    const int tiles_z = n == 3 ? (MZ + TZ - 1) / TZ : 1;
     cr->TX = TX;
     cr->TY = TY;
     cr->TZ = TZ;
-    cr->tiles_x = tiles_x;
-    cr->tiles_y = tiles_y;
-    cr->tiles_z = tiles_z;
-    cr->ntiles = tiles_x * tiles_y * tiles_z;
-    const int64_t ntiles = cx->batch * (int64_t)tiles_x * tiles_y * tiles_z;
-    unsigned long long *flags = nullptr;
-    unsigned int *ticket = nullptr;
+    cr->tiles_x = (MX + TX - 1) / TX;
+    cr->tiles_y = (MY + TY - 1) / TY;
+    cr->tiles_z = n == 3 ? (MZ + TZ - 1) / TZ : 1;
+    cr->ntiles = cr->tiles_x * cr->tiles_y * cr->tiles_z;
+    const int64_t ncnt = nlist * (int64_t)cr->ntiles * W;
+    const int64_t nflags = k1_scan_chunks(nlist, cr->ntiles, W);
+    // K1 scratch: (tile, warp) counts, scan flags, scan ticket (one allocation, zeroed)
+    const size_t cnt_bytes = ((sizeof(int32_t) * ncnt + 15) / 16) * 16;
+    const size_t scratch_bytes = cnt_bytes + sizeof(unsigned long long) * nflags + 16;
+    int32_t *cnt = nullptr;
     cudaError_t e = cudaMallocAsync(&cr->d_rec, rsz * nlist * cr->vcap, st);
     if (e == cudaSuccess) e = cudaMallocAsync(&cr->d_count, sizeof(int32_t) * nlist, st);
     if (e == cudaSuccess) e = cudaMallocAsync(&cr->d_tile_off, sizeof(int32_t) * nlist * (cr->ntiles + 1), st);
     if (e == cudaSuccess) e = cudaMallocAsync(&cr->d_stats, sizeof(int64_t) * nstats, st);
-    if (e == cudaSuccess) e = cudaMallocAsync(&flags, sizeof(unsigned long long) * ntiles * cr->Q, st);
-    if (e == cudaSuccess) e = cudaMallocAsync(&ticket, sizeof(unsigned int), st);
+    // records in fixed-capacity (tile, warp) regions before the copy to the lists
+    const int cap_r = 32 * (n == 3 ? TZ : TY / W);
+    const int64_t scap = (int64_t)cr->ntiles * W * cap_r;
+    const bool direct = (int64_t)cr->ntiles * W == 1;
+    void *rscratch = nullptr;
+    if (e == cudaSuccess) e = cudaMallocAsync(&cnt, scratch_bytes, st);
+    if (e == cudaSuccess && !direct) e = cudaMallocAsync(&rscratch, rsz * nlist * scap, st);
     if (e == cudaSuccess) e = cudaMemsetAsync(cr->d_stats, 0, sizeof(int64_t) * nstats, st);
-    if (e == cudaSuccess) e = cudaMemsetAsync(flags, 0, sizeof(unsigned long long) * ntiles * cr->Q, st);
-    if (e == cudaSuccess) e = cudaMemsetAsync(ticket, 0, sizeof(unsigned int), st);
+    if (e == cudaSuccess) e = cudaMemsetAsync(cnt, 0, scratch_bytes, st);
     if (e == cudaSuccess) {
-        K1Args a{};
-        a.img = cx->d_img;
-        a.dtype = cx->dtype;
-        a.construction = cx->construction;
-        a.ndim = n;
-        a.batch = cx->batch;
-        a.npix = cx->npix;
-        a.vcap = cr->vcap;
-        for (int k = 0; k < n; ++k) {
-            a.m[k] = (int)cx->m[k];
-            a.M[k] = (int)cx->M[k];
-            a.sh[k] = cx->sh[k];
-        }
-        a.TX = TX;
-        a.TY = TY;
-        a.TZ = TZ;
-        a.tile_off = cr->d_tile_off;
-        // TMA-staged persistent K1: opt-in, measured no faster than the plain
-        // kernel (K1 is issue-bound, not load-bound)
-        a.use_tma = getenv("EUCALC_K1_TMA") ? 1 : 0;
-        a.tiles_x = tiles_x;
-        a.tiles_y = tiles_y;
-        a.tiles_z = tiles_z;
-        a.rec = cr->d_rec;
-        a.wide = cr->wide;
-        a.count = cr->d_count;
-        a.flags = flags;
-        a.ticket = ticket;
-        a.stats = cr->d_stats;
-        a.abs_sum = cr->d_stats + cx->batch * (1 << n) * 2;
-        a.max_rec = a.abs_sum + nlist;
+        K1Args a = k1_args(cr);
+        a.cnt = cnt;
+        a.flags = (unsigned long long *)((unsigned char *)cnt + cnt_bytes);
+        a.ticket = (unsigned int *)(a.flags + nflags);
+        a.scratch = rscratch;
+        a.scap = scap;
+        a.cap_r = cap_r;
+        a.direct = direct;
         {
             ProfScope ps("k1_critical", st);
             e = launch_k1(a, st);
         }
-        // asynchronous read-back of the list lengths and statistics into pinned
-        // memory; sync_counts() later waits on this event only
+        // asynchronous read-back of the list lengths and |Delta^-| statistics into
+        // pinned memory; sync_counts() later waits on this event only
         cr->pinned_stats_off = ((sizeof(int32_t) * nlist + 15) / 16) * 16;
         const size_t need = cr->pinned_stats_off + sizeof(int64_t) * nstats;
         cr->pinned = pinned_get(need, &cr->pinned_bytes);
@@ -862,8 +868,8 @@ eucalc_status eucalc_critical_points(const eucalc_complex *cx, void *stream, euc
                                 sizeof(int64_t) * nstats, cudaMemcpyDeviceToHost, st);
         if (e == cudaSuccess) e = cudaEventRecord(cr->k1_done, st);
     }
-    if (flags) cudaFreeAsync(flags, st);
-    if (ticket) cudaFreeAsync(ticket, st);
+    if (cnt) cudaFreeAsync(cnt, st);
+    if (rscratch) cudaFreeAsync(rscratch, st);
     if (e != cudaSuccess) {
         if (cr->d_rec) cudaFreeAsync(cr->d_rec, st);
         if (cr->d_count) cudaFreeAsync(cr->d_count, st);
@@ -900,9 +906,20 @@ eucalc_status eucalc_destroy_critical(eucalc_critical *cr) {
 eucalc_status eucalc_critical_counts(const eucalc_critical *ccr, int64_t *h_counts, void *stream) {
     if (!ccr || !h_counts) return fail(EUCALC_E_ARG, "NULL argument");
     eucalc_critical *cr = const_cast<eucalc_critical *>(ccr);
-    eucalc_status s = sync_counts(cr, (cudaStream_t)stream);
+    cudaStream_t st = (cudaStream_t)stream;
+    eucalc_status s = sync_counts(cr, st);
     if (s != EUCALC_OK) return s;
-    memcpy(h_counts, cr->h_stats, sizeof(int64_t) * cr->cx->batch * (1 << cr->cx->ndim) * 2);
+    const size_t nb = sizeof(int64_t) * cr->cx->batch * (1 << cr->cx->ndim) * 2;
+    std::lock_guard<std::mutex> lk(cr->mu);
+    if (!cr->have_orthant_counts) {
+        // N^-, N^ord per orthant: the K1 stencil once more, counting only
+        cr->users.note(st, cr->owner_stream);
+        CK(launch_k1_stats(k1_args(cr), st));
+        CK(cudaMemcpyAsync(cr->h_stats, cr->d_stats, nb, cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        cr->have_orthant_counts = true;
+    }
+    memcpy(h_counts, cr->h_stats, nb);
     return EUCALC_OK;
 }
 

@@ -91,6 +91,7 @@ struct Critical {
     cudaStream_t owner_stream = nullptr;
     StreamSet users;
     cudaEvent_t k1_done = nullptr;  // after the async read-back of counts/stats
+    bool have_orthant_counts = false;  // N^-, N^ord computed (eucalc_critical_counts)
     void *pinned = nullptr;         // pinned host copy: int32 counts, then int64 stats
     size_t pinned_bytes = 0, pinned_stats_off = 0;
 };
@@ -106,19 +107,30 @@ struct K1Args {
     int64_t batch, npix, vcap;
     int m[kMaxN], M[kMaxN];
     int TX, TY, TZ, tiles_x, tiles_y, tiles_z;
+    int W;              // warps (pencils) per tile: 8 in 3-D (one per row), 1 in 2-D
     int sh[kMaxN];
     void *rec;
     bool wide;
     int32_t *count;
     int32_t *tile_off;  // [batch][Q][ntiles+1] list offset of each tile (+ total)
-    unsigned long long *flags;
-    unsigned int *ticket;
-    int64_t *stats;
+    int32_t *cnt;       // [batch][Q][ntiles][W] kept counts -> (scan) offsets (zeroed)
+    void *scratch;      // [batch][Q][scap] records in fixed-capacity (tile, warp) regions
+    int64_t scap;       // scratch records per list = ntiles * W * cap_r
+    int cap_r;          // records per region = vertices of one (tile, warp)
+    int Q;
+    bool direct;        // one region per image: records go straight to the lists
+    unsigned long long *flags;  // [k1_scan_chunks] scan look-back flags (zeroed)
+    unsigned int *ticket;       // scan chunk ticket (zeroed)
+    int64_t *stats;     // [batch][2^n][2] N^-, N^ord (on demand: launch_k1_stats)
     int64_t *abs_sum;
     int64_t *max_rec;
-    int use_tma;  // TMA-staged persistent kernel when the image layout allows it
 };
+// K1 tile geometry for an image of ndim dims (vertex extents M).
+void k1_geometry(int ndim, const int64_t *M, int *TX, int *TY, int *TZ, int *W);
+// Look-back flags k1_scan needs for `lists` lists of ntiles * W counts.
+int64_t k1_scan_chunks(int64_t lists, int64_t ntiles, int W);
 cudaError_t launch_k1(const K1Args &a, cudaStream_t s);
+cudaError_t launch_k1_stats(const K1Args &a, cudaStream_t s);
 
 // Per-direction info for K2/K3 (host-computed, copied to device).
 struct DirInfo {

@@ -3,36 +3,48 @@
 // For every vertex x of every image and every sign vector eps:
 //   Delta^-(eps, x) = chi(phi | lwst(eps, x))
 // where the lower star is the set of cells at doubled coordinates 2x - delta o eps,
-// delta in {0,1}^n, restricted to existing cells (E16). One CTA owns a
-// tile of vertices (full rows when they fit, so lists come out in row-major
-// vertex order); the image tile plus a one-vertex halo is staged in shared
-// memory as int32 with a sentinel for out-of-range positions:
-//   VERTEX: phi(cell) = min of its vertices; out-of-range vertex = INT_MIN,
-//                   so a cell touching it has phi = INT_MIN = "does not exist".
+// delta in {0,1}^n, restricted to existing cells (E16):
+//   VERTEX: phi(cell) = min of its vertices; the cell exists iff all of
+//                   its vertices do (out-of-range vertex = lowest sentinel);
 //   TOP: phi(cell) = min over its top cofaces (pixels); out-of-range
-//                   pixel = INT_MAX, so a cell whose fixed pixel index is out of
-//                   range has phi = INT_MAX = "does not exist", while an in-range
-//                   face at the image border takes the min of its real cofaces.
-// Per vertex all 3^n star-cell values are formed in registers (separable mins),
-// masked to 0 where the cell does not exist, and the 2^n lower-star sums come
-// from an in-register inclusion-exclusion transform (38 adds in 3-D).
+//                   pixel = highest sentinel, so a cell whose fixed pixel index is
+//                   out of range does not exist while a border face keeps the min
+//                   of its real cofaces.
+// Per vertex the 3^n star values are box mins of the neighbourhood, masked to 0
+// where the cell does not exist, and the 2^n lower-star sums come from an
+// inclusion-exclusion transform along every axis.
 //
 // Compaction: per antipodal pair {eps, -eps} (eps the representative with
 // eps_{n-1} = -1) a vertex is kept iff Delta^-(eps) != 0 or Delta^-(-eps) != 0
 // (this covers the classical points of both orthants and every ordinary point,
-// since J(eps) = Delta^-(eps) - Delta^-(-eps)). Warp ballot/popc + block scan
-// give the in-tile order; a decoupled look-back over the image's tiles (dynamic
-// ticket order) gives each tile's global offset, so the list order is
-// deterministic (tile-major; within a tile by warp, vertex batch and lane) with
-// a single pass.
-// Tiles are boxes of <= kTileV vertices (the whole image when it fits; else
-// 64 x 32 in 2-D, 16 x 16 x 8 in 3-D), so a tile spans a narrow band of heights
-// in every direction; K1 records each tile's list offset for K2's culling.
-#include <cuda.h>
-#include <cudaTypedefs.h>
-
+// since J(eps) = Delta^-(eps) - Delta^-(-eps)).
+//
+// Work decomposition ("pencils"): one warp owns 32 consecutive vertices of the
+// fastest axis x (one per lane) and walks the slowest axis (z in 3-D, y in 2-D)
+// plane by plane, so the stencil is separable along the walk: each step loads
+// only the new plane's neighbourhood (each lane its own column, x +- 1 by warp
+// shuffles), and for VERTEX the box mins and the inclusion-exclusion of the two
+// planes it already saw are carried in registers. There is no shared memory and
+// no block barrier on the hot path.
+//
+// Deterministic order without a look-back or a second stencil pass:
+//   k1_pencil<EMIT>: each (tile, warp) writes its kept vertices, in walk order and
+//                    lane order (ballot prefix), into its own fixed-capacity region
+//                    of scratch lists (capacity = its vertex count, so no overflow),
+//                    and its count per pair (+ sum and max of |Delta^-| over the
+//                    list, for the host's width choices);
+//   k1_scan         : per (image, pair) list, exclusive scan of the region counts in
+//                    (tile, warp) order -> each region's list offset, the per-tile
+//                    offsets K2 uses to cull tiles, and the list length;
+//   k1_copy         : every region's records to their offset (a memory copy).
+// Images that are a single region (2-D images of <= 32 x 64 vertices) are
+// written in place by k1_pencil alone.
+// Tiles (K2's culling unit) are boxes of 32 x 8 x 8 vertices in 3-D (8 warps =
+// 8 rows, each walking 8 planes) and 32 x 64 in 2-D (one warp walking 64 rows);
+// a list is ordered by tile (x fastest, then y, then z), then warp (row), then
+// walk step, then lane. The per-orthant counts N^-, N^ord are a third,
+// on-demand variant (k1_pencil<STATS>, eucalc_critical_counts).
 #include <algorithm>
-
 #include <climits>
 #include <type_traits>
 
@@ -41,57 +53,21 @@
 namespace eucalc {
 namespace {
 
-constexpr int kThreads = 256;
-constexpr int kTileV = 2048;  // vertices per tile (max)
-constexpr int kPerWarp = kTileV / (kThreads / 32);  // staging slice per warp
+constexpr int kWarps = 8, kThreads = 32 * kWarps;
+constexpr int kWalk3 = 64;  // planes walked by one warp in 3-D (8 tiles deep)
+// tile geometry (k1_geometry): 3-D 32 x 8 x 8 (8 warps = rows, 8 planes); 2-D 32 x 64,
+// walked by a.W warps of 64 / a.W rows each (W = 1 when the image is one tile: then
+// it is one region and its lists are written in place; else W = 4, so a 2-D image
+// offers 4 pencils per tile)
+template <int N> struct Tile;
+template <> struct Tile<3> { static constexpr int TY = 8, TZ = 8, W = 8, SEG = 8; };
+template <> struct Tile<2> { static constexpr int TY = 64, TZ = 1; };
+constexpr int kEmit = 0, kStats = 1;
 
 __host__ __device__ constexpr int pow3(int k) { return k == 0 ? 1 : 3 * pow3(k - 1); }
 
-template <typename T>
-__device__ __forceinline__ int load_img(const T *p, int64_t i) { return (int)__ldg(p + i); }
-
-__device__ __forceinline__ unsigned long long ld_relaxed(const unsigned long long *p) {
-    unsigned long long v;
-    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-    return v;
-}
-__device__ __forceinline__ void st_relaxed(unsigned long long *p, unsigned long long v) {
-    asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
-
-// Flag word for the tile look-back: status in bits 62..63 (1 = aggregate,
-// 2 = inclusive prefix), count in the low 62 bits.
-constexpr unsigned long long kAgg = 1ull << 62, kIncl = 2ull << 62, kValMask = (1ull << 62) - 1;
-
-// Warp-wide decoupled look-back. Returns the exclusive prefix of tile `t`
-// (t >= 1) given flags for tiles [0, t) of this (image, pair); `stride` between
-// consecutive tiles' flag words.
-__device__ long long lookback(unsigned long long *flag_t, int t, int stride, long long agg) {
-    const int lane = threadIdx.x & 31;
-    long long excl = 0;  // the tile's aggregate is already published (k1_tile)
-    int j = t - 1;
-    while (true) {
-        int idx = j - lane;
-        unsigned long long f = kIncl;  // virtual inclusive 0 before tile 0
-        if (idx >= 0) {
-            const unsigned long long *p = flag_t - (long long)(t - idx) * stride;
-            do { f = ld_relaxed(p); } while ((f >> 62) == 0);
-        }
-        unsigned incl = __ballot_sync(0xffffffffu, (f >> 62) == 2);
-        int first = incl ? __ffs(incl) - 1 : 31;
-        long long v = (lane <= first) ? (long long)(f & kValMask) : 0;
-        for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-        excl += v;
-        if (incl) break;
-        j -= 32;
-    }
-    if (lane == 0) st_relaxed(flag_t, kIncl | (unsigned long long)(excl + agg));
-    return excl;
-}
-
 // Compile-time loop: f(std::integral_constant<int, I>) for I in [B, E). Every
-// index below is a constant expression, so the 3^n star values stay in
-// registers (a runtime-indexed array would live in local memory).
+// index below is a constant expression, so the star values stay in registers.
 template <int B, int E, typename F>
 __device__ __forceinline__ void static_for(F &&f) {
     if constexpr (B < E) {
@@ -116,606 +92,699 @@ __host__ __device__ constexpr bool top_coface(int idx, int c) {
     return true;
 }
 
-// Staged region element: int16 for 8-bit images (the sentinels -32768 / 32767
-// lie outside 0..255: half the shared memory, more CTAs per SM), else int32.
-template <typename TIn>
-using RegT = std::conditional_t<sizeof(TIn) == 1, short, int>;
-template <typename R>
-__host__ __device__ constexpr int sent_lo() { return sizeof(R) == 2 ? -32768 : INT_MIN; }
-template <typename R>
-__host__ __device__ constexpr int sent_hi() { return sizeof(R) == 2 ? 32767 : INT_MAX; }
-
-template <int N, int CONS, typename R>
-__device__ __forceinline__ void vertex_dminus(const R *s, int sz, int sy, int base, int (&dm)[1 << N]) {
-    constexpr int P3 = pow3(N);
-    int val[P3];
-    auto stride = [&](int k) { return (k == N - 1) ? 1 : ((k == N - 2) ? sy : sz); };
-    if constexpr (CONS == EUCALC_VERTEX) {
-        // point values of the 3^n neighbourhood, then separable box mins: after
-        // axis k, val[o] = min over the vertices of the cell spanned by x and x+o
-        static_for<0, P3>([&](auto I) {
+// Inclusion-exclusion along every axis of a 3^M array of masked cell values:
+// slot +1 <- v(0) - v(-1) (eps_k = +1), slot -1 <- v(0) - v(+1) (eps_k = -1).
+// Corner (digits 0/2 per axis) then holds the lower-star sum of that sign vector.
+template <int M>
+__device__ __forceinline__ void incl_excl(int (&v)[pow3(M)]) {
+    static_for<0, M>([&](auto K) {
+        constexpr int k = decltype(K)::value, st = pow3(M - 1 - k);
+        static_for<0, pow3(M)>([&](auto I) {
             constexpr int idx = decltype(I)::value;
-            int off = 0;
-            static_for<0, N>([&](auto K) { off += (digit3<N>(idx, decltype(K)::value) - 1) * stride(decltype(K)::value); });
-            val[idx] = s[base + off];
-        });
-        static_for<0, N>([&](auto K) {
-            constexpr int k = decltype(K)::value, st = pow3(N - 1 - k);
-            static_for<0, P3>([&](auto I) {
-                constexpr int idx = decltype(I)::value, ok = digit3<N>(idx, k);
-                if constexpr (ok != 1) val[idx] = min(val[idx], val[idx + (1 - ok) * st]);
-            });
-        });
-        static_for<0, P3>([&](auto I) {
-            constexpr int idx = decltype(I)::value;
-            // 8-bit images (int16 region): weights >= 0 > sentinel, so one max masks
-            if constexpr (sizeof(R) == 2) val[idx] = max(val[idx], 0);
-            else val[idx] = (val[idx] == sent_lo<R>()) ? 0 : val[idx];
-        });
-    } else {
-        // 2^n pixels around the vertex (pixel x + c, c in {-1,0}^n); base <-> c = 0
-        constexpr int P2 = 1 << N;
-        int pix[P2];
-        static_for<0, P2>([&](auto C) {
-            constexpr int c = decltype(C)::value;
-            int off = 0;
-            static_for<0, N>([&](auto K) {
-                if constexpr (!((c >> decltype(K)::value) & 1)) off -= stride(decltype(K)::value);
-            });
-            pix[c] = s[base + off];
-        });
-        static_for<0, P3>([&](auto I) {
-            constexpr int idx = decltype(I)::value;
-            int mval = sent_hi<R>();
-            static_for<0, P2>([&](auto C) {
-                if constexpr (top_coface<N>(idx, decltype(C)::value)) mval = min(mval, pix[decltype(C)::value]);
-            });
-            val[idx] = (mval == sent_hi<R>()) ? 0 : mval;
-        });
-    }
-    // inclusion-exclusion: along axis k, slot +1 <- z(0) - z(-1) (eps_k=+1), slot -1 <- z(0) - z(+1)
-    static_for<0, N>([&](auto K) {
-        constexpr int k = decltype(K)::value, st = pow3(N - 1 - k);
-        static_for<0, P3>([&](auto I) {
-            constexpr int idx = decltype(I)::value;
-            if constexpr (digit3<N>(idx, k) == 1) {
-                const int a = val[idx - st], c = val[idx], b = val[idx + st];
-                val[idx + st] = c - a;
-                val[idx - st] = c - b;
+            if constexpr (digit3<M>(idx, k) == 1) {
+                const int a = v[idx - st], c = v[idx], b = v[idx + st];
+                v[idx + st] = c - a;
+                v[idx - st] = c - b;
             }
         });
     });
-    static_for<0, (1 << N)>([&](auto E) {
-        constexpr int e = decltype(E)::value;
-        constexpr int idx = (((e >> 0) & 1) ? 2 * pow3(N - 1) : 0) + (N > 1 && ((e >> 1) & 1) ? 2 * pow3(N - 2) : 0) +
-                            (N > 2 && ((e >> 2) & 1) ? 2 * pow3(N - 3 < 0 ? 0 : N - 3) : 0);
-        dm[e] = val[idx];
-    });
 }
 
-// ---- 3-D VERTEX, 8-bit region: a thread walks one z-column of the tile and
-// carries the planes it shares with the next vertex. The box mins and the
-// inclusion-exclusion above are separable (min and the per-axis difference
-// commute), and max(min(a,b),0) = min(max(a,0),max(b,0)), so per vertex only the
-// new plane z+1 is loaded, min-reduced in-plane and masked; the z pass combines
-// planes. In-plane values p[dy*3+dx], digit 0/1/2 <-> offset -1/0/+1.
-__device__ __forceinline__ void plane_min(const short *s, int sy, int pbase, int (&p)[9]) {
-#pragma unroll
-    for (int dy = 0; dy < 3; ++dy)
-#pragma unroll
-        for (int dx = 0; dx < 3; ++dx) p[dy * 3 + dx] = s[pbase + (dy - 1) * sy + (dx - 1)];
-#pragma unroll
-    for (int dx = 0; dx < 3; ++dx) {  // y pass: cells spanned by x and x + o_y
-        p[dx] = min(p[dx], p[3 + dx]);
-        p[6 + dx] = min(p[6 + dx], p[3 + dx]);
-    }
-#pragma unroll
-    for (int dy = 0; dy < 3; ++dy) {  // x pass
-        p[dy * 3] = min(p[dy * 3], p[dy * 3 + 1]);
-        p[dy * 3 + 2] = min(p[dy * 3 + 2], p[dy * 3 + 1]);
-    }
-#pragma unroll
-    for (int i = 0; i < 9; ++i) p[i] = max(p[i], 0);  // missing cell (sentinel) -> 0
-}
-// in-plane inclusion-exclusion, corner slots t[(dy>>1)*2 + (dx>>1)], dy, dx in {0,2}:
-// slot 2 <- mid - (offset -1), slot 0 <- mid - (offset +1), as in vertex_dminus
-__device__ __forceinline__ void plane_ie(const int (&p)[9], int (&t)[4]) {
-    int r[3][2];
-#pragma unroll
-    for (int dy = 0; dy < 3; ++dy) {
-        r[dy][1] = p[dy * 3 + 1] - p[dy * 3];
-        r[dy][0] = p[dy * 3 + 1] - p[dy * 3 + 2];
-    }
-#pragma unroll
-    for (int xs = 0; xs < 2; ++xs) {
-        t[2 + xs] = r[1][xs] - r[0][xs];
-        t[xs] = r[1][xs] - r[2][xs];
-    }
+// corner of a 3^M array for in-plane sign bits `bits` (bit j <-> in-plane axis j,
+// j = 0 the slowest): digit 2 where the bit is set, 0 where clear
+template <int M>
+__host__ __device__ constexpr int corner(int bits) {
+    int idx = 0;
+    for (int j = 0; j < M; ++j) idx += (((bits >> j) & 1) ? 2 : 0) * pow3(M - 1 - j);
+    return idx;
 }
 
-// Shared state of one tile (per CTA).
-template <int N>
-struct K1Shared {
-    int warp[kThreads / 32][1 << (N - 1)];
-    int run[1 << (N - 1)];
-    long long excl[1 << (N - 1)];
-    int ostat[1 << N][2];
+// Element type of the sentinel-carrying values: int16 suffices for 8-bit images.
+template <int CONS, typename TIn>
+struct Sent {
+    // VERTEX: lowest (a missing vertex makes the cell's min the sentinel);
+    // TOP: highest (a missing pixel drops out of the min)
+    static constexpr int value = CONS == EUCALC_VERTEX ? (sizeof(TIn) == 1 ? -1 : INT_MIN) : INT_MAX;
 };
 
-// One tile: stage the image region (from global memory, or from the raw TMA box
-// `raw` of xbox x ybox x zbox elements at image coordinates (x0-xoff, y0-1, z0-1),
-// xoff = 16 bytes of elements: TMA wants 16-byte aligned innermost box starts),
-// run the stencil, compact, look back, copy out. All threads of the CTA call it;
-// `sh.ostat` must be zero on entry (it is left zero on exit).
-template <int N, int CONS, typename TIn, typename RecT>
-__device__ __forceinline__ void k1_tile(const K1Args &a, unsigned ticket, const TIn *raw, int xbox, int ybox,
-                                        RecT *stage, RegT<TIn> *reg, K1Shared<N> &sh) {
-    constexpr int Q = 1 << (N - 1);
-    constexpr int FULL = (1 << N) - 1;
-    auto &s_warp = sh.warp;
-    auto &s_run = sh.run;
-    auto &s_excl = sh.excl;
-    auto &s_ostat = sh.ostat;
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int tiles_per_img = a.tiles_x * a.tiles_y * a.tiles_z;
-    const int64_t b = ticket / tiles_per_img;
-    const int t = ticket % tiles_per_img;
-    const int tx = t % a.tiles_x, ty = (t / a.tiles_x) % a.tiles_y, tz = t / (a.tiles_x * a.tiles_y);
+// Masked cell value: VERTEX 8-bit images hold values >= 0 > sentinel -1, so one
+// max masks (and commutes with min, so it can be applied before the walk's min);
+// otherwise compare with the sentinel.
+template <int CONS, typename TIn>
+__device__ __forceinline__ int mask_cell(int v) {
+    if constexpr (CONS == EUCALC_VERTEX && sizeof(TIn) == 1) return max(v, 0);
+    else return v == Sent<CONS, TIn>::value ? 0 : v;
+}
 
-    // vertex-lattice extents along (z, y, x) view; a tile is a TZ x TY x TX box of vertices
-    const int MX = a.M[N - 1];
-    const int MY = (N >= 2) ? a.M[N - 2] : 1;
-    const int MZ = (N == 3) ? a.M[0] : 1;
-    const int mX = a.m[N - 1];
-    const int mY = (N >= 2) ? a.m[N - 2] : 1;
-    const int mZ = (N == 3) ? a.m[0] : 1;
-    const int x0 = tx * a.TX, y0 = ty * a.TY, z0 = tz * a.TZ;
-    const int TXe = min(a.TX, MX - x0), TYe = min(a.TY, MY - y0), TZe = (N == 3) ? min(a.TZ, MZ - z0) : 1;
-    const int RX = TXe + 2, RY = TYe + 2, RZ = (N == 3) ? TZe + 2 : 1;
+struct Geo {
+    int MX, MY, MZ;  // vertex extents of the (x, y, z) view (MY = 1 in 1-D, MZ = 1 in 2-D)
+    int mX, mY, mZ;  // pixel extents
+};
 
-    // ---- stage the input region (image index = vertex idx for VERTEX, pixel idx
-    // for TOP) with a one-voxel halo: planes z0-1 .. z0+TZe, rows y0-1 .. y0+TYe,
-    // cols x0-1 .. x0+TXe; one warp per region row, lanes along the row
-    const TIn *img = reinterpret_cast<const TIn *>(a.img) + b * a.npix;
-    const int SENT = (CONS == EUCALC_VERTEX) ? sent_lo<RegT<TIn>>() : sent_hi<RegT<TIn>>();
-    if (raw) {  // TMA box already in shared memory (out-of-range elements zero-filled)
-        for (int row = warp; row < RZ * RY; row += kThreads / 32) {
-            const int pz = row / RY, ry = row - pz * RY;
-            const int gy = y0 - 1 + ry, gz = (N == 3) ? z0 - 1 + pz : 0;
-            const bool rin = gy >= 0 && gy < mY && gz >= 0 && gz < mZ;
-            RegT<TIn> *dst = reg + row * RX;
-            const TIn *src = raw + ((long long)pz * ybox + ry) * xbox + (16 / (int)sizeof(TIn) - 1);
-            for (int rx = lane; rx < RX; rx += 32) {
-                const int gx = x0 - 1 + rx;
-                dst[rx] = (rin && gx >= 0 && gx < mX) ? (int)src[rx] : SENT;
-            }
-        }
-    } else {
-        // flat walk over the region (all lanes busy), element index -> (pz, ry, rx)
-        // advanced incrementally by kThreads (no division per element), four
-        // (2-D) or eight (3-D: config 4 gray K1 0.390 -> 0.382 ms) loads in flight
-        const int RXY = RX * RY, NR = RXY * RZ;
-        const int sz_ = kThreads / RXY, r1 = kThreads - sz_ * RXY, sy_ = r1 / RX, sx_ = r1 - sy_ * RX;
-        int pz = tid / RXY, rem = tid - pz * RXY, ry = rem / RX, rx = rem - ry * RX;
-        constexpr int kLd = N == 3 ? 8 : 4;  // loads in flight per thread
-        for (int i0 = tid; i0 < NR; i0 += kLd * kThreads) {
-            int v[kLd];
-#pragma unroll
-            for (int u = 0; u < kLd; ++u) {
-                const int gx = x0 - 1 + rx, gy = y0 - 1 + ry, gz = (N == 3) ? z0 - 1 + pz : 0;
-                const bool in = i0 + u * kThreads < NR && gx >= 0 && gx < mX && gy >= 0 && gy < mY && gz >= 0 && gz < mZ;
-                v[u] = in ? load_img(img, ((int64_t)gz * mY + gy) * mX + gx) : SENT;
-                rx += sx_;
-                if (rx >= RX) {
-                    rx -= RX;
-                    ++ry;
-                }
-                ry += sy_;
-                if (ry >= RY) {
-                    ry -= RY;
-                    ++pz;
-                }
-                pz += sz_;
-            }
-#pragma unroll
-            for (int u = 0; u < kLd; ++u)
-                if (i0 + u * kThreads < NR) reg[i0 + u * kThreads] = v[u];
+// One row of the current plane: each lane's value at x and its neighbours x - 1
+// and x + 1 (warp shuffles; lanes 0 / 31 load the halo). Values outside the image
+// are the sentinel. `row_ok` is warp-uniform.
+template <typename TIn, bool RIGHT>
+__device__ __forceinline__ void load_row(const TIn *row, bool row_ok, int x, int ext, int sent, int &l, int &m,
+                                         int &r) {
+    const int lane = threadIdx.x & 31;
+    const int hx = lane == 0 ? x - 1 : x + 1;
+    const bool hlane = lane == 0 || (RIGHT && lane == 31);
+    int v = sent, hv = sent;
+    if (row_ok && x < ext) v = (int)__ldg(row + x);
+    if (row_ok && hlane && (unsigned)hx < (unsigned)ext) hv = (int)__ldg(row + hx);
+    m = v;
+    l = __shfl_up_sync(0xffffffffu, v, 1);
+    l = lane == 0 ? hv : l;
+    if constexpr (RIGHT) {
+        r = __shfl_down_sync(0xffffffffu, v, 1);
+        r = lane == 31 ? hv : r;
+    }
+}
+
+// ------------------------------------------------------------------ VERTEX walk
+// Walk state of one lane (vertex column x, row y): the in-plane box mins of the
+// current plane w (pm, 3^(N-1) values, unmasked unless the mask commutes), the
+// inclusion-exclusion corners of the cells spanning planes w-1 .. w (tlow) and
+// the raw values of plane w+1, loaded one step ahead (the walk is latency-bound
+// otherwise: the load is then in flight for a whole step).
+template <int N>
+struct Raw {
+    static constexpr int R = N == 3 ? 3 : 1;  // in-plane rows: y-1, y, y+1 (3-D) / the row (2-D)
+    int m[R];  // this lane's column
+    int h[R];  // halo column: lane 0 holds x - 1, lane 31 holds x + 1
+};
+
+
+// Loads of consecutive planes for one lane: a pointer at (plane p, row y-1, column
+// x) advanced one plane per load; row / column validity fixed per lane. Sentinel
+// outside the image (predicated loads, nothing dereferenced out of range).
+template <int N, typename TIn>
+struct PlaneCursor;
+template <int N, typename TIn>
+struct PlaneCursor {
+    const TIn *ptr;
+    long long pstride;  // elements per plane
+    int rstride;        // elements per row (3-D)
+    int p, pend;        // next plane, plane extent
+    int hdx;            // halo column offset: -1 (lane 0), +1 (lane 31)
+    bool rok[N == 3 ? 3 : 1], xok, hok;
+    __device__ __forceinline__ void init(const TIn *img, const Geo &g, int p0, int y, int x) {
+        const int lane = threadIdx.x & 31;
+        hdx = lane == 0 ? -1 : 1;
+        xok = x < g.MX;
+        hok = (lane == 0 || lane == 31) && (unsigned)(x + hdx) < (unsigned)g.MX;
+        p = p0;
+        if constexpr (N == 3) {
+            pend = g.MZ;
+            pstride = (long long)g.MY * g.MX;
+            rstride = g.MX;
+            for (int k = 0; k < 3; ++k) rok[k] = (unsigned)(y - 1 + k) < (unsigned)g.MY;
+            ptr = img + (long long)p0 * pstride + (long long)(y - 1) * g.MX + x;
+        } else {
+            pend = g.MY;
+            pstride = g.MX;
+            rstride = 0;
+            rok[0] = true;
+            ptr = img + (long long)p0 * g.MX + x;
         }
     }
-    __syncthreads();
-
-    // ---- per vertex stencil + compaction into shared staging
-    const int sy = RX, sz = RX * RY;
-    const int TP = TXe * TYe;
-    const int TV = TP * TZe;
-    int cnt_o[1 << N][2];
+    __device__ __forceinline__ void load(int sent, Raw<N> &r) {
+        const bool pok = (unsigned)p < (unsigned)pend;
 #pragma unroll
-    for (int e = 0; e < (1 << N); ++e) cnt_o[e][0] = cnt_o[e][1] = 0;
-    // per thread: at most kTileV / kThreads vertices; 16-bit records keep the sum in int32
+        for (int k = 0; k < Raw<N>::R; ++k) {
+            const TIn *row = ptr + k * rstride;
+            int v = sent, hv = sent;
+            if (pok && rok[k] && xok) v = (int)__ldg(row);
+            if (pok && rok[k] && hok) hv = (int)__ldg(row + hdx);
+            r.m[k] = v;
+            r.h[k] = hv;
+        }
+        ptr += pstride;
+        ++p;
+    }
+};
+
+template <int N, typename TIn>
+struct VState {
+    static constexpr int P = pow3(N - 1), C = 1 << (N - 1);
+    int pm[P];
+    int tlow[C];
+    Raw<N> next;
+    PlaneCursor<N, TIn> cur;
+};
+
+// In-plane box mins (3^(N-1) cells spanned by the vertex and its in-plane
+// neighbours) from a plane's raw values: x +- 1 by warp shuffles.
+template <int N, int CONS, typename TIn>
+__device__ __forceinline__ void plane_reduce(const Raw<N> &r, int (&o)[pow3(N - 1)]) {
+    const int lane = threadIdx.x & 31;
+    int v[Raw<N>::R * 3];
+#pragma unroll
+    for (int k = 0; k < Raw<N>::R; ++k) {
+        const int l = __shfl_up_sync(0xffffffffu, r.m[k], 1), rr = __shfl_down_sync(0xffffffffu, r.m[k], 1);
+        v[k * 3] = lane == 0 ? r.h[k] : l;
+        v[k * 3 + 1] = r.m[k];
+        v[k * 3 + 2] = lane == 31 ? r.h[k] : rr;
+    }
+    if constexpr (N == 3) {
+#pragma unroll
+        for (int dx = 0; dx < 3; ++dx) {  // y pass: cells spanned by y and y + o_y
+            v[dx] = min(v[dx], v[3 + dx]);
+            v[6 + dx] = min(v[6 + dx], v[3 + dx]);
+        }
+    }
+#pragma unroll
+    for (int dy = 0; dy < Raw<N>::R; ++dy) {  // x pass
+        v[dy * 3] = min(v[dy * 3], v[dy * 3 + 1]);
+        v[dy * 3 + 2] = min(v[dy * 3 + 2], v[dy * 3 + 1]);
+    }
+#pragma unroll
+    for (int i = 0; i < pow3(N - 1); ++i) {
+        if constexpr (CONS == EUCALC_VERTEX && sizeof(TIn) == 1) o[i] = max(v[i], 0);  // mask commutes with min
+        else o[i] = v[i];
+    }
+}
+
+template <int N, int CONS, typename TIn>
+__device__ __forceinline__ void masked_ie(const int (&in)[pow3(N - 1)], int (&t)[1 << (N - 1)]) {
+    int v[pow3(N - 1)];
+#pragma unroll
+    for (int i = 0; i < pow3(N - 1); ++i) {
+        if constexpr (CONS == EUCALC_VERTEX && sizeof(TIn) == 1) v[i] = in[i];  // masked in plane_boxmin
+        else v[i] = mask_cell<CONS, TIn>(in[i]);
+    }
+    incl_excl<N - 1>(v);
+#pragma unroll
+    for (int c = 0; c < (1 << (N - 1)); ++c) t[c] = v[corner<N - 1>(c)];
+}
+
+// Prime the walk at plane w: pm = box mins of w, tlow = corners of min(w-1, w),
+// plane w+1 in flight.
+template <int N, int CONS, typename TIn>
+__device__ __forceinline__ void vwalk_prime(const TIn *img, const Geo &g, int w, int y, int x, VState<N, TIn> &s) {
+    constexpr int S = Sent<CONS, TIn>::value;
+    Raw<N> r0, r1;
+    s.cur.init(img, g, w - 1, y, x);
+    s.cur.load(S, r0);
+    s.cur.load(S, r1);
+    s.cur.load(S, s.next);
+    int pp[pow3(N - 1)];
+    plane_reduce<N, CONS, TIn>(r0, pp);
+    plane_reduce<N, CONS, TIn>(r1, s.pm);
+#pragma unroll
+    for (int i = 0; i < pow3(N - 1); ++i) pp[i] = min(pp[i], s.pm[i]);
+    masked_ie<N, CONS, TIn>(pp, s.tlow);
+}
+
+// One walk step: Delta^- of all 2^N sign vectors at plane w, state advanced to w + 1.
+// Orthant e: bit 0 <-> the walk axis (axis 0), bit k <-> axis k.
+template <int N, int CONS, typename TIn>
+__device__ __forceinline__ void vwalk_step(VState<N, TIn> &s, int (&dm)[1 << N]) {
+    constexpr int P = pow3(N - 1), C = 1 << (N - 1);
+    int pn[P], cu[P], tup[C], tmid[C];
+    Raw<N> ahead;
+    s.cur.load(Sent<CONS, TIn>::value, ahead);  // plane w + 2, in flight during this step
+    plane_reduce<N, CONS, TIn>(s.next, pn);
+#pragma unroll
+    for (int i = 0; i < P; ++i) cu[i] = min(s.pm[i], pn[i]);  // cells spanning w .. w+1
+    masked_ie<N, CONS, TIn>(cu, tup);
+    masked_ie<N, CONS, TIn>(s.pm, tmid);
+    static_for<0, (1 << N)>([&](auto E) {
+        constexpr int e = decltype(E)::value;
+        // in-plane bits: axis k (k >= 1) <-> bit k of e <-> corner bit j = k - 1 (slowest first)
+        constexpr int c = e >> 1;
+        if constexpr (e & 1) dm[e] = tmid[c] - s.tlow[c];
+        else dm[e] = tmid[c] - tup[c];
+    });
+#pragma unroll
+    for (int c = 0; c < C; ++c) s.tlow[c] = tup[c];
+#pragma unroll
+    for (int i = 0; i < P; ++i) s.pm[i] = pn[i];
+    s.next = ahead;
+}
+
+// ------------------------------------------------------------------ TOP walk
+// The vertex's 2^N pixels (bit k of the corner set <-> pixel x_k, clear <-> x_k - 1);
+// the walk carries the pixels of plane w - 1 (bit 0 clear).
+template <int N>
+struct TState {
+    int prev[1 << (N - 1)];
+};
+
+template <int N, typename TIn>
+__device__ __forceinline__ void top_plane(const TIn *img, const Geo &g, int p, int y, int x, int (&o)[1 << (N - 1)]) {
+    // pixels (p, y-1 / y, x-1 / x) of plane p; in-plane corner bit 0 <-> axis 1, ...
+    constexpr int S = Sent<EUCALC_TOP, TIn>::value;
+    const bool pok = p >= 0 && p < (N == 3 ? g.mZ : g.mY);
+    int dummy;
+    if constexpr (N == 3) {
+#pragma unroll
+        for (int by = 0; by < 2; ++by) {
+            const int yy = y - 1 + by;
+            const bool ok = pok && yy >= 0 && yy < g.mY;
+            int l, m;
+            load_row<TIn, false>(img + ((long long)p * g.mY + (ok ? yy : 0)) * g.mX, ok, x, g.mX, S, l, m, dummy);
+            o[by * 2 + 0] = l;  // bit for axis 2 (x) is the low bit of the in-plane index
+            o[by * 2 + 1] = m;
+        }
+    } else {
+        int l, m;
+        load_row<TIn, false>(img + (long long)(pok ? p : 0) * g.mX, pok, x, g.mX, S, l, m, dummy);
+        o[0] = l;
+        o[1] = m;
+    }
+}
+
+template <int N, typename TIn>
+__device__ __forceinline__ void twalk_step(const TIn *img, const Geo &g, int w, int y, int x, TState<N> &s,
+                                           int (&dm)[1 << N]) {
+    constexpr int P3 = pow3(N), PX = 1 << N;
+    int cur[1 << (N - 1)];
+    top_plane<N, TIn>(img, g, w, y, x, cur);
+    // pix[c]: c bit k (axis k) set <-> pixel index x_k; in-plane index of axes 1..N-1
+    // has axis N-1 (x) as its lowest bit
+    int pix[PX];
+    static_for<0, PX>([&](auto CC) {
+        constexpr int c = decltype(CC)::value;
+        constexpr int ip = N == 3 ? (((c >> 1) & 1) << 1) | ((c >> 2) & 1) : ((c >> 1) & 1);
+        if constexpr (c & 1) pix[c] = cur[ip];
+        else pix[c] = s.prev[ip];
+    });
+    int val[P3];
+    static_for<0, P3>([&](auto I) {
+        constexpr int idx = decltype(I)::value;
+        int m = INT_MAX;
+        static_for<0, PX>([&](auto C) {
+            if constexpr (top_coface<N>(idx, decltype(C)::value)) m = min(m, pix[decltype(C)::value]);
+        });
+        val[idx] = mask_cell<EUCALC_TOP, TIn>(m);
+    });
+    incl_excl<N>(val);
+    static_for<0, PX>([&](auto E) {
+        constexpr int e = decltype(E)::value;
+        constexpr int idx = (e & 1 ? 2 * pow3(N - 1) : 0) + ((e >> 1) & 1 ? 2 * pow3(N - 2) : 0) +
+                            (N == 3 && ((e >> 2) & 1) ? 2 : 0);
+        dm[e] = val[idx];
+    });
+#pragma unroll
+    for (int i = 0; i < (1 << (N - 1)); ++i) s.prev[i] = cur[i];
+}
+
+// ------------------------------------------------------------------ the pencil kernel
+template <int N, int CONS, typename TIn>
+struct Walker {
+    VState<N, TIn> v;
+    TState<N> t;
+    __device__ __forceinline__ void prime(const TIn *img, const Geo &g, int w, int y, int x) {
+        if constexpr (CONS == EUCALC_VERTEX) vwalk_prime<N, CONS, TIn>(img, g, w, y, x, v);
+        else top_plane<N, TIn>(img, g, w - 1, y, x, t.prev);
+    }
+    __device__ __forceinline__ void step(const TIn *img, const Geo &g, int w, int y, int x, int (&dm)[1 << N]) {
+        if constexpr (CONS == EUCALC_VERTEX) vwalk_step<N, CONS, TIn>(v, dm);
+        else twalk_step<N, TIn>(img, g, w, y, x, t, dm);
+    }
+};
+
+// Predicated record store (no branch around it: a divergent `if` costs a
+// reconvergence and the address setup on one side only).
+__device__ __forceinline__ void st_rec_if(Rec16 *p, uint32_t c, int a, int b, bool pred) {
+    const unsigned w = (unsigned)(a & 0xffff) | ((unsigned)b << 16);
+    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %3, 0;\n\t@q st.global.v2.b32 [%0], {%1, %2};\n\t}" ::"l"(p),
+                 "r"(c), "r"(w), "r"((unsigned)pred)
+                 : "memory");
+}
+__device__ __forceinline__ void st_rec_if(Rec32 *p, uint32_t c, int a, int b, bool pred) {
+    if (pred) {
+        p->c = c;
+        p->a = a;
+        p->b = b;
+    }
+}
+
+// MODE kEmit : records into the (tile, warp) regions of the scratch lists, the
+//              regions' counts and the |Delta^-| statistics of the lists;
+//      kStats: per-orthant N^-, N^ord (eucalc_critical_counts).
+template <int N, int CONS, typename TIn, typename RecT, int MODE>
+__global__ void __launch_bounds__(kThreads, 3) k1_pencil(K1Args a) {
+    constexpr int Q = 1 << (N - 1), FULL = (1 << N) - 1;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    Geo g;
+    g.MX = a.M[N - 1];
+    g.MY = N >= 2 ? a.M[N - 2] : 1;
+    g.MZ = N == 3 ? a.M[0] : 1;
+    g.mX = a.m[N - 1];
+    g.mY = N >= 2 ? a.m[N - 2] : 1;
+    g.mZ = N == 3 ? a.m[0] : 1;
+    const int tiles_img = a.tiles_x * a.tiles_y * a.tiles_z;
+    // this warp's pencil: image b, column block tx (x0 = 32 tx), row y (3-D) and
+    // walk range [w0, w1) over the walk axis (z in 3-D, y in 2-D)
+    long long b;
+    int tx, y, w0, w1, ty_t, tz0, wslot;
+    if constexpr (N == 3) {
+        const int nzc = (g.MZ + kWalk3 - 1) / kWalk3;
+        long long cta = blockIdx.x;
+        tx = (int)(cta % a.tiles_x);
+        cta /= a.tiles_x;
+        ty_t = (int)(cta % a.tiles_y);
+        cta /= a.tiles_y;
+        const int zc = (int)(cta % nzc);
+        b = cta / nzc;
+        y = ty_t * Tile<N>::TY + warp;
+        w0 = zc * kWalk3;
+        w1 = min(g.MZ, w0 + kWalk3);
+        tz0 = w0 / Tile<N>::TZ;
+        wslot = warp;
+        if (y >= g.MY) return;
+    } else {
+        const long long gw = (long long)blockIdx.x * kWarps + warp;
+        if (gw >= a.batch * tiles_img * a.W) return;
+        const int r = (int)(gw % a.W);
+        b = gw / a.W / tiles_img;
+        const int t = (int)(gw / a.W % tiles_img);
+        tx = t % a.tiles_x;
+        ty_t = t / a.tiles_x;
+        y = 0;
+        w0 = ty_t * Tile<N>::TY + r * (Tile<N>::TY / a.W);
+        w1 = min(g.MY, w0 + Tile<N>::TY / a.W);
+        tz0 = 0;
+        wslot = r;
+        if (w0 >= g.MY) return;  // an empty region of a ragged tile (its count stays 0)
+    }
+    const int x = tx * 32 + lane;
+    const bool xin = x < g.MX;
+    const TIn *img = reinterpret_cast<const TIn *>(a.img) + b * a.npix;
+    const int W = N == 3 ? Tile<3>::W : a.W;  // warps (regions) per tile
+    // records go to this (tile, warp)'s region of the scratch lists (fixed capacity
+    // cap_r = its vertex count), or straight to the lists when an image is one region
+    RecT *out = reinterpret_cast<RecT *>(a.direct ? a.rec : a.scratch);
+    const long long lcap = a.direct ? a.vcap : a.scap;
+    int run[Q];       // kept records so far in the current (tile, warp)
+    RecT *dst[Q];     // first record of the current (tile, warp) region in each list
     using AccT = std::conditional_t<std::is_same<RecT, Rec16>::value, int, long long>;
     AccT abs_sum[Q];
     int max_rec[Q];
+    int cnt_c[1 << N], cnt_o[Q];
 #pragma unroll
     for (int q = 0; q < Q; ++q) {
+        run[q] = 0;
+        dst[q] = out;
         abs_sum[q] = 0;
         max_rec[q] = 0;
+        cnt_o[q] = 0;
     }
-
-    int wrun[Q];
 #pragma unroll
-    for (int q = 0; q < Q; ++q) wrun[q] = 0;
-    // vertex index li = c0 + tid -> (lz, ly, lx), advanced incrementally by kThreads
-    const int vz_ = kThreads / TP, v1 = kThreads - vz_ * TP, vy_ = v1 / TXe, vx_ = v1 - vy_ * TXe;
-    int lz = tid / TP, lrem = tid - lz * TP, ly = lrem / TXe, lx = lrem - ly * TXe;
-    // full-plane tiles (TP == kThreads): vertex li + kThreads is the same (lx, ly) at lz + 1
-    constexpr bool kSlide = N == 3 && CONS == EUCALC_VERTEX && sizeof(RegT<TIn>) == 2;
-    const bool slide = kSlide && TP == kThreads;
-    int sl_pm[9], sl_tlow[4];  // plane lz (masked box mins); corners of min(plane lz-1, plane lz)
-    if constexpr (kSlide) {
-        if (slide) {
-            const int base0 = (lz + 1) * sz + (ly + 1) * sy + (lx + 1);
-            int pp[9];
-            plane_min(reinterpret_cast<const short *>(reg), sy, base0 - sz, pp);
-            plane_min(reinterpret_cast<const short *>(reg), sy, base0, sl_pm);
+    for (int e = 0; e < (1 << N); ++e) cnt_c[e] = 0;
+    // the (tile, warp) slot of the tile holding walk step w
+    auto slot = [&](int w) -> long long {
+        const int tt = N == 3 ? ((tz0 + (w - w0) / Tile<N>::TZ) * a.tiles_y + ty_t) * a.tiles_x + tx
+                              : ty_t * a.tiles_x + tx;
+        return (long long)tt * W + wslot;
+    };
+    auto flush = [&](int w_last) {  // the (tile, warp) holding step w_last is complete
+        if constexpr (MODE == kEmit) {
+            if (lane == 0) {
+                const long long sl = slot(w_last);
 #pragma unroll
-            for (int i = 0; i < 9; ++i) pp[i] = min(pp[i], sl_pm[i]);
-            plane_ie(pp, sl_tlow);
-        }
-    }
-    for (int c0 = 0; c0 < TV; c0 += kThreads) {
-        const int li = c0 + tid;
-        const bool valid = li < TV;
-        int dm[1 << N];
-        if (kSlide && slide) {
-            if constexpr (kSlide) {
-                const int base = (lz + 1) * sz + (ly + 1) * sy + (lx + 1);
-                int pn[9], cu[9], tup[4], tmid[4];
-                plane_min(reinterpret_cast<const short *>(reg), sy, base + sz, pn);
-#pragma unroll
-                for (int i = 0; i < 9; ++i) cu[i] = min(sl_pm[i], pn[i]);  // cells spanning lz .. lz+1
-                plane_ie(cu, tup);
-                plane_ie(sl_pm, tmid);
-                // z pass: slot 2 (eps_z = +1, bit 0 of e) <- mid - low, slot 0 <- mid - up
-#pragma unroll
-                for (int e = 0; e < (1 << N); ++e) {
-                    const int i = ((e >> 1) & 1) * 2 + ((e >> 2) & 1);
-                    dm[e] = (e & 1) ? tmid[i] - sl_tlow[i] : tmid[i] - tup[i];
+                for (int q = 0; q < Q; ++q) {
+                    if (a.direct) {  // one region per image: its count is the list length
+                        a.count[b * Q + q] = run[q];
+                        a.tile_off[(b * Q + q) * 2] = 0;
+                        a.tile_off[(b * Q + q) * 2 + 1] = run[q];
+                    } else {
+                        a.cnt[(b * Q + q) * (long long)tiles_img * W + sl] = run[q];
+                    }
                 }
-#pragma unroll
-                for (int i = 0; i < 4; ++i) sl_tlow[i] = tup[i];
-#pragma unroll
-                for (int i = 0; i < 9; ++i) sl_pm[i] = pn[i];
             }
-        } else if (valid) {
-            const int base = ((N == 3) ? (lz + 1) * sz : 0) + (ly + 1) * sy + (lx + 1);
-            vertex_dminus<N, CONS>(reg, sz, sy, base, dm);
-        } else {
+        }
+#pragma unroll
+        for (int q = 0; q < Q; ++q) run[q] = 0;
+    };
+    auto load_base = [&](int w) {
+        if constexpr (MODE == kEmit) {
+            const long long sl = slot(w);
+#pragma unroll
+            for (int q = 0; q < Q; ++q) dst[q] = out + (b * Q + q) * lcap + sl * a.cap_r;
+        }
+    };
+    Walker<N, CONS, TIn> wk;
+    wk.prime(img, g, w0, y, x);
+    load_base(w0);
+    const int seg = N == 3 ? Tile<3>::SEG : Tile<2>::TY / a.W;  // walk steps per region
+    int left = seg;
+    for (int w = w0; w < w1; ++w) {
+        if (left == 0) {  // tile boundary
+            flush(w - 1);
+            load_base(w);
+            left = seg;
+        }
+        --left;
+        int dm[1 << N];
+        wk.step(img, g, w, y, x, dm);
+        if (!xin) {
 #pragma unroll
             for (int e = 0; e < (1 << N); ++e) dm[e] = 0;
         }
+        if constexpr (MODE == kStats) {
 #pragma unroll
-        for (int e = 0; e < (1 << N); ++e) {
-            cnt_o[e][0] += dm[e] != 0;
-            cnt_o[e][1] += dm[e] != dm[e ^ FULL];
+            for (int e = 0; e < (1 << N); ++e) cnt_c[e] += dm[e] != 0;
+#pragma unroll
+            for (int q = 0; q < Q; ++q) cnt_o[q] += dm[q] != dm[q ^ FULL];
+        } else {
+            uint32_t coord = 0;
+            if constexpr (MODE == kEmit) {
+                coord = (uint32_t)x << a.sh[N - 1];
+                if constexpr (N == 3) coord |= ((uint32_t)y << a.sh[1]) | ((uint32_t)w << a.sh[0]);
+                else coord |= (uint32_t)w << a.sh[0];
+            }
+#pragma unroll
+            for (int q = 0; q < Q; ++q) {
+                const int da = dm[q], db = dm[q ^ FULL];
+                const bool keep = (da | db) != 0;
+                const unsigned bal = __ballot_sync(0xffffffffu, keep);
+                st_rec_if(dst[q] + run[q] + __popc(bal & ((1u << lane) - 1)), coord, da, db, keep);
+                const int s = abs(da) + abs(db);
+                abs_sum[q] += s;
+                max_rec[q] = max(max_rec[q], s);
+                run[q] += __popc(bal);
+            }
         }
-        uint32_t coord = 0;
-        if (valid) {
-            const int gx = x0 + lx, gy = y0 + ly;
-            coord = ((uint32_t)gx << a.sh[N - 1]);
-            if (N >= 2) coord |= ((uint32_t)gy << a.sh[N - 2]);
-            if (N == 3) coord |= ((uint32_t)(z0 + lz) << a.sh[0]);
-        }
-        lx += vx_;
-        if (lx >= TXe) {
-            lx -= TXe;
-            ++ly;
-        }
-        ly += vy_;
-        if (ly >= TYe) {
-            ly -= TYe;
-            ++lz;
-        }
-        lz += vz_;
-        // warp-private compaction: warp w appends to its own slice of the
-        // staging area (no block barrier per vertex batch); the tile's order is
-        // (warp, batch, lane) and the slices are concatenated at copy-out
+    }
+    flush(w1 - 1);
+    if constexpr (MODE == kEmit) {
+        // |Delta^-| statistics of the lists (order-independent integer reductions)
 #pragma unroll
         for (int q = 0; q < Q; ++q) {
-            const bool keep = dm[q] != 0 || dm[q ^ FULL] != 0;
-            const unsigned bal = __ballot_sync(0xffffffffu, keep);
-            if (keep) {
-                RecT r;
-                r.c = coord;
-                r.a = dm[q];
-                r.b = dm[q ^ FULL];
-                stage[q * kTileV + warp * kPerWarp + wrun[q] + __popc(bal & ((1u << lane) - 1))] = r;
+            AccT v = abs_sum[q];
+            for (int d = 16; d; d >>= 1) v += __shfl_xor_sync(0xffffffffu, v, d);
+            if (lane == 0 && v) atomicAdd((unsigned long long *)&a.abs_sum[b * Q + q], (unsigned long long)(long long)v);
+            int mr = max_rec[q];
+            for (int d = 16; d; d >>= 1) mr = max(mr, __shfl_xor_sync(0xffffffffu, mr, d));
+            if (lane == 0 && mr) atomicMax((unsigned long long *)&a.max_rec[b * Q + q], (unsigned long long)mr);
+        }
+    }
+    if constexpr (MODE == kStats) {
+#pragma unroll
+        for (int e = 0; e < (1 << N); ++e) {
+            int c = cnt_c[e], o = cnt_o[(e >> (N - 1)) & 1 ? (e ^ FULL) : e];
+            for (int d = 16; d; d >>= 1) {
+                c += __shfl_xor_sync(0xffffffffu, c, d);
+                o += __shfl_xor_sync(0xffffffffu, o, d);
             }
-            wrun[q] += __popc(bal);
-            abs_sum[q] += abs(dm[q]) + abs(dm[q ^ FULL]);
-            max_rec[q] = max(max_rec[q], abs(dm[q]) + abs(dm[q ^ FULL]));
-        }
-    }
-    if (lane == 0) {
-#pragma unroll
-        for (int q = 0; q < Q; ++q) s_warp[warp][q] = wrun[q];
-    }
-    __syncthreads();
-    if (tid < Q) {
-        int tot = 0;
-        for (int w = 0; w < kThreads / 32; ++w) tot += s_warp[w][tid];
-        s_run[tid] = tot;
-        // publish this tile's aggregate now, before the statistics below, so that
-        // successors looking back find it sooner (tile 0 publishes its inclusive prefix)
-        unsigned long long *flag_t = a.flags + ((int64_t)b * tiles_per_img + t) * Q + tid;
-        st_relaxed(flag_t, (t == 0 ? kIncl : kAgg) | (unsigned long long)tot);
-    }
-
-    // ---- per-image statistics (order-independent integer sums: deterministic)
-#pragma unroll
-    for (int e = 0; e < (1 << N); ++e) {
-        int c = cnt_o[e][0], o = cnt_o[e][1];
-        for (int d = 16; d; d >>= 1) {
-            c += __shfl_xor_sync(0xffffffffu, c, d);
-            o += __shfl_xor_sync(0xffffffffu, o, d);
-        }
-        if (lane == 0) {
-            atomicAdd(&s_ostat[e][0], c);
-            atomicAdd(&s_ostat[e][1], o);
-        }
-    }
-#pragma unroll
-    for (int q = 0; q < Q; ++q) {
-        AccT v = abs_sum[q];
-        for (int d = 16; d; d >>= 1) v += __shfl_xor_sync(0xffffffffu, v, d);
-        if (lane == 0 && v) atomicAdd((unsigned long long *)&a.abs_sum[b * Q + q], (unsigned long long)(long long)v);
-        int mr = max_rec[q];
-        for (int d = 16; d; d >>= 1) mr = max(mr, __shfl_xor_sync(0xffffffffu, mr, d));
-        if (lane == 0 && mr) atomicMax((unsigned long long *)&a.max_rec[b * Q + q], (unsigned long long)mr);
-    }
-    __syncthreads();
-    if (tid < (1 << N) * 2) {
-        int v = (&s_ostat[0][0])[tid];
-        if (v) atomicAdd((unsigned long long *)&a.stats[b * (1 << N) * 2 + tid], (unsigned long long)v);
-        (&s_ostat[0][0])[tid] = 0;  // ready for the CTA's next tile
-    }
-
-    // ---- look-back per pair (warp q), then ordered copy-out
-    if (warp < Q) {
-        const int q = warp;
-        const long long agg = s_run[q];
-        unsigned long long *flag_t = a.flags + ((int64_t)b * tiles_per_img + t) * Q + q;
-        long long excl;
-        if (t == 0) {
-            excl = 0;  // inclusive prefix published with the aggregate
-        } else {
-            excl = lookback(flag_t, t, Q, agg);
-        }
-        if (lane == 0) {
-            s_excl[q] = excl;
-            // per-tile list offsets: K2's height-window culling streams only the
-            // tiles whose height range meets the window
-            int32_t *toff = a.tile_off + (b * Q + q) * (int64_t)(tiles_per_img + 1);
-            toff[t] = (int32_t)excl;
-            if (t == tiles_per_img - 1) {
-                a.count[b * Q + q] = (int32_t)(excl + agg);
-                toff[tiles_per_img] = (int32_t)(excl + agg);
+            if (lane == 0) {
+                if (c) atomicAdd((unsigned long long *)&a.stats[(b * (1 << N) + e) * 2], (unsigned long long)c);
+                if (o) atomicAdd((unsigned long long *)&a.stats[(b * (1 << N) + e) * 2 + 1], (unsigned long long)o);
             }
         }
     }
-    __syncthreads();
-    RecT *out = reinterpret_cast<RecT *>(a.rec);
+}
+
+// Exclusive scan of each list's (tile, warp) counts, in place -> offsets; the
+// per-tile offsets (first warp of each tile) and the list length. One warp per
+// chunk of 256 counts, chunks handed out by a ticket in list order; a chunk's
+// prefix comes from a warp-wide decoupled look-back over the earlier chunks of
+// its list (flag = status in bits 62-63: 1 aggregate, 2 inclusive prefix).
+constexpr int kScanPer = 8, kScanChunk = 32 * kScanPer;
+constexpr unsigned long long kAgg = 1ull << 62, kIncl = 2ull << 62, kValMask = (1ull << 62) - 1;
+
+__device__ __forceinline__ unsigned long long ld_relaxed(const unsigned long long *p) {
+    unsigned long long v;
+    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_relaxed(unsigned long long *p, unsigned long long v) {
+    asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+__global__ void __launch_bounds__(kThreads) k1_scan(K1Args a, long long chunks_per_list, long long total) {
+    const int lane = threadIdx.x & 31;
+    unsigned tk = 0;
+    if (lane == 0) tk = atomicAdd(a.ticket, 1u);
+    tk = __shfl_sync(0xffffffffu, tk, 0);
+    if (tk >= total) return;
+    const long long L = tk / chunks_per_list, j = tk % chunks_per_list;
+    const int tiles_img = a.tiles_x * a.tiles_y * a.tiles_z;
+    const long long n = (long long)tiles_img * a.W;
+    int32_t *c = a.cnt + L * n;
+    const long long i0 = j * kScanChunk + (long long)lane * kScanPer;
+    int v[kScanPer];
+    int t = 0;
 #pragma unroll
-    for (int q = 0; q < Q; ++q) {
-        int before = 0;  // this warp's slice follows the slices of warps 0..warp-1
-        for (int w = 0; w < warp; ++w) before += s_warp[w][q];
-        RecT *dst = out + (b * Q + q) * a.vcap + s_excl[q] + before;
-        const RecT *src = stage + q * kTileV + warp * kPerWarp;
-        for (int i = lane; i < s_warp[warp][q]; i += 32) dst[i] = src[i];
+    for (int k = 0; k < kScanPer; ++k) {
+        v[k] = i0 + k < n ? c[i0 + k] : 0;
+        t += v[k];
     }
-    __syncthreads();  // staging, region and shared counters are reused by the next tile
+    int incl = t;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const int u = __shfl_up_sync(0xffffffffu, incl, d);
+        if (lane >= d) incl += u;
+    }
+    const long long agg = __shfl_sync(0xffffffffu, incl, 31);
+    unsigned long long *flag = a.flags + tk;
+    long long prefix = 0;
+    if (j == 0) {
+        if (lane == 0) st_relaxed(flag, kIncl | (unsigned long long)agg);
+    } else {
+        if (lane == 0) st_relaxed(flag, kAgg | (unsigned long long)agg);
+        long long back = j - 1;  // predecessor chunks j-1 .. 0 of this list (flags tk-1 .. tk-j)
+        while (true) {
+            const long long idx = back - lane;
+            unsigned long long f = kIncl;  // virtual inclusive 0 before chunk 0
+            if (idx >= 0) {
+                const unsigned long long *p = a.flags + (tk - j + idx);
+                do { f = ld_relaxed(p); } while ((f >> 62) == 0);
+            }
+            const unsigned inc = __ballot_sync(0xffffffffu, (f >> 62) == 2);
+            const int first = inc ? __ffs(inc) - 1 : 31;
+            long long val = lane <= first ? (long long)(f & kValMask) : 0;
+            for (int d = 16; d; d >>= 1) val += __shfl_xor_sync(0xffffffffu, val, d);
+            prefix += val;
+            if (inc) break;
+            back -= 32;
+        }
+        if (lane == 0) st_relaxed(flag, kIncl | (unsigned long long)(prefix + agg));
+    }
+    long long run = prefix + incl - t;
+    int32_t *toff = a.tile_off + L * (long long)(tiles_img + 1);
+#pragma unroll
+    for (int k = 0; k < kScanPer; ++k) {
+        const long long i = i0 + k;
+        if (i < n) {
+            c[i] = (int32_t)run;
+            if (i % a.W == 0) toff[i / a.W] = (int32_t)run;
+        }
+        run += v[k];
+    }
+    if (j == chunks_per_list - 1 && lane == 0) {
+        toff[tiles_img] = (int32_t)(prefix + agg);
+        a.count[L] = (int32_t)(prefix + agg);
+    }
 }
 
-// 3-D: at most 80 registers so that three CTAs fit per SM (the 8-bit region +
-// staging of a 16x16x8 tile is 72 KB, three fit in shared memory too)
-template <int N, int CONS, typename TIn, typename RecT>
-__global__ void __launch_bounds__(kThreads, N == 3 ? 3 : 1) k1_kernel(K1Args a) {
-    constexpr int Q = 1 << (N - 1);
-    extern __shared__ __align__(16) unsigned char smem[];
-    RecT *stage = reinterpret_cast<RecT *>(smem);           // [Q][kTileV]
-    RegT<TIn> *reg = reinterpret_cast<RegT<TIn> *>(stage + Q * kTileV);  // input region
-    __shared__ K1Shared<N> sh;
-    __shared__ unsigned s_ticket;
-    if (threadIdx.x == 0) s_ticket = atomicAdd(a.ticket, 1u);
-    if (threadIdx.x < (1 << N) * 2) (&sh.ostat[0][0])[threadIdx.x] = 0;
+// The records of every (tile, warp) region, from its fixed-capacity scratch
+// region to its scanned position. A CTA owns kCopyRegions consecutive regions of
+// a list, whose destinations form one contiguous range: thread t copies
+// destination records t, t + 256, ... and finds each one's region by binary search
+// over the regions' offsets in shared memory (coalesced stores, mostly coalesced
+// loads, no per-region latency chain).
+constexpr int kCopyRegions = 32;
+
+template <typename RecT>
+__global__ void __launch_bounds__(kThreads) k1_copy(K1Args a, long long cpl) {
+    __shared__ int s_off[kCopyRegions + 1];
+    const long long L = blockIdx.x / cpl, j = blockIdx.x % cpl;
+    const long long nreg = (long long)a.tiles_x * a.tiles_y * a.tiles_z * a.W;
+    const long long r0 = j * kCopyRegions;
+    const int nr = (int)min((long long)kCopyRegions, nreg - r0);
+    const int32_t *off = a.cnt + L * nreg + r0;
+    for (int i = threadIdx.x; i < nr; i += kThreads) s_off[i] = off[i];
+    if (threadIdx.x == 0) s_off[nr] = r0 + nr < nreg ? off[nr] : a.count[L];
     __syncthreads();
-    k1_tile<N, CONS, TIn, RecT>(a, s_ticket, nullptr, 0, 0, stage, reg, sh);
-}
-
-// ---- TMA-staged K1 for large images: a persistent CTA keeps the next tile's
-// box (image region + halo) in flight with cp.async.bulk.tensor while it works
-// on the current one (double buffer, one mbarrier per buffer). Requires 16-byte
-// aligned image rows; the tensor map is 3-D (x, y, image) or 4-D (x, y, z, image).
-__device__ __forceinline__ uint32_t smem_addr(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
-
-template <int N>
-__device__ __forceinline__ void tma_box(const CUtensorMap *tm, void *dst, unsigned long long *bar, int x, int y, int z,
-                                        int b) {
-    if (N == 2)
-        asm volatile(
-            "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];"
-            ::"r"(smem_addr(dst)), "l"(tm), "r"(x), "r"(y), "r"(b), "r"(smem_addr(bar))
-            : "memory");
-    else
-        asm volatile(
-            "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], "
-            "[%6];" ::"r"(smem_addr(dst)),
-            "l"(tm), "r"(x), "r"(y), "r"(z), "r"(b), "r"(smem_addr(bar))
-            : "memory");
+    const int base = s_off[0], T = s_off[nr] - base;
+    const RecT *src = reinterpret_cast<const RecT *>(a.scratch) + L * a.scap + r0 * a.cap_r;
+    RecT *dst = reinterpret_cast<RecT *>(a.rec) + L * a.vcap + base;
+#pragma unroll 4
+    for (int d = threadIdx.x; d < T; d += kThreads) {
+        const int x = base + d;
+        int lo = 0, hi = nr - 1;  // last region r with s_off[r] <= x
+        while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (s_off[mid] <= x) lo = mid;
+            else hi = mid - 1;
+        }
+        dst[d] = src[(long long)lo * a.cap_r + (x - s_off[lo])];
+    }
 }
 
 template <int N, int CONS, typename TIn, typename RecT>
-__global__ void __launch_bounds__(kThreads) k1_tma(const __grid_constant__ CUtensorMap tm, K1Args a, int xbox, int ybox,
-                                                   int zbox) {
-    constexpr int Q = 1 << (N - 1);
-    extern __shared__ __align__(128) unsigned char k1_smem_tma[];
-    const int box_bytes = xbox * ybox * zbox * (int)sizeof(TIn);
-    const int box_pad = (box_bytes + 127) / 128 * 128;
-    TIn *raw[2] = {reinterpret_cast<TIn *>(k1_smem_tma), reinterpret_cast<TIn *>(k1_smem_tma + box_pad)};
-    RecT *stage = reinterpret_cast<RecT *>(k1_smem_tma + 2 * box_pad);  // [Q][kTileV]
-    RegT<TIn> *reg = reinterpret_cast<RegT<TIn> *>(stage + Q * kTileV);  // input region
-    __shared__ K1Shared<N> sh;
-    __shared__ unsigned long long bar[2];
-    __shared__ unsigned s_next;
-    const int tiles_per_img = a.tiles_x * a.tiles_y * a.tiles_z;
-    const unsigned total = (unsigned)(a.batch * tiles_per_img);
-    auto issue = [&](unsigned tk, int buf) {  // thread 0: TMA of tile tk's box into raw[buf]
-        const int b = (int)(tk / tiles_per_img), t = (int)(tk % tiles_per_img);
-        const int tx = t % a.tiles_x, ty = (t / a.tiles_x) % a.tiles_y, tz = t / (a.tiles_x * a.tiles_y);
-        asm volatile("mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(&bar[buf])),
-                     "r"(box_bytes)
-                     : "memory");
-        tma_box<N>(&tm, raw[buf], &bar[buf], tx * a.TX - 16 / (int)sizeof(TIn), ty * a.TY - 1, N == 3 ? tz * a.TZ - 1 : 0, b);
-    };
-    if (threadIdx.x == 0) {
-        for (int k = 0; k < 2; ++k)
-            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(&bar[k])) : "memory");
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        s_next = atomicAdd(a.ticket, 1u);
-        if (s_next < total) issue(s_next, 0);
+cudaError_t launch_t(const K1Args &a, cudaStream_t s, int mode) {
+    const int tiles_img = a.tiles_x * a.tiles_y * a.tiles_z;
+    long long grid;
+    if (N == 3) {
+        const int nzc = (a.M[0] + kWalk3 - 1) / kWalk3;
+        grid = a.batch * (long long)a.tiles_x * a.tiles_y * nzc;
+    } else {
+        grid = (a.batch * tiles_img * a.W + kWarps - 1) / kWarps;
     }
-    if (threadIdx.x < (1 << N) * 2) (&sh.ostat[0][0])[threadIdx.x] = 0;
-    __syncthreads();
-    unsigned cur = s_next;
-    int buf = 0;
-    unsigned phase[2] = {0, 0};
-    while (cur < total) {
-        __syncthreads();  // every thread has read s_next
-        if (threadIdx.x == 0) {
-            s_next = atomicAdd(a.ticket, 1u);
-            if (s_next < total) issue(s_next, buf ^ 1);  // raw[buf^1] was consumed by the previous tile
-        }
-        // wait for this tile's box
-        asm volatile(
-            "{\n\t.reg .pred p;\nK1W_%=:\n\t"
-            "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%0], %1;\n\t"
-            "@!p bra K1W_%=;\n}" ::"r"(smem_addr(&bar[buf])),
-            "r"(phase[buf])
-            : "memory");
-        phase[buf] ^= 1;
-        k1_tile<N, CONS, TIn, RecT>(a, cur, raw[buf], xbox, ybox, stage, reg, sh);  // ends with __syncthreads
-        cur = s_next;
-        buf ^= 1;
+    if (grid == 0) return cudaSuccess;
+    if (mode == kStats) {
+        k1_pencil<N, CONS, TIn, RecT, kStats><<<(unsigned)grid, kThreads, 0, s>>>(a);
+        count_launch();
+        return cudaGetLastError();
     }
-}
-
-
-// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda)
-PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
-    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
-    static bool tried = false;
-    if (!tried) {
-        tried = true;
-        void *p = nullptr;
-        cudaDriverEntryPointQueryResult q;
-        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
-            q == cudaDriverEntryPointSuccess)
-            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
-        cudaGetLastError();
-    }
-    return fn;
-}
-
-template <typename TIn>
-CUtensorMapDataType tma_type() {
-    return sizeof(TIn) == 1 ? CU_TENSOR_MAP_DATA_TYPE_UINT8
-                            : sizeof(TIn) == 2 ? CU_TENSOR_MAP_DATA_TYPE_UINT16 : CU_TENSOR_MAP_DATA_TYPE_INT32;
-}
-
-template <int N, int CONS, typename TIn, typename RecT>
-cudaError_t launch_t(const K1Args &a, cudaStream_t s) {
-    constexpr int Q = 1 << (N - 1);
-    const int planes = (N == 3) ? a.TZ + 2 : 1;
-    const size_t region = sizeof(RegT<TIn>) * planes * (a.TY + 2) * (a.TX + 2);
-    const size_t stage = sizeof(RecT) * Q * kTileV;
-    const int64_t ntiles = a.batch * (int64_t)a.tiles_x * a.tiles_y * a.tiles_z;
-    // TMA path: tiled images with 16-byte aligned base, rows and tile origins, boxes
-    // within 256 per dimension. The innermost box start must be 16-byte aligned
-    // (measured: other starts fault), so a box spans cols x0-xoff .. x0+TX rounded
-    // up to xoff, xoff = 16 bytes of elements, instead of the one-column halo.
-    const int e = (int)sizeof(TIn), xoff = 16 / e;
-    const int xbox = (xoff + a.TX + 1 + xoff - 1) / xoff * xoff, ybox = a.TY + 2, zbox = N == 3 ? a.TZ + 2 : 1;
-    const bool tma = ntiles > 1 && ((int64_t)a.m[N - 1] * e) % 16 == 0 && (a.TX * e) % 16 == 0 &&
-                     ((uintptr_t)a.img & 15) == 0 && xbox <= 256 && ybox <= 256 && zbox <= 256 &&
-                     encode_fn() != nullptr && a.use_tma;
-    if (tma) {
-        CUtensorMap tm;
-        cuuint64_t dims[5], strides[4];
-        cuuint32_t box[5], estr[5] = {1, 1, 1, 1, 1};
-        int rank = 0;
-        dims[rank] = (cuuint64_t)a.m[N - 1];
-        box[rank++] = (cuuint32_t)xbox;
-        dims[rank] = (cuuint64_t)a.m[N - 2];
-        box[rank++] = (cuuint32_t)ybox;
-        if (N == 3) {
-            dims[rank] = (cuuint64_t)a.m[0];
-            box[rank++] = (cuuint32_t)zbox;
-        }
-        dims[rank] = (cuuint64_t)a.batch;
-        box[rank++] = 1;
-        cuuint64_t st = (cuuint64_t)a.m[N - 1] * e;
-        for (int k = 0; k < rank - 1; ++k) {
-            strides[k] = st;
-            st *= dims[k + 1];
-        }
-        CUresult r = encode_fn()(&tm, tma_type<TIn>(), (cuuint32_t)rank, const_cast<void *>(a.img), dims, strides, box,
-                                 estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                                 CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-        if (r == CUDA_SUCCESS) {
-            const size_t box_pad = ((size_t)xbox * ybox * zbox * e + 127) / 128 * 128;
-            const size_t smem = 2 * box_pad + stage + region;
-            auto kern = k1_tma<N, CONS, TIn, RecT>;
-            int occ = 0;
-            cudaError_t err = prepare_kernel((const void *)kern, kThreads, smem, &occ);
-            if (err != cudaSuccess) return err;
-            int dev = 0, sms = 148;
-            cudaGetDevice(&dev);
-            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-            const int64_t grid = std::min<int64_t>(ntiles, (int64_t)std::max(occ, 1) * sms);
-            kern<<<(unsigned)grid, kThreads, smem, s>>>(tm, a, xbox, ybox, zbox);
-            count_launch();
-            return cudaGetLastError();
-        }
-    }
-    const size_t smem = stage + region;
-    auto kern = k1_kernel<N, CONS, TIn, RecT>;
-    cudaError_t err = prepare_kernel((const void *)kern, kThreads, smem, nullptr);
-    if (err != cudaSuccess) return err;
-    kern<<<(unsigned)ntiles, kThreads, smem, s>>>(a);
+    k1_pencil<N, CONS, TIn, RecT, kEmit><<<(unsigned)grid, kThreads, 0, s>>>(a);
     count_launch();
+    if (a.direct) return cudaGetLastError();  // one region per image: written in place
+    const long long cpl = ((long long)tiles_img * a.W + kScanChunk - 1) / kScanChunk;
+    const long long chunks = a.batch * (1 << (N - 1)) * cpl;
+    k1_scan<<<(unsigned)((chunks + kWarps - 1) / kWarps), kThreads, 0, s>>>(a, cpl, chunks);
+    const long long ccpl = ((long long)tiles_img * a.W + kCopyRegions - 1) / kCopyRegions;
+    k1_copy<RecT><<<(unsigned)(a.batch * (1 << (N - 1)) * ccpl), kThreads, 0, s>>>(a, ccpl);
+    count_launch(2);
     return cudaGetLastError();
 }
 
 template <int N, int CONS, typename TIn>
-cudaError_t launch_r(const K1Args &a, cudaStream_t s) {
-    return a.wide ? launch_t<N, CONS, TIn, Rec32>(a, s) : launch_t<N, CONS, TIn, Rec16>(a, s);
+cudaError_t launch_r(const K1Args &a, cudaStream_t s, int mode) {
+    return a.wide ? launch_t<N, CONS, TIn, Rec32>(a, s, mode) : launch_t<N, CONS, TIn, Rec16>(a, s, mode);
 }
 template <int N, int CONS>
-cudaError_t launch_d(const K1Args &a, cudaStream_t s) {
+cudaError_t launch_d(const K1Args &a, cudaStream_t s, int mode) {
     switch (a.dtype) {
-    case EUCALC_U8: return launch_r<N, CONS, uint8_t>(a, s);
-    case EUCALC_I16: return launch_r<N, CONS, int16_t>(a, s);
-    default: return launch_r<N, CONS, int32_t>(a, s);
+    case EUCALC_U8: return launch_r<N, CONS, uint8_t>(a, s, mode);
+    case EUCALC_I16: return launch_r<N, CONS, int16_t>(a, s, mode);
+    default: return launch_r<N, CONS, int32_t>(a, s, mode);
     }
+}
+cudaError_t launch_any(const K1Args &a, cudaStream_t s, int mode) {
+    if (a.ndim == 2)
+        return a.construction == EUCALC_VERTEX ? launch_d<2, EUCALC_VERTEX>(a, s, mode)
+                                               : launch_d<2, EUCALC_TOP>(a, s, mode);
+    return a.construction == EUCALC_VERTEX ? launch_d<3, EUCALC_VERTEX>(a, s, mode)
+                                           : launch_d<3, EUCALC_TOP>(a, s, mode);
 }
 
 }  // namespace
 
-cudaError_t launch_k1(const K1Args &a, cudaStream_t s) {
-    if (a.ndim == 2)
-        return a.construction == EUCALC_VERTEX ? launch_d<2, EUCALC_VERTEX>(a, s) : launch_d<2, EUCALC_TOP>(a, s);
-    return a.construction == EUCALC_VERTEX ? launch_d<3, EUCALC_VERTEX>(a, s) : launch_d<3, EUCALC_TOP>(a, s);
+int64_t k1_scan_chunks(int64_t lists, int64_t ntiles, int W) {
+    return lists * ((ntiles * W + kScanChunk - 1) / kScanChunk);
 }
 
-int k1_tile_vertices() { return kTileV; }
+void k1_geometry(int ndim, const int64_t *M, int *TX, int *TY, int *TZ, int *W) {
+    *TX = 32;
+    if (ndim == 3) {
+        *TY = 8;
+        *TZ = 8;
+        *W = 8;
+    } else {
+        *TY = 64;
+        *TZ = 1;
+        *W = (M[1] <= 32 && M[0] <= 64) ? 1 : 4;
+    }
+}
+
+cudaError_t launch_k1(const K1Args &a, cudaStream_t s) { return launch_any(a, s, kEmit); }
+cudaError_t launch_k1_stats(const K1Args &a, cudaStream_t s) { return launch_any(a, s, kStats); }
 
 }  // namespace eucalc

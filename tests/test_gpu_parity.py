@@ -462,28 +462,34 @@ def test_degenerate_images(construction):
     check_transforms(one, np.array([[1, 1]], np.int32), construction, r1)
 
 
-K1_TMA_CASES = [((96, 128), np.uint8, "vertex"), ((96, 128), np.uint8, "top"), ((50, 72), np.int16, "vertex"),
-                ((40, 36), np.int32, "top"), ((20, 24, 32), np.uint8, "vertex"), ((19, 23, 16), np.uint8, "top"),
-                ((9, 10, 16), np.int16, "vertex")]
+K1_GEOMETRY_CASES = [
+    # 3-D: several 64-plane walk chunks, rows not a multiple of 8, x not a multiple of 32
+    ((150, 20, 70), np.uint8, "vertex"), ((150, 20, 70), np.uint8, "top"),
+    ((70, 9, 33), np.int16, "vertex"), ((66, 9, 31), np.int32, "top"),
+    ((65, 17, 40), np.int32, "vertex"),
+    # 2-D: several 64-row tiles and 32-wide column blocks, ragged both ways
+    ((130, 100), np.uint8, "vertex"), ((130, 100), np.uint8, "top"), ((129, 65), np.int16, "top"),
+    ((200, 33), np.int32, "vertex"),
+]
 
 
-@pytest.mark.parametrize("case", K1_TMA_CASES, ids=lambda c: f"{c[0]}-{np.dtype(c[1]).name}-{c[2]}")
-def test_k1_tma_staging(case, monkeypatch):
-    """With EUCALC_K1_TMA set, tiled images with 16-byte aligned rows take the TMA-staged persistent K1
-    (cp.async.bulk.tensor boxes, double-buffered); its lists equal the oracle's and
-    the plain kernel's exactly."""
+@pytest.mark.parametrize("case", K1_GEOMETRY_CASES, ids=lambda c: f"{c[0]}-{np.dtype(c[1]).name}-{c[2]}")
+def test_k1_pencil_geometry(case):
+    """K1's pencils (32 vertices per warp, walking the slowest axis in 64-plane
+    chunks in 3-D / 64-row tiles in 2-D) on extents that are not multiples of the
+    tile: critical tables vs the oracle's star sums, the per-orthant counts, and
+    transforms (K2 culls by the K1 tile offsets) on a few directions."""
     shape, dt, construction = case
-    monkeypatch.setenv("EUCALC_K1_TMA", "1")
     rng = np.random.default_rng(sum(shape))
     lo, hi = (0, 256) if dt == np.uint8 else (-300, 300)
     images = rng.integers(lo, hi, size=(2, *shape)).astype(dt)
-    dirs = synth.random_directions(5, len(shape), 7, 3)
+    dirs = np.concatenate([synth.random_directions(4, len(shape), 7, 3),
+                           synth.random_directions(2, len(shape), 300, 5)])
     cx, cr, res = run_gpu(images, dirs, construction)
     check_critical(images, construction, cr, imgs_to_check=[1])
-    check_transforms(images, dirs, construction, res, pairs=[(0, 0), (1, 4)])
-    monkeypatch.delenv("EUCALC_K1_TMA")
-    cr2 = eu.critical_points(eu.build_complex(images, construction))
-    for b in range(2):
-        for e in range(1 << len(shape)):
-            for x, y in zip(cr.export(b, e), cr2.export(b, e)):
-                np.testing.assert_array_equal(x, y)
+    check_transforms(images, dirs, construction, res, pairs=[(0, 0), (1, 3), (1, 4), (0, 5)])
+    cnt = cr.counts()
+    g = oracle.Grid(images[1], construction)
+    for e in range(1 << len(shape)):
+        c, _, o, _ = g.critical_table(e)
+        assert tuple(cnt[1, e]) == (len(c), len(o))
