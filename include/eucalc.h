@@ -268,6 +268,11 @@ int eucalc_profile_read(const char *stage, double *ms, int64_t *launches);
 int eucalc_profile_span(const char *stage, double *ms);
 /* Kernel launches issued by this library on the calling thread since the last reset. */
 int64_t eucalc_launch_count(int reset);
+/* Diagnostic (tests): K2 block-regime segments whose checked packed histogram
+ * bins flagged a possible field overflow and were recomputed with split bins,
+ * since the last reset. Counted only while the EUCALC_K2_CHK_BITS test hook is
+ * set (the count is read back after each such call, which synchronises it). */
+int64_t eucalc_k2_restarts(int reset);
 const char *eucalc_status_string(eucalc_status s);
 const char *eucalc_last_error(void);
 int64_t eucalc_last_bad_index(void);

@@ -77,6 +77,8 @@ def lib():
         L.eucalc_profile_span.argtypes = [ctypes.c_char_p, ctypes.POINTER(ctypes.c_double)]
         L.eucalc_launch_count.argtypes = [I32]
         L.eucalc_launch_count.restype = I64
+        L.eucalc_k2_restarts.argtypes = [I32]
+        L.eucalc_k2_restarts.restype = I64
         L.eucalc_status_string.restype = ctypes.c_char_p
         L.eucalc_last_error.restype = ctypes.c_char_p
         L.eucalc_last_bad_index.restype = I64
@@ -501,6 +503,12 @@ def profile_span(stage=None):
     ms = ctypes.c_double()
     lib().eucalc_profile_span(stage.encode() if stage else None, ctypes.byref(ms))
     return ms.value
+
+
+def k2_restarts(reset=False) -> int:
+    """eucalc_k2_restarts: block-regime segments recomputed with split bins (counted
+    only under the EUCALC_K2_CHK_BITS test hook)."""
+    return int(lib().eucalc_k2_restarts(1 if reset else 0))
 
 
 def launch_count(reset=False) -> int:

@@ -24,6 +24,7 @@ namespace {
 thread_local std::string g_err;
 thread_local int64_t g_bad = -1;
 thread_local int64_t g_launches = 0;
+std::atomic<int64_t> g_k2_restarts{0};  // eucalc_k2_restarts (test hook EUCALC_K2_CHK_BITS)
 
 // ---- stage timing (eucalc_profile_*) ----
 struct ProfRec {
@@ -672,6 +673,11 @@ int64_t eucalc_launch_count(int reset) {
     if (reset) g_launches = 0;
     return v;
 }
+int64_t eucalc_k2_restarts(int reset) {
+    int64_t v = g_k2_restarts.load();
+    if (reset) g_k2_restarts = 0;
+    return v;
+}
 
 eucalc_status eucalc_build_complex(const void *img, int dtype, int ndim, const int64_t *shape, int64_t batch,
                                    int construction, void *stream, eucalc_complex **out) {
@@ -1207,6 +1213,13 @@ eucalc_status transforms_impl(const eucalc_critical *ccr, const int32_t *dirs, i
         a.sum16 = cr->max_abs_sum < 32768;
         a.max_rec = cr->max_rec;
         a.max_abs_sum = cr->max_abs_sum;
+        a.no_chk = getenv("EUCALC_K2_NO_CHK") != nullptr;
+        {
+            int k = 14;  // test hook: a narrower checked range forces the split-bin restart
+            if (const char *v = getenv("EUCALC_K2_CHK_BITS")) k = std::max(1, std::min(14, atoi(v)));
+            a.chk_bias = (1u << k) * 0x10001u;
+            a.chk_mask = ((0xffffu << (k + 1)) & 0xffffu) * 0x10001u;
+        }
         int64_t scap = 0;
         const size_t sbytes = k2_stage_bytes(a, num_sms(), &scap);
         if (sbytes) {
@@ -1216,6 +1229,12 @@ eucalc_status transforms_impl(const eucalc_critical *ccr, const int32_t *dirs, i
         }
         ProfScope ps("k2_transforms", st);
         e = launch_k2(a, st, num_sms());
+        if (e == cudaSuccess && getenv("EUCALC_K2_CHK_BITS")) {  // test hook: read the restart count
+            unsigned r = 0;
+            e = cudaMemcpyAsync(&r, ticket + 3, sizeof(unsigned), cudaMemcpyDeviceToHost, st);
+            if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+            g_k2_restarts += r;
+        }
     }
     if (e == cudaSuccess && host_out) {
         // copy back: offsets first (to learn the exact totals), then the used entries

@@ -177,6 +177,8 @@ struct K2Args {
     int sparse_max;             // lists of <= sparse_max (<= 32) records: register sort instead of histogram
     bool sum16;                 // every list's sum |a|+|b| < 2^15: (wj, wc) prefix sums fit packed 16+16 bits
     int64_t max_rec, max_abs_sum;  // K1 statistics: max |a|+|b| of a record, max list sum of |a|+|b|
+    bool no_chk;                // block regime: never use checked packed bins (EUCALC_K2_NO_CHK, tests)
+    unsigned chk_bias, chk_mask;  // checked packed bins: fields in [-2^k, 2^k), k = 14 (EUCALC_K2_CHK_BITS, tests)
     void *stage;                // block regime: per-CTA output staging (k2_stage_bytes), or NULL
     int64_t stage_cap;          // entries per staged array per CTA
     // fused HT (NEXT f2): kbar table (fp64) over u in [ht_U0, ...), or NULL

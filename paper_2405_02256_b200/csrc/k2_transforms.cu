@@ -141,6 +141,23 @@ struct Hist {
             if (wj) atomicAdd(j + w, (unsigned)wj);
         }
     }
+    // PACK, checked: the same add, returning nonzero if the bin's new packed word
+    // leaves [-2^14, 2^14) in either field. The atomic's old value is the exact sum
+    // of the adds before it in the bin's atomic order; if every such prefix stayed
+    // in range, one more record (|field| <= max_rec < 2^14) cannot wrap a field, so
+    // the first prefix that leaves the range is decoded exactly and flagged. No flag
+    // anywhere => every bin's final sums are in range and the packed words exact.
+    // (x + 2^14 in both fields has bits 15 and 31 clear iff both are in range:
+    // bias 0x40004000, mask 0x80008000; EUCALC_K2_CHK_BITS < 14 narrows the range
+    // for tests.)
+    // Returns the biased new word; the caller ORs these and tests the OR against
+    // the mask once ((x & m) | (y & m) = (x | y) & m).
+    __device__ __forceinline__ unsigned add_chk(int bin, int wc, int wj, unsigned bias) const {
+        const int w = SWZ ? swz(bin) : bin;
+        const unsigned v = (unsigned)(wj * 65536 + wc);
+        const unsigned old = atomicAdd(c + w, v);
+        return old + v + bias;
+    }
     // PACK only: the raw packed words of bins b0..b0+3 (b0 % 4 == 0), optionally cleared
     __device__ __forceinline__ void load4raw(int b0, unsigned (&u)[4], bool clear) const {
         if constexpr (SWZ) {
@@ -848,10 +865,12 @@ constexpr size_t kBlockSmem = 200 * 1024;
 // the warp's lanes stride the range, four records in flight per lane (the list
 // streams from L2; a lone load per lane leaves the SM latency-bound).
 // U: records in flight per thread; DP as decode; CHECK: skip records outside
-// the window (false when the window covers the whole height range).
-template <int U, int DP, bool CHECK, typename RecT, bool PACK, bool SWZ>
+// the window (false when the window covers the whole height range); CHK: checked
+// packed adds (Hist::add_chk), biased words OR-ed into `bad`.
+template <int U, int DP, bool CHECK, bool CHK, typename RecT, bool PACK, bool SWZ>
 __device__ __forceinline__ void fill_range_t(const K2Args &a, const RecT *list, int beg, int end, const DirInfo &di,
-                                             int lo, int wbins, const Hist<PACK, SWZ> &hs, int lane, int step) {
+                                             int lo, int wbins, const Hist<PACK, SWZ> &hs, int lane, int step,
+                                             unsigned &bad) {
     int i = beg + lane;
     for (; i + (U - 1) * step < end; i += U * step) {
         RecT r[U];
@@ -862,22 +881,37 @@ __device__ __forceinline__ void fill_range_t(const K2Args &a, const RecT *list, 
             int bin, wc, wj;
             decode<DP>(r[u], di, a, bin, wc, wj);
             bin -= lo;
-            if (!CHECK || (unsigned)bin < (unsigned)wbins) hs.add(bin, wc, wj);
+            if (!CHECK || (unsigned)bin < (unsigned)wbins) {
+                if constexpr (CHK) bad |= hs.add_chk(bin, wc, wj, a.chk_bias);
+                else hs.add(bin, wc, wj);
+            }
         }
     }
     for (; i < end; i += step) {
         int bin, wc, wj;
         decode<DP>(list[i], di, a, bin, wc, wj);
         bin -= lo;
-        if (!CHECK || (unsigned)bin < (unsigned)wbins) hs.add(bin, wc, wj);
+        if (!CHECK || (unsigned)bin < (unsigned)wbins) {
+            if constexpr (CHK) bad |= hs.add_chk(bin, wc, wj, a.chk_bias);
+            else hs.add(bin, wc, wj);
+        }
     }
 }
 
-template <int U, int DP, typename RecT, bool PACK, bool SWZ>
+// CHK: checked adds when `chk` (run-time uniform: a segment whose packed bins are
+// proven exact skips the check and the atomics' return values).
+template <int U, int DP, bool CHK, typename RecT, bool PACK, bool SWZ>
 __device__ __forceinline__ void fill_range(const K2Args &a, const RecT *list, int beg, int end, const DirInfo &di,
-                                           int lo, int wbins, const Hist<PACK, SWZ> &hs, int lane, int step) {
-    if (lo == 0 && wbins >= di.R) fill_range_t<U, DP, false>(a, list, beg, end, di, lo, wbins, hs, lane, step);
-    else fill_range_t<U, DP, true>(a, list, beg, end, di, lo, wbins, hs, lane, step);
+                                           int lo, int wbins, const Hist<PACK, SWZ> &hs, int lane, int step,
+                                           unsigned &bad, bool chk) {
+    const bool whole = lo == 0 && wbins >= di.R;
+    if (CHK && chk) {
+        if (whole) fill_range_t<U, DP, false, CHK>(a, list, beg, end, di, lo, wbins, hs, lane, step, bad);
+        else fill_range_t<U, DP, true, CHK>(a, list, beg, end, di, lo, wbins, hs, lane, step, bad);
+    } else {
+        if (whole) fill_range_t<U, DP, false, false>(a, list, beg, end, di, lo, wbins, hs, lane, step, bad);
+        else fill_range_t<U, DP, true, false>(a, list, beg, end, di, lo, wbins, hs, lane, step, bad);
+    }
 }
 
 // Height range (bins relative to hlo) of K1 tile t: a TZ x TY x TX box of
@@ -913,12 +947,13 @@ __device__ __forceinline__ void tile_bins(const K2Args &a, const DirInfo &di, in
 // of once per window.
 constexpr int kMaxHitTiles = 4096;  // culled-tile list in shared memory
 
-template <int DP, typename RecT, bool PACK, bool SWZ>
+template <int DP, bool CHK, typename RecT, bool PACK, bool SWZ>
 __device__ void fill_window(const K2Args &a, const RecT *list, const int32_t *toff, int n, const DirInfo &di,
-                            int lo, int wbins, bool cull, const Hist<PACK, SWZ> &hs, int *s_hit, int *s_nhit) {
+                            int lo, int wbins, bool cull, const Hist<PACK, SWZ> &hs, int *s_hit, int *s_nhit,
+                            unsigned &bad, bool chk) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     if (!cull) {
-        fill_range<8, DP>(a, list, 0, n, di, lo, wbins, hs, threadIdx.x, kBlockThreads);
+        fill_range<8, DP, CHK>(a, list, 0, n, di, lo, wbins, hs, threadIdx.x, kBlockThreads, bad, chk);
         return;
     }
     if (a.ntiles <= kMaxHitTiles) {
@@ -935,7 +970,7 @@ __device__ void fill_window(const K2Args &a, const RecT *list, const int32_t *to
         const int nhit = *s_nhit;
         for (int k = warp; k < nhit; k += kBlockWarps) {
             const int tt = s_hit[k];
-            fill_range<4, DP>(a, list, toff[tt], toff[tt + 1], di, lo, wbins, hs, lane, 32);
+            fill_range<4, DP, CHK>(a, list, toff[tt], toff[tt + 1], di, lo, wbins, hs, lane, 32, bad, chk);
         }
         return;
     }
@@ -951,7 +986,7 @@ __device__ void fill_window(const K2Args &a, const RecT *list, const int32_t *to
         while (m) {
             const int tt = t0 + __ffs(m) - 1;
             m &= m - 1;
-            fill_range<4, DP>(a, list, toff[tt], toff[tt + 1], di, lo, wbins, hs, lane, 32);
+            fill_range<4, DP, CHK>(a, list, toff[tt], toff[tt + 1], di, lo, wbins, hs, lane, 32, bad, chk);
         }
     }
 }
@@ -967,10 +1002,32 @@ struct BlockShared {
 
 // One segment (image b, direction d) of the block regime with histogram bins of
 // kind PACK over windows of `win` bins (`hist` holds win words per array).
+// PACK: every fill checks its adds (Hist::add_chk) against chk_mask (0 when a
+// bound proves the packed bins exact); on a flag, before anything of the segment
+// reaches global memory, it returns false (the caller reruns the segment with
+// split bins); else true.
 template <bool PACK, int DP, typename RecT, typename OutT>
-__device__ __forceinline__ void block_segment(const K2Args &a, const OutPtrs<OutT> &outp, unsigned *hist, int win,
-                                              long long s, long long b, long long d, BlockShared &sh) {
+__device__ __forceinline__ bool block_segment(const K2Args &a, const OutPtrs<OutT> &outp, unsigned *hist, int win,
+                                              long long s, long long b, long long d, BlockShared &sh,
+                                              unsigned chk_mask) {
+    constexpr bool CHK = PACK;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    unsigned bad = 0;
+    // after a checked fill: restart with split bins if any add left the range
+    auto overflowed = [&]() -> bool {
+        if constexpr (CHK) {
+            if (__syncthreads_or(bad & chk_mask)) {
+                if (threadIdx.x == 0) atomicAdd(a.ticket + 3, 1u);  // eucalc_k2_restarts
+                for (int i = threadIdx.x; i < win; i += kBlockThreads) hist[i] = 0;
+                __syncthreads();
+                return true;
+            }
+            return false;
+        } else {
+            __syncthreads();
+            return false;
+        }
+    };
     Hist<PACK, true> hs;
     hs.c = hist;
     hs.j = hist + win;
@@ -999,8 +1056,8 @@ __device__ __forceinline__ void block_segment(const K2Args &a, const OutPtrs<Out
         const long long ht_off = outp.tab ? ht_tab_off(a, di) : 0;
         for (int w = 0; w < nwin; ++w) {
             const int lo = w * win, wb = min(win, di.R - lo);
-            fill_window<DP>(a, list, toff, n, di, lo, wb, cull, hs, sh.hit, &sh.nhit);
-            __syncthreads();
+            fill_window<DP, CHK>(a, list, toff, n, di, lo, wb, cull, hs, sh.hit, &sh.nhit, bad, chk_mask != 0);
+            if (overflowed()) return false;
             const int b0 = min(wb, warp * per), b1 = min(wb, b0 + per);
             int c = 0, o = 0, sc = 0, sj = 0;
             for (int base = b0; base < b1; base += kGroup) {
@@ -1084,14 +1141,14 @@ __device__ __forceinline__ void block_segment(const K2Args &a, const OutPtrs<Out
                 ht_write(a, s, t);
             }
         }
-        return;
+        return true;
     }
     // phase A: counts over all windows
     long long nc = 0, no = 0;
     for (int w = 0; w < nwin; ++w) {
         const int lo = w * win, wb = min(win, di.R - lo);
-        fill_window<DP>(a, list, toff, n, di, lo, wb, cull, hs, sh.hit, &sh.nhit);
-        __syncthreads();
+        fill_window<DP, CHK>(a, list, toff, n, di, lo, wb, cull, hs, sh.hit, &sh.nhit, bad, chk_mask != 0);
+        if (overflowed()) return false;
         int c = 0, o = 0;
         const int b0 = min(wb, warp * per), b1 = min(wb, b0 + per);
         for (int base = b0; base < b1; base += kGroup) count_group(hs, base, c, o, nwin > 1);
@@ -1126,7 +1183,9 @@ __device__ __forceinline__ void block_segment(const K2Args &a, const OutPtrs<Out
     for (int w = 0; w < nwin; ++w) {
         const int lo = w * win, wb = min(win, di.R - lo);
         if (nwin > 1) {
-            fill_window<DP>(a, list, toff, n, di, lo, wb, cull, hs, sh.hit, &sh.nhit);
+            // unchecked: phase A's checks proved every bin's final sums in range, and
+            // packed sums are exact for in-range finals whatever the add order
+            fill_window<DP, false>(a, list, toff, n, di, lo, wb, cull, hs, sh.hit, &sh.nhit, bad, false);
             __syncthreads();
         }
         const int b0 = min(wb, warp * per), b1 = min(wb, b0 + per);
@@ -1187,6 +1246,7 @@ __device__ __forceinline__ void block_segment(const K2Args &a, const OutPtrs<Out
             ht_write(a, s, t);
         }
     }
+    return true;
 }
 
 // Block regime. A segment uses packed 16+16 bins (one atomic per record, windows
@@ -1208,8 +1268,11 @@ __global__ void __launch_bounds__(kBlockThreads, 1) k2_block(K2Args a, long long
         if (s >= nseg) break;
         const long long b = s / a.D, d = s % a.D;
         const long long bin_bound = min((long long)a.dirs[d].line * (long long)a.max_rec, (long long)a.max_abs_sum);
-        if (bin_bound < 32768) block_segment<true, DP, RecT, OutT>(a, outp, hist, 2 * win, s, b, d, sh);
-        else block_segment<false, DP, RecT, OutT>(a, outp, hist, win, s, b, d, sh);
+        // packed bins: proven exact (no check), or checked (restart split on a flag)
+        const bool proven = bin_bound < 32768;
+        if (!(proven || (a.max_rec < 16384 && !a.no_chk)) ||
+            !block_segment<true, DP, RecT, OutT>(a, outp, hist, 2 * win, s, b, d, sh, proven ? 0u : a.chk_mask))
+            block_segment<false, DP, RecT, OutT>(a, outp, hist, win, s, b, d, sh, 0u);
     }
 }
 

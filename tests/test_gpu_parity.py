@@ -169,6 +169,29 @@ def test_block_regime_3d_culled_windows():
     check_transforms(vol, dirs, "vertex", res)
 
 
+@pytest.mark.parametrize("env", [{}, {"EUCALC_K2_CHK_BITS": "1"}, {"EUCALC_K2_CHK_BITS": "6"},
+                                 {"EUCALC_K2_NO_CHK": "1"}], ids=["checked", "restart", "partial", "split"])
+def test_block_regime_checked_packed_bins(env, monkeypatch):
+    """Block regime with packed 16+16 bins whose exactness no bound proves: every
+    add is checked and a flagged segment restarts with split bins. The test hooks
+    narrow the checked range (bits 1: every segment restarts; bits 6: some do) or
+    disable the packed path; all must give the oracle's exact representations."""
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    eu.k2_restarts(reset=True)
+    vol = synth.smooth_volume(64, 78)[None]
+    # small coordinates: many vertices per height level, so no bound proves the packed bins
+    dirs = np.array([[1, 1, 1], [2, -1, 3], [-1, 2, 1], [3, -2, -1], [1, -1, 2], [-2, -3, -1]], np.int32)
+    cx, cr, res = run_gpu(vol, dirs, "vertex")
+    check_transforms(vol, dirs, "vertex", res)
+    if env.get("EUCALC_K2_CHK_BITS") == "1":  # every unproven segment restarted
+        assert eu.k2_restarts() == len(dirs)
+    img = np.stack([synth.grf_image(160, 6), 255 - synth.grf_image(160, 7)])
+    d2 = np.concatenate([synth.random_directions(4, 2, 90, 6), np.array([[90, -89]], np.int32)])
+    cx, cr, res = run_gpu(img, d2, "top")
+    check_transforms(img, d2, "top", res)
+
+
 def test_negative_and_int32_weights():
     rng = np.random.default_rng(3)
     images = rng.integers(-40000, 40000, size=(2, 12, 11)).astype(np.int32)
