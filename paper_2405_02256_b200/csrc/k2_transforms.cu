@@ -50,14 +50,22 @@ __device__ __forceinline__ unsigned long long pack2(long long c, long long o) {
     return ((unsigned long long)c << 31) | (unsigned long long)o;
 }
 
+// Publishes segment s's aggregate (s = 0: its inclusive prefix) for the look-backs
+// of later segments (lane 0 of the calling warp).
+__device__ __forceinline__ void seg_publish(unsigned long long *flags, long long s, long long nc, long long no) {
+    if ((threadIdx.x & 31) == 0) st_relaxed(flags + s, (s == 0 ? kIncl : kAgg) | pack2(nc, no));
+}
+
 // Warp-wide look-back over segment flags (status | nc:31 | no:31). Returns the
-// exclusive prefixes (nc, no) of segment s and publishes its inclusive prefix.
+// exclusive prefixes (nc, no) of segment s and publishes its inclusive prefix;
+// PUBLISHED: its aggregate is already out (seg_publish).
+template <bool PUBLISHED = false>
 __device__ void seg_lookback(unsigned long long *flags, long long s, long long nc, long long no,
                              long long &exc_c, long long &exc_o) {
     const int lane = threadIdx.x & 31;
     long long ec = 0, eo = 0;
     if (s > 0) {
-        if (lane == 0) st_relaxed(flags + s, kAgg | pack2(nc, no));
+        if (!PUBLISHED && lane == 0) st_relaxed(flags + s, kAgg | pack2(nc, no));
         long long j = s - 1;
         while (true) {
             long long idx = j - lane;
@@ -993,6 +1001,7 @@ __device__ void fill_window(const K2Args &a, const RecT *list, const int32_t *to
 
 struct BlockShared {
     long long seg;
+    int cnt[2];                // staged segment: (nc, no)
     int wsum[kBlockWarps][4];  // per-warp (nc, no, sum wc, sum wj)
     long long exc[2];
     double ht[kBlockWarps];
@@ -1040,109 +1049,6 @@ __device__ __forceinline__ bool block_segment(const K2Args &a, const OutPtrs<Out
     const bool cull = nwin > 1 && a.ntiles > 1;
     // each warp owns a contiguous, 128-aligned range of the window
     const int per = ((win / kBlockWarps) + kGroup - 1) / kGroup * kGroup;
-    if (a.stage && nwin > 1) {
-        // ONE fill per window: the window's entries go to this CTA's staging at
-        // segment-local positions; after the look-back they are copied to the CSR.
-        OutPtrs<OutT> scr = outp;
-        OutT *base = reinterpret_cast<OutT *>(a.stage) + (long long)blockIdx.x * 6 * a.stage_cap;
-        scr.eh = base;
-        scr.ev = base + a.stage_cap;
-        scr.cv = base + 2 * a.stage_cap;
-        scr.ch = base + 3 * a.stage_cap;
-        scr.oh = base + 4 * a.stage_cap;
-        scr.ov = base + 5 * a.stage_cap;
-        int pc_carry = 0, po_carry = 0, e_carry = 0, r_carry = 0;
-        double ht = 0.0;
-        const long long ht_off = outp.tab ? ht_tab_off(a, di) : 0;
-        for (int w = 0; w < nwin; ++w) {
-            const int lo = w * win, wb = min(win, di.R - lo);
-            fill_window<DP, CHK>(a, list, toff, n, di, lo, wb, cull, hs, sh.hit, &sh.nhit, bad, chk_mask != 0);
-            if (overflowed()) return false;
-            const int b0 = min(wb, warp * per), b1 = min(wb, b0 + per);
-            int c = 0, o = 0, sc = 0, sj = 0;
-            for (int base = b0; base < b1; base += kGroup) {
-                int wc[4], wj[4];
-                hs.load4(base + 4 * lane, wc, wj, false);
-#pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                    c += wc[q] != 0;
-                    o += wj[q] != 0;
-                    sc += wc[q];
-                    sj += wj[q];
-                }
-            }
-            c = warp_sum(c);
-            o = warp_sum(o);
-            sc = warp_sum(sc);
-            sj = warp_sum(sj);
-            if (lane == 0) {
-                sh.wsum[warp][0] = c;
-                sh.wsum[warp][1] = o;
-                sh.wsum[warp][2] = sc;
-                sh.wsum[warp][3] = sj;
-            }
-            __syncthreads();
-            int pc = pc_carry, po = po_carry, er = e_carry, rr = r_carry;
-            int tc = 0, to = 0, tsc = 0, tsj = 0;
-            for (int k = 0; k < kBlockWarps; ++k) {
-                if (k < warp) {
-                    pc += sh.wsum[k][0];
-                    po += sh.wsum[k][1];
-                    er += sh.wsum[k][2];
-                    rr += sh.wsum[k][3];
-                }
-                tc += sh.wsum[k][0];
-                to += sh.wsum[k][1];
-                tsc += sh.wsum[k][2];
-                tsj += sh.wsum[k][3];
-            }
-            for (int base = b0; base < b1; base += kGroup)
-                emit_group<kModeAny>(scr, hs, base, di.hlo + lo, er, rr, pc, po, ht, ht_off);
-            pc_carry += tc;
-            po_carry += to;
-            e_carry += tsc;
-            r_carry += tsj;
-            __syncthreads();
-        }
-        if (warp == 0) {
-            long long ec, eo;
-            seg_lookback(a.flags, s, pc_carry, po_carry, ec, eo);
-            if (lane == 0) {
-                sh.exc[0] = ec;
-                sh.exc[1] = eo;
-                write_offsets(a, s, ec, eo, pc_carry, po_carry);
-            }
-        }
-        __syncthreads();
-        const long long ec = sh.exc[0], eo = sh.exc[1];
-        for (int i = threadIdx.x; i < pc_carry; i += kBlockThreads) {
-            if (outp.ect) {
-                outp.eh[ec + i] = scr.eh[i];
-                outp.ev[ec + i] = scr.ev[i];
-            }
-            if (outp.cls) {
-                if (!outp.alias) outp.ch[ec + i] = scr.ch[i];
-                outp.cv[ec + i] = scr.cv[i];
-            }
-        }
-        if (outp.ord) {
-            for (int i = threadIdx.x; i < po_carry; i += kBlockThreads) {
-                outp.oh[eo + i] = scr.oh[i];
-                outp.ov[eo + i] = scr.ov[i];
-            }
-        }
-        if (outp.tab) {
-            for (int k = 16; k; k >>= 1) ht += __shfl_xor_sync(0xffffffffu, ht, k);
-            if (lane == 0) sh.ht[warp] = ht;
-            __syncthreads();
-            if (threadIdx.x == 0) {
-                double t = 0.0;
-                for (int k = 0; k < kBlockWarps; ++k) t += sh.ht[k];
-                ht_write(a, s, t);
-            }
-        }
-        return true;
-    }
     // phase A: counts over all windows
     long long nc = 0, no = 0;
     for (int w = 0; w < nwin; ++w) {
@@ -1249,6 +1155,180 @@ __device__ __forceinline__ bool block_segment(const K2Args &a, const OutPtrs<Out
     return true;
 }
 
+// Staged variant (the pipelined block kernel): ONE fill per window, the
+// segment's entries go to the staging buffer `base` at segment-local positions;
+// its counts end in sh.cnt (nc, no) and its HT (if fused) is written. Nothing is
+// published. Returns false when a checked packed fill flagged (rerun split).
+template <bool PACK, int DP, typename RecT, typename OutT>
+__device__ __forceinline__ bool block_segment_staged(const K2Args &a, const OutPtrs<OutT> &outp, unsigned *hist,
+                                                     int win, long long s, long long b, long long d,
+                                                     BlockShared &sh, unsigned chk_mask, OutT *base) {
+    constexpr bool CHK = PACK;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    unsigned bad = 0;
+    auto overflowed = [&]() -> bool {
+        if constexpr (CHK) {
+            if (__syncthreads_or(bad & chk_mask)) {
+                if (threadIdx.x == 0) atomicAdd(a.ticket + 3, 1u);  // eucalc_k2_restarts
+                for (int i = threadIdx.x; i < win; i += kBlockThreads) hist[i] = 0;
+                __syncthreads();
+                return true;
+            }
+            return false;
+        } else {
+            __syncthreads();
+            return false;
+        }
+    };
+    Hist<PACK, true> hs;
+    hs.c = hist;
+    hs.j = hist + win;
+    const RecT *recs = reinterpret_cast<const RecT *>(a.rec);
+    const DirInfo di = a.dirs[d];
+    const RecT *list = recs + (b * a.Q + di.q) * a.vcap;
+    const int32_t *toff = a.tile_off + (b * a.Q + di.q) * (long long)(a.ntiles + 1);
+    const int n = a.count[b * a.Q + di.q];
+    const int nwin = (di.R + win - 1) / win;
+    const bool cull = nwin > 1 && a.ntiles > 1;
+    const int per = ((win / kBlockWarps) + kGroup - 1) / kGroup * kGroup;
+    OutPtrs<OutT> scr = outp;
+    scr.eh = base;
+    scr.ev = base + a.stage_cap;
+    scr.cv = base + 2 * a.stage_cap;
+    scr.ch = base + 3 * a.stage_cap;
+    scr.oh = base + 4 * a.stage_cap;
+    scr.ov = base + 5 * a.stage_cap;
+    scr.ect = outp.ect || outp.cls;  // staged heights serve both (T_c = T)
+    scr.alias = true;
+    int pc_carry = 0, po_carry = 0, e_carry = 0, r_carry = 0;
+    double ht = 0.0;
+    const long long ht_off = outp.tab ? ht_tab_off(a, di) : 0;
+    for (int w = 0; w < nwin; ++w) {
+        const int lo = w * win, wb = min(win, di.R - lo);
+        fill_window<DP, CHK>(a, list, toff, n, di, lo, wb, cull, hs, sh.hit, &sh.nhit, bad, chk_mask != 0);
+        if (overflowed()) return false;
+        const int b0 = min(wb, warp * per), b1 = min(wb, b0 + per);
+        int c = 0, o = 0, sc = 0, sj = 0;
+        for (int base = b0; base < b1; base += kGroup) {
+            int wc[4], wj[4];
+            hs.load4(base + 4 * lane, wc, wj, false);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                c += wc[q] != 0;
+                o += wj[q] != 0;
+                sc += wc[q];
+                sj += wj[q];
+            }
+        }
+        c = warp_sum(c);
+        o = warp_sum(o);
+        sc = warp_sum(sc);
+        sj = warp_sum(sj);
+        if (lane == 0) {
+            sh.wsum[warp][0] = c;
+            sh.wsum[warp][1] = o;
+            sh.wsum[warp][2] = sc;
+            sh.wsum[warp][3] = sj;
+        }
+        __syncthreads();
+        int pc = pc_carry, po = po_carry, er = e_carry, rr = r_carry;
+        int tc = 0, to = 0, tsc = 0, tsj = 0;
+        for (int k = 0; k < kBlockWarps; ++k) {
+            if (k < warp) {
+                pc += sh.wsum[k][0];
+                po += sh.wsum[k][1];
+                er += sh.wsum[k][2];
+                rr += sh.wsum[k][3];
+            }
+            tc += sh.wsum[k][0];
+            to += sh.wsum[k][1];
+            tsc += sh.wsum[k][2];
+            tsj += sh.wsum[k][3];
+        }
+        for (int base = b0; base < b1; base += kGroup)
+            emit_group<kModeAny>(scr, hs, base, di.hlo + lo, er, rr, pc, po, ht, ht_off);
+        pc_carry += tc;
+        po_carry += to;
+        e_carry += tsc;
+        r_carry += tsj;
+        __syncthreads();
+    }
+    if (outp.tab) {  // fused HT: warp partials, then a fixed-order sum over warps
+        for (int k = 16; k; k >>= 1) ht += __shfl_xor_sync(0xffffffffu, ht, k);
+        if (lane == 0) sh.ht[warp] = ht;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            double t = 0.0;
+            for (int k = 0; k < kBlockWarps; ++k) t += sh.ht[k];
+            ht_write(a, s, t);
+        }
+    }
+    if (threadIdx.x == 0) {
+        sh.cnt[0] = pc_carry;
+        sh.cnt[1] = po_carry;
+    }
+    return true;
+}
+
+// Staged entries of a resolved segment -> the CSR (four loads in flight per thread).
+template <typename OutT>
+__device__ __forceinline__ void copy_out(const OutPtrs<OutT> &outp, const OutT *base, long long cap, long long ec,
+                                         long long eo, int nc, int no) {
+    const OutT *eh = base, *ev = base + cap, *cv = base + 2 * cap, *ch = base + 3 * cap, *oh = base + 4 * cap,
+               *ov = base + 5 * cap;
+    constexpr int U = 4;
+    if (outp.ect || outp.cls) {
+        for (int i0 = threadIdx.x; i0 < nc; i0 += U * kBlockThreads) {
+            OutT h[U], v[U], c[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int i = i0 + u * kBlockThreads;
+                if (i < nc) {
+                    h[u] = eh[i];
+                    v[u] = ev[i];
+                    c[u] = cv[i];
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int i = i0 + u * kBlockThreads;
+                if (i < nc) {
+                    if (outp.ect) {
+                        outp.eh[ec + i] = h[u];
+                        outp.ev[ec + i] = v[u];
+                    }
+                    if (outp.cls) {
+                        if (!outp.alias) outp.ch[ec + i] = h[u];
+                        outp.cv[ec + i] = c[u];
+                    }
+                }
+            }
+        }
+    }
+    if (outp.ord) {
+        for (int i0 = threadIdx.x; i0 < no; i0 += U * kBlockThreads) {
+            OutT h[U], v[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int i = i0 + u * kBlockThreads;
+                if (i < no) {
+                    h[u] = oh[i];
+                    v[u] = ov[i];
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int i = i0 + u * kBlockThreads;
+                if (i < no) {
+                    outp.oh[eo + i] = h[u];
+                    outp.ov[eo + i] = v[u];
+                }
+            }
+        }
+    }
+    (void)ch;
+}
+
 // Block regime. A segment uses packed 16+16 bins (one atomic per record, windows
 // of 2*win bins) when its bins provably stay below 2^15: every bin holds at most
 // di.line records (the vertices of one height level) of |a|+|b| <= max_rec, and
@@ -1260,6 +1340,62 @@ __global__ void __launch_bounds__(kBlockThreads, 1) k2_block(K2Args a, long long
     __shared__ BlockShared sh;
     const OutPtrs<OutT> outp(a);
     for (int i = threadIdx.x; i < 2 * win; i += kBlockThreads) hist[i] = 0;
+    // packed bins: proven exact (no check), or checked (rerun split on a flag)
+    auto packed_mask = [&](long long d, bool &use_packed) -> unsigned {
+        const long long bin_bound = min((long long)a.dirs[d].line * (long long)a.max_rec, (long long)a.max_abs_sum);
+        const bool proven = bin_bound < 32768;
+        use_packed = proven || (a.max_rec < 16384 && !a.no_chk);
+        return proven ? 0u : a.chk_mask;
+    };
+    if (a.stage) {
+        // Pipelined: segment s is filled and emitted into staging buffer `cur` and
+        // its aggregate published; then the PREVIOUS segment of this CTA is looked
+        // back (its predecessors have had a whole segment's time to publish) and
+        // copied from the other buffer to the CSR.
+        int cur = 0;
+        long long prev = -1;
+        int pnc = 0, pno = 0;
+        OutT *stage = reinterpret_cast<OutT *>(a.stage);
+        while (true) {
+            __syncthreads();
+            if (threadIdx.x == 0) sh.seg = (long long)atomicAdd(a.ticket, 1u);
+            __syncthreads();
+            const long long s = sh.seg;
+            int nc = 0, no = 0;
+            if (s < nseg) {
+                const long long b = s / a.D, d = s % a.D;
+                OutT *buf = stage + ((long long)blockIdx.x * 2 + cur) * 6 * a.stage_cap;
+                bool packed;
+                const unsigned m = packed_mask(d, packed);
+                if (!packed || !block_segment_staged<true, DP, RecT, OutT>(a, outp, hist, 2 * win, s, b, d, sh, m, buf))
+                    block_segment_staged<false, DP, RecT, OutT>(a, outp, hist, win, s, b, d, sh, 0u, buf);
+                __syncthreads();
+                nc = sh.cnt[0];
+                no = sh.cnt[1];
+                if (threadIdx.x == 0) seg_publish(a.flags, s, nc, no);
+            }
+            if (prev >= 0) {
+                if (threadIdx.x < 32) {
+                    long long ec, eo;
+                    seg_lookback<true>(a.flags, prev, pnc, pno, ec, eo);
+                    if (threadIdx.x == 0) {
+                        sh.exc[0] = ec;
+                        sh.exc[1] = eo;
+                        write_offsets(a, prev, ec, eo, pnc, pno);
+                    }
+                }
+                __syncthreads();
+                const OutT *pbuf = stage + ((long long)blockIdx.x * 2 + (cur ^ 1)) * 6 * a.stage_cap;
+                copy_out(outp, pbuf, a.stage_cap, sh.exc[0], sh.exc[1], pnc, pno);
+            }
+            if (s >= nseg) break;
+            prev = s;
+            pnc = nc;
+            pno = no;
+            cur ^= 1;
+        }
+        return;
+    }
     while (true) {
         __syncthreads();
         if (threadIdx.x == 0) sh.seg = (long long)atomicAdd(a.ticket, 1u);
@@ -1267,11 +1403,9 @@ __global__ void __launch_bounds__(kBlockThreads, 1) k2_block(K2Args a, long long
         const long long s = sh.seg;
         if (s >= nseg) break;
         const long long b = s / a.D, d = s % a.D;
-        const long long bin_bound = min((long long)a.dirs[d].line * (long long)a.max_rec, (long long)a.max_abs_sum);
-        // packed bins: proven exact (no check), or checked (restart split on a flag)
-        const bool proven = bin_bound < 32768;
-        if (!(proven || (a.max_rec < 16384 && !a.no_chk)) ||
-            !block_segment<true, DP, RecT, OutT>(a, outp, hist, 2 * win, s, b, d, sh, proven ? 0u : a.chk_mask))
+        bool packed;
+        const unsigned m = packed_mask(d, packed);
+        if (!packed || !block_segment<true, DP, RecT, OutT>(a, outp, hist, 2 * win, s, b, d, sh, m))
             block_segment<false, DP, RecT, OutT>(a, outp, hist, win, s, b, d, sh, 0u);
     }
 }
@@ -1360,7 +1494,7 @@ size_t k2_stage_bytes(const K2Args &a, int num_sms, int64_t *cap) {
     // per stream and segment: at most min(list length, R) entries
     const int64_t c = std::max<int64_t>(1, std::min<int64_t>(a.max_count, a.R_max));
     const long long grid = std::min<long long>(nseg, num_sms);
-    const size_t bytes = (size_t)grid * 6 * (size_t)c * (size_t)a.elem_bytes;
+    const size_t bytes = (size_t)grid * 2 * 6 * (size_t)c * (size_t)a.elem_bytes;  // two buffers per CTA
     if (bytes > (size_t(4) << 30)) return 0;
     *cap = c;
     return bytes;
