@@ -2,6 +2,7 @@
 // See include/eucalc.h for the contract of every entry point.
 #include <algorithm>
 #include <atomic>
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -64,6 +65,25 @@ struct ProfScope {
             cudaEventRecord(b, st);
             g_prof_recs.push_back(ProfRec{stage, a, b, g_launches - l0});
         }
+    }
+};
+
+// ---- host trace (EUCALC_HOST_TRACE=1: microseconds between marks, to stderr) ----
+struct HostTrace {
+    bool on = getenv("EUCALC_HOST_TRACE") != nullptr;
+    std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now(), last = t0;
+    const char *fn;
+    std::string line;
+    explicit HostTrace(const char *f) : fn(f) {}
+    void mark(const char *what) {
+        if (!on) return;
+        const auto t = std::chrono::steady_clock::now();
+        line += std::string(" ") + what + "=" +
+                std::to_string(std::chrono::duration_cast<std::chrono::microseconds>(t - last).count());
+        last = t;
+    }
+    ~HostTrace() {
+        if (on) fprintf(stderr, "[trace] %s:%s us\n", fn, line.c_str());
     }
 };
 
@@ -578,11 +598,12 @@ K1Args k1_args(const Critical *cr) {
         a.sh[k] = cx->sh[k];
     }
     int TX, TY, TZ, W;
-    k1_geometry(n, cx->M, &TX, &TY, &TZ, &W);
+    k1_geometry(n, cx->M, cx->dtype, cx->construction, &TX, &TY, &TZ, &W);
     a.TX = cr->TX;
     a.TY = cr->TY;
     a.TZ = cr->TZ;
     a.W = W;
+    a.walk = k1_walk(n, cx->M, cx->batch, cr->TX, cr->TY);
     a.tiles_x = cr->tiles_x;
     a.tiles_y = cr->tiles_y;
     a.tiles_z = cr->tiles_z;
@@ -819,7 +840,7 @@ eucalc_status eucalc_critical_points(const eucalc_complex *cx, void *stream, euc
     // tiles (K2's culling unit and K1's offset granularity): boxes of TX x TY x TZ
     // vertices, W pencils (warps) each (k1_critical.cu)
     int TX, TY, TZ, W;
-    k1_geometry(n, cx->M, &TX, &TY, &TZ, &W);
+    k1_geometry(n, cx->M, cx->dtype, cx->construction, &TX, &TY, &TZ, &W);
     const int MX = (int)cx->M[n - 1], MY = (int)cx->M[n - 2], MZ = n == 3 ? (int)cx->M[0] : 1;
     cr->TX = TX;
     cr->TY = TY;
@@ -839,7 +860,7 @@ eucalc_status eucalc_critical_points(const eucalc_complex *cx, void *stream, euc
     if (e == cudaSuccess) e = cudaMallocAsync(&cr->d_tile_off, sizeof(int32_t) * nlist * (cr->ntiles + 1), st);
     if (e == cudaSuccess) e = cudaMallocAsync(&cr->d_stats, sizeof(int64_t) * nstats, st);
     // records in fixed-capacity (tile, warp) regions before the copy to the lists
-    const int cap_r = 32 * (n == 3 ? TZ : TY / W);
+    const int cap_r = TX * (n == 3 ? TZ : TY / W);
     const int64_t scap = (int64_t)cr->ntiles * W * cap_r;
     const bool direct = (int64_t)cr->ntiles * W == 1;
     void *rscratch = nullptr;
@@ -1035,6 +1056,7 @@ struct HtReq {
 eucalc_status transforms_impl(const eucalc_critical *ccr, const int32_t *dirs, int64_t D, eucalc_steps *ect,
                               eucalc_steps *ordinary, eucalc_steps *classical, const HtReq *ht, int64_t *required_out,
                               void *stream) {
+    HostTrace tr("transforms");
     if (!ccr) return fail(EUCALC_E_STATE, "NULL handle");
     if (ht) {
         if (ht->kernel < EUCALC_K_GAUSS || ht->kernel > EUCALC_K_EXP) return fail(EUCALC_E_ARG, "bad kernel");
@@ -1051,6 +1073,7 @@ eucalc_status transforms_impl(const eucalc_critical *ccr, const int32_t *dirs, i
     std::shared_ptr<PlanEntry> pe;
     eucalc_status s = get_plan(cx, dirs, D, st, pe);
     if (s != EUCALC_OK) return s;
+    tr.mark("plan");
     const DirPlan &p = pe->p;
     if (ht) {
         // the fused HT tabulates kbar over the directions' whole u range (8 B per
@@ -1070,6 +1093,7 @@ eucalc_status transforms_impl(const eucalc_critical *ccr, const int32_t *dirs, i
     int64_t bnd = 0;
     s = bounds(cr, p, st, bnd);
     if (s != EUCALC_OK) return s;
+    tr.mark("bounds(k1 wait)");
     if (required_out) *required_out = bnd;
     eucalc_steps *outs[3] = {ect, ordinary, classical};
     int eb = 0;
@@ -1153,6 +1177,7 @@ eucalc_status transforms_impl(const eucalc_critical *ccr, const int32_t *dirs, i
         free_scratch();
         return fail(EUCALC_E_NOMEM, "scratch");
     }
+    tr.mark("checks+arena");
     unsigned long long *flags = (unsigned long long *)ar[0];
     unsigned int *ticket = (unsigned int *)(flags + S);
     int *cnts = (int *)ar[1];
@@ -1220,6 +1245,7 @@ eucalc_status transforms_impl(const eucalc_critical *ccr, const int32_t *dirs, i
             a.chk_bias = (1u << k) * 0x10001u;
             a.chk_mask = ((0xffffu << (k + 1)) & 0xffffu) * 0x10001u;
         }
+        tr.mark("memset+table+args");
         int64_t scap = 0;
         const size_t sbytes = k2_stage_bytes(a, num_sms(), &scap);
         if (sbytes) {
@@ -1227,8 +1253,10 @@ eucalc_status transforms_impl(const eucalc_critical *ccr, const int32_t *dirs, i
             a.stage_cap = a.stage ? scap : 0;
             if (!a.stage) cudaGetLastError();  // no staging: the block regime fills twice
         }
+        tr.mark("stage");
         ProfScope ps("k2_transforms", st);
         e = launch_k2(a, st, num_sms());
+        tr.mark("launch_k2");
         if (e == cudaSuccess && getenv("EUCALC_K2_CHK_BITS")) {  // test hook: read the restart count
             unsigned r = 0;
             e = cudaMemcpyAsync(&r, ticket + 3, sizeof(unsigned), cudaMemcpyDeviceToHost, st);

@@ -108,6 +108,7 @@ struct K1Args {
     int m[kMaxN], M[kMaxN];
     int TX, TY, TZ, tiles_x, tiles_y, tiles_z;
     int W;              // warps (pencils) per tile: 8 in 3-D (one per row), 1 in 2-D
+    int walk;           // 3-D: planes walked per CTA (k1_walk)
     int sh[kMaxN];
     void *rec;
     bool wide;
@@ -126,7 +127,9 @@ struct K1Args {
     int64_t *max_rec;
 };
 // K1 tile geometry for an image of ndim dims (vertex extents M).
-void k1_geometry(int ndim, const int64_t *M, int *TX, int *TY, int *TZ, int *W);
+void k1_geometry(int ndim, const int64_t *M, int dtype, int construction, int *TX, int *TY, int *TZ, int *W);
+// 3-D: planes walked per K1 CTA for a batch of images
+int k1_walk(int ndim, const int64_t *M, int64_t batch, int TX, int TY);
 // Look-back flags k1_scan needs for `lists` lists of ntiles * W counts.
 int64_t k1_scan_chunks(int64_t lists, int64_t ntiles, int W);
 cudaError_t launch_k1(const K1Args &a, cudaStream_t s);

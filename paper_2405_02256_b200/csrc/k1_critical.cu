@@ -599,6 +599,316 @@ __global__ void __launch_bounds__(kThreads, 3) k1_pencil(K1Args a) {
     }
 }
 
+// ------------------------------------------------------------------ 3-D VERTEX 8-bit: two vertices per lane
+// For 8-bit VERTEX images a missing vertex can carry the sentinel 0 instead of
+// -1: the masked cell value max(min(..., -1), 0) = 0 = min(..., 0) and every
+// real value is >= 0. Masking then disappears and every box min is a plain min
+// of values in [0, 255], so a lane can hold the columns x0 = 64 tx + 2 lane and
+// x0 + 1 as the two 16-bit halves of one register: the mins run as one
+// VIMNMX.U16x2 for both vertices, and the inclusion-exclusion subtractions as
+// one IADD3 each (a + K - b) with a bias K per level that keeps both halves
+// non-negative, so no borrow crosses from the low half into the high half:
+//   box mins            [0, 255]            bias 0
+//   x pass  v(0)-v(+-1) |.| <= 255          bias 256  (K1)
+//   y pass  (corners)   |.| <= 510          bias 512  (K2)
+//   Delta^- (walk axis) |.| <= 1020         bias 1024 (K3)
+// (each level's K exceeds the previous level's range, so every half stays in
+// [0, 2044]). The result is the same Delta^- as the scalar walk above, bit for
+// bit; only the arithmetic is packed. A warp covers 64 columns, so the tiles of
+// this variant are 64 x 8 x 8 vertices (k1_geometry).
+namespace v8 {
+constexpr uint32_t K1 = 0x01000100u, K2 = 0x02000200u, K3 = 0x04000400u, K4 = 0x08000800u;
+constexpr uint32_t kUnbias = 0xfc00fc00u;  // -1024 in each half (VIADD.16x2)
+
+__device__ __forceinline__ uint32_t mn(uint32_t a, uint32_t b) { return __vminu2(a, b); }
+
+// predicated loads (no branch, nothing dereferenced when !ok): a u16 pair of
+// columns, or one byte
+__device__ __forceinline__ uint32_t ld_u16(const uint8_t *p, bool ok) {
+    uint32_t v;
+    asm("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\tmov.u32 %0, 0;\n\t@q ld.global.nc.u16 %0, [%1];\n\t}"
+        : "=r"(v) : "l"(p), "r"((unsigned)ok));
+    return v;
+}
+__device__ __forceinline__ uint32_t ld_u8(const uint8_t *p, bool ok) {
+    uint32_t v;
+    asm("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\tmov.u32 %0, 0;\n\t@q ld.global.nc.u8 %0, [%1];\n\t}"
+        : "=r"(v) : "l"(p), "r"((unsigned)ok));
+    return v;
+}
+
+// One plane's raw values for a lane: rows y-1, y, y+1 as packed column pairs
+// (low half x0, high half x0+1) and the halo column (lane 0: x0-1 in the high
+// half, lane 31: x0+2 in the low half; 0 elsewhere).
+struct Raw {
+    uint32_t m[3], h[3];
+};
+
+// Loads of consecutive planes (AL: rows start on even addresses, so a column
+// pair is one u16 load). Lane pointers are fixed (row y-1, column x0, and the
+// halo column); the plane offset and the row stride are CTA-uniform, so the
+// per-step address arithmetic runs on the uniform datapath.
+template <bool AL>
+struct Cursor {
+    const uint8_t *bp, *hp;  // lane's (row y-1, column x0) and halo column of plane 0
+    long long po, pstride;   // uniform: offset of the next plane to load
+    int rstride, p, pend, hsh;
+    unsigned rmask;          // bit k: row y-1+k exists
+    bool ok0, ok1, hok;
+    __device__ __forceinline__ void init(const uint8_t *img, int MX, int MY, int MZ, int p0, int y, int x0) {
+        const int lane = threadIdx.x & 31;
+        const int hdx = lane == 0 ? -1 : 2;
+        hsh = lane == 0 ? 16 : 0;
+        ok0 = x0 < MX;
+        ok1 = x0 + 1 < MX;
+        hok = (lane == 0 || lane == 31) && (unsigned)(x0 + hdx) < (unsigned)MX;
+        pstride = (long long)MY * MX;
+        rstride = MX;
+        p = p0;
+        pend = MZ;
+        rmask = 0;
+        for (int k = 0; k < 3; ++k) rmask |= ((unsigned)(y - 1 + k) < (unsigned)MY ? 1u : 0u) << k;
+        bp = img + (long long)(y - 1) * MX + x0;
+        hp = bp + hdx;
+        po = (long long)p0 * pstride;
+    }
+    __device__ __forceinline__ void load(Raw &r) {
+        const bool pok = (unsigned)p < (unsigned)pend;
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            const long long o = po + (long long)k * rstride;
+            const bool ok = pok && ((rmask >> k) & 1u);
+            if constexpr (AL) {
+                // bytes b0 b1 -> halves (b0, b1)
+                r.m[k] = __byte_perm(ld_u16(bp + o, ok && ok0), 0u, 0x4140);
+            } else {
+                r.m[k] = __byte_perm(ld_u8(bp + o, ok && ok0), ld_u8(bp + o + 1, ok && ok1), 0x5410);
+            }
+            r.h[k] = ld_u8(hp + o, ok && hok) << hsh;
+        }
+        po += pstride;
+        ++p;
+    }
+};
+
+// In-plane box mins of the 3 x 3 cells around both vertices (index dy * 3 + dx,
+// digit 0 <-> offset -1): x +- 1 by warp shuffles and byte permutes.
+__device__ __forceinline__ void plane_reduce(const Raw &r, uint32_t (&o)[9]) {
+    const int lane = threadIdx.x & 31;
+    uint32_t A[3][3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        const uint32_t M = r.m[k];
+        uint32_t up = __shfl_up_sync(0xffffffffu, M, 1), dn = __shfl_down_sync(0xffffffffu, M, 1);
+        up = lane == 0 ? r.h[k] : up;   // high half: column x0 - 1
+        dn = lane == 31 ? r.h[k] : dn;  // low half: column x0 + 2
+        const uint32_t L = __byte_perm(up, M, 0x5432);  // (x0-1, x0)
+        const uint32_t R = __byte_perm(M, dn, 0x5432);  // (x0+1, x0+2)
+        A[k][0] = mn(L, M);
+        A[k][1] = M;
+        A[k][2] = mn(M, R);
+    }
+#pragma unroll
+    for (int dx = 0; dx < 3; ++dx) {
+        o[dx] = mn(A[0][dx], A[1][dx]);
+        o[3 + dx] = A[1][dx];
+        o[6 + dx] = mn(A[2][dx], A[1][dx]);
+    }
+}
+
+// In-plane inclusion-exclusion to the 4 corners (bit 0 <-> y, bit 1 <-> x; set
+// <-> +1), bias 512 (10 IADD3).
+__device__ __forceinline__ void ie(const uint32_t (&v)[9], uint32_t (&t)[4]) {
+    uint32_t xp[3], xm[3];
+#pragma unroll
+    for (int r = 0; r < 3; ++r) {
+        xp[r] = v[r * 3 + 1] + K1 - v[r * 3 + 0];  // slot +1: v(0) - v(-1)
+        xm[r] = v[r * 3 + 1] + K1 - v[r * 3 + 2];  // slot -1: v(0) - v(+1)
+    }
+    t[0] = xm[1] + K2 - xm[2];  // y -1, x -1
+    t[1] = xm[1] + K2 - xm[0];  // y +1, x -1
+    t[2] = xp[1] + K2 - xp[2];  // y -1, x +1
+    t[3] = xp[1] + K2 - xp[0];  // y +1, x +1
+}
+
+// Walk state at plane w
+struct State {
+    uint32_t pm[9];    // box mins of plane w
+    uint32_t tlow[4];  // corners of min(plane w-1, plane w)
+    uint32_t tmid[4];  // corners of plane w
+    Raw next;          // raw plane w+1 (loaded one step ahead)
+};
+
+template <bool AL>
+__device__ __forceinline__ void prime(Cursor<AL> &cur, State &s, const uint8_t *img, int MX, int MY, int MZ, int w,
+                                      int y, int x0) {
+    Raw r0, r1;
+    cur.init(img, MX, MY, MZ, w - 1, y, x0);
+    cur.load(r0);
+    cur.load(r1);
+    cur.load(s.next);
+    uint32_t pp[9];
+    plane_reduce(r0, pp);
+    plane_reduce(r1, s.pm);
+#pragma unroll
+    for (int i = 0; i < 9; ++i) pp[i] = mn(pp[i], s.pm[i]);
+    ie(pp, s.tlow);
+    ie(s.pm, s.tmid);
+}
+
+// Delta^- + 1024 of both vertices for all 8 sign vectors at plane w (e bit 0
+// <-> z, bit 1 <-> y, bit 2 <-> x) from the state `in` at w; `out` = the state
+// at w + 1 (two states alternate, so advancing costs no register moves)
+template <bool AL>
+__device__ __forceinline__ void step(Cursor<AL> &cur, const State &in, State &out, uint32_t (&dm)[8]) {
+    cur.load(out.next);  // plane w + 2, in flight during this step and the next
+    uint32_t cu[9];
+    plane_reduce(in.next, out.pm);
+#pragma unroll
+    for (int i = 0; i < 9; ++i) cu[i] = mn(in.pm[i], out.pm[i]);
+    ie(cu, out.tlow);
+    ie(out.pm, out.tmid);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+        const int c = e >> 1;
+        dm[e] = (e & 1) ? in.tmid[c] + K3 - in.tlow[c] : in.tmid[c] + K3 - out.tlow[c];
+    }
+}
+
+__device__ __forceinline__ void st_rec_w(Rec16 *p, uint32_t c, uint32_t w, bool pred) {
+    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %3, 0;\n\t@q st.global.v2.b32 [%0], {%1, %2};\n\t}" ::"l"(p),
+                 "r"(c), "r"(w), "r"((unsigned)pred)
+                 : "memory");
+}
+}  // namespace v8
+
+// Records of a 3-D 8-bit VERTEX image into the (tile, warp) regions (as
+// k1_pencil<3, VERTEX, uint8_t, Rec16, kEmit>, tiles 64 x 8 x 8, a.walk planes per
+// CTA). Region order: walk step, lane, column (x0 before x0 + 1).
+template <bool AL>
+__global__ void __launch_bounds__(kThreads, 2) k1_pencil_v8(K1Args a) {
+    constexpr int Q = 4, TZ = 8;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int MX = a.M[2], MY = a.M[1], MZ = a.M[0];
+    const int tiles_img = a.tiles_x * a.tiles_y * a.tiles_z;
+    const int nzc = (MZ + a.walk - 1) / a.walk;
+    long long cta = blockIdx.x;
+    const int tx = (int)(cta % a.tiles_x);
+    cta /= a.tiles_x;
+    const int ty_t = (int)(cta % a.tiles_y);
+    cta /= a.tiles_y;
+    const int zc = (int)(cta % nzc);
+    const long long b = cta / nzc;
+    const int y = ty_t * 8 + warp;
+    if (y >= MY) return;
+    const int w0 = zc * a.walk, w1 = min(MZ, w0 + a.walk), tz0 = w0 / TZ;
+    const int x0 = tx * 64 + 2 * lane;
+    const uint8_t *img = reinterpret_cast<const uint8_t *>(a.img) + b * a.npix;
+    Rec16 *out = reinterpret_cast<Rec16 *>(a.direct ? a.rec : a.scratch);
+    const long long lcap = a.direct ? a.vcap : a.scap;
+    int run[Q], abs_acc[Q];
+    uint32_t ssum[Q], smax[Q];
+    Rec16 *dst[Q];
+#pragma unroll
+    for (int q = 0; q < Q; ++q) {
+        run[q] = 0;
+        abs_acc[q] = 0;
+        ssum[q] = 0;
+        smax[q] = 0;
+    }
+    auto slot = [&](int w) -> long long {
+        const int tt = ((tz0 + (w - w0) / TZ) * a.tiles_y + ty_t) * a.tiles_x + tx;
+        return (long long)tt * 8 + warp;
+    };
+    auto load_base = [&](int w) {
+        const long long sl = slot(w);
+#pragma unroll
+        for (int q = 0; q < Q; ++q) dst[q] = out + (b * Q + q) * lcap + sl * a.cap_r;
+    };
+    auto flush = [&](int w_last) {
+        if (lane == 0) {
+            const long long sl = slot(w_last);
+#pragma unroll
+            for (int q = 0; q < Q; ++q) {
+                if (a.direct) {
+                    a.count[b * Q + q] = run[q];
+                    a.tile_off[(b * Q + q) * 2] = 0;
+                    a.tile_off[(b * Q + q) * 2 + 1] = run[q];
+                } else {
+                    a.cnt[(b * Q + q) * (long long)tiles_img * 8 + sl] = run[q];
+                }
+            }
+        }
+#pragma unroll
+        for (int q = 0; q < Q; ++q) {
+            run[q] = 0;
+            abs_acc[q] += (int)(ssum[q] & 0xffffu) + (int)(ssum[q] >> 16);  // <= 8 steps x 2040 per half
+            ssum[q] = 0;
+        }
+    };
+    v8::Cursor<AL> cur;
+    v8::State sa, sb;
+    v8::prime(cur, sa, img, MX, MY, MZ, w0, y, x0);
+    load_base(w0);
+    const uint32_t cstep = 1u << a.sh[2];
+    uint32_t coord = ((uint32_t)x0 << a.sh[2]) | ((uint32_t)y << a.sh[1]) | ((uint32_t)w0 << a.sh[0]);
+    const uint32_t cw = 1u << a.sh[0];
+    const unsigned lt = (1u << lane) - 1;
+    auto emit = [&](const uint32_t (&dm)[8]) {
+        uint32_t ab[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) ab[e] = __vmaxu2(dm[e], v8::K4 - dm[e]);  // |Delta^-| + 1024 per half
+#pragma unroll
+        for (int q = 0; q < Q; ++q) {
+            const uint32_t s = ab[q] + ab[q ^ 7] - v8::K4;  // |a| + |b| per half
+            ssum[q] += s;
+            smax[q] = __vmaxu2(smax[q], s);
+            const uint32_t r0 = __vadd2(__byte_perm(dm[q], dm[q ^ 7], 0x5410), v8::kUnbias);  // x0: a | b << 16
+            const uint32_t r1 = __vadd2(__byte_perm(dm[q], dm[q ^ 7], 0x7632), v8::kUnbias);  // x0 + 1
+            const bool k0 = r0 != 0, k1 = r1 != 0;
+            const unsigned b0 = __ballot_sync(0xffffffffu, k0), b1 = __ballot_sync(0xffffffffu, k1);
+            const int p0 = run[q] + __popc(b0 & lt) + __popc(b1 & lt);
+            v8::st_rec_w(dst[q] + p0, coord, r0, k0);
+            v8::st_rec_w(dst[q] + p0 + (int)k0, coord + cstep, r1, k1);
+            run[q] += __popc(b0) + __popc(b1);
+        }
+        coord += cw;
+    };
+    // two walk steps per iteration (states a -> b -> a); regions are 8 planes and
+    // start on even steps, so a region boundary falls between iterations
+    int w = w0;
+    for (; w + 1 < w1; w += 2) {
+        if (w > w0 && ((w - w0) & (TZ - 1)) == 0) {  // tile boundary
+            flush(w - 1);
+            load_base(w);
+        }
+        uint32_t dm[8];
+        v8::step(cur, sa, sb, dm);
+        emit(dm);
+        v8::step(cur, sb, sa, dm);
+        emit(dm);
+    }
+    if (w < w1) {  // odd tail
+        if (w > w0 && ((w - w0) & (TZ - 1)) == 0) {
+            flush(w - 1);
+            load_base(w);
+        }
+        uint32_t dm[8];
+        v8::step(cur, sa, sb, dm);
+        emit(dm);
+    }
+    flush(w1 - 1);
+#pragma unroll
+    for (int q = 0; q < Q; ++q) {
+        int v = abs_acc[q];
+        for (int d = 16; d; d >>= 1) v += __shfl_xor_sync(0xffffffffu, v, d);
+        if (lane == 0 && v) atomicAdd((unsigned long long *)&a.abs_sum[b * Q + q], (unsigned long long)(long long)v);
+        int mr = max((int)(smax[q] & 0xffffu), (int)(smax[q] >> 16));
+        for (int d = 16; d; d >>= 1) mr = max(mr, __shfl_xor_sync(0xffffffffu, mr, d));
+        if (lane == 0 && mr) atomicMax((unsigned long long *)&a.max_rec[b * Q + q], (unsigned long long)mr);
+    }
+}
+
 // Exclusive scan of each list's (tile, warp) counts, in place -> offsets; the
 // per-tile offsets (first warp of each tile) and the list length. One warp per
 // chunk of 256 counts, chunks handed out by a ticket in list order; a chunk's
@@ -749,6 +1059,27 @@ template <int N, int CONS, typename TIn>
 cudaError_t launch_r(const K1Args &a, cudaStream_t s, int mode) {
     return a.wide ? launch_t<N, CONS, TIn, Rec32>(a, s, mode) : launch_t<N, CONS, TIn, Rec16>(a, s, mode);
 }
+
+// 3-D 8-bit VERTEX images: the two-vertices-per-lane pencils, then the same scan
+// and copy as launch_t
+cudaError_t launch_v8(const K1Args &a, cudaStream_t s) {
+    const int tiles_img = a.tiles_x * a.tiles_y * a.tiles_z;
+    const int nzc = (a.M[0] + a.walk - 1) / a.walk;
+    const long long grid = a.batch * (long long)a.tiles_x * a.tiles_y * nzc;
+    if (grid == 0) return cudaSuccess;
+    if (a.M[2] % 2 == 0) k1_pencil_v8<true><<<(unsigned)grid, kThreads, 0, s>>>(a);
+    else k1_pencil_v8<false><<<(unsigned)grid, kThreads, 0, s>>>(a);
+    count_launch();
+    if (a.direct) return cudaGetLastError();
+    const long long cpl = ((long long)tiles_img * a.W + kScanChunk - 1) / kScanChunk;
+    const long long chunks = a.batch * 4 * cpl;
+    k1_scan<<<(unsigned)((chunks + kWarps - 1) / kWarps), kThreads, 0, s>>>(a, cpl, chunks);
+    const long long ccpl = ((long long)tiles_img * a.W + kCopyRegions - 1) / kCopyRegions;
+    k1_copy<Rec16><<<(unsigned)(a.batch * 4 * ccpl), kThreads, 0, s>>>(a, ccpl);
+    count_launch(2);
+    return cudaGetLastError();
+}
+bool use_v8(const K1Args &a) { return a.TX == 64; }
 template <int N, int CONS>
 cudaError_t launch_d(const K1Args &a, cudaStream_t s, int mode) {
     switch (a.dtype) {
@@ -757,7 +1088,15 @@ cudaError_t launch_d(const K1Args &a, cudaStream_t s, int mode) {
     default: return launch_r<N, CONS, int32_t>(a, s, mode);
     }
 }
-cudaError_t launch_any(const K1Args &a, cudaStream_t s, int mode) {
+cudaError_t launch_any(const K1Args &a_in, cudaStream_t s, int mode) {
+    if (use_v8(a_in)) {
+        if (mode == kEmit) return launch_v8(a_in, s);
+    }
+    K1Args a = a_in;
+    if (a.ndim == 3 && a.TX != 32) {  // the scalar kernel's statistics pass over 32-wide column blocks
+        a.TX = 32;
+        a.tiles_x = (a.M[2] + 31) / 32;
+    }
     if (a.ndim == 2)
         return a.construction == EUCALC_VERTEX ? launch_d<2, EUCALC_VERTEX>(a, s, mode)
                                                : launch_d<2, EUCALC_TOP>(a, s, mode);
@@ -771,9 +1110,20 @@ int64_t k1_scan_chunks(int64_t lists, int64_t ntiles, int W) {
     return lists * ((ntiles * W + kScanChunk - 1) / kScanChunk);
 }
 
-void k1_geometry(int ndim, const int64_t *M, int *TX, int *TY, int *TZ, int *W) {
+int k1_walk(int ndim, const int64_t *M, int64_t batch, int TX, int TY) {
+    if (ndim != 3) return 0;
+    // planes per CTA: long walks amortise the 2-plane prime, but keep >= 6 CTAs per SM's worth of work
+    const int64_t cols = batch * ((M[2] + TX - 1) / TX) * ((M[1] + TY - 1) / TY);
+    int walk = 64;
+    while (walk > 8 && cols * ((M[0] + walk - 1) / walk) < 6 * 148) walk /= 2;
+    return walk;
+}
+
+void k1_geometry(int ndim, const int64_t *M, int dtype, int construction, int *TX, int *TY, int *TZ, int *W) {
     *TX = 32;
     if (ndim == 3) {
+        // 8-bit VERTEX volumes: two vertices per lane (k1_pencil_v8), 64-wide tiles
+        if (dtype == EUCALC_U8 && construction == EUCALC_VERTEX && !getenv("EUCALC_K1_SCALAR")) *TX = 64;
         *TY = 8;
         *TZ = 8;
         *W = 8;

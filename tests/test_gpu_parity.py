@@ -490,6 +490,10 @@ K1_GEOMETRY_CASES = [
     ((150, 20, 70), np.uint8, "vertex"), ((150, 20, 70), np.uint8, "top"),
     ((70, 9, 33), np.int16, "vertex"), ((66, 9, 31), np.int32, "top"),
     ((65, 17, 40), np.int32, "vertex"),
+    # 3-D 8-bit VERTEX (two vertices per lane, 64-wide tiles): odd x extent (byte
+    # loads), an odd number of planes (odd walk tail), x = 64 exactly, x < 32
+    ((37, 29, 131), np.uint8, "vertex"), ((9, 5, 64), np.uint8, "vertex"), ((200, 3, 2), np.uint8, "vertex"),
+    ((23, 8, 1), np.uint8, "vertex"),
     # 2-D: several 64-row tiles and 32-wide column blocks, ragged both ways
     ((130, 100), np.uint8, "vertex"), ((130, 100), np.uint8, "top"), ((129, 65), np.int16, "top"),
     ((200, 33), np.int32, "vertex"),
