@@ -354,7 +354,18 @@ struct PlanEntry {
     DirInfo *d_info = nullptr;
     int32_t *d_csum = nullptr, *d_order = nullptr, *d_ts = nullptr, *d_tl = nullptr;
     uint64_t stamp = 0;
+    // K2 unit path (k2_unit): directions grouped by (pair, side) into units, and
+    // each direction's staging slot within an image; built on first use
+    std::mutex unit_mu;
+    bool units_built = false;
+    int64_t nunits = 0, stage_img = 0;
+    int4 *d_units = nullptr;
+    int32_t *d_unit_dirs = nullptr;
+    int64_t *d_stage_base = nullptr;
     ~PlanEntry() {
+        cudaFree(d_units);
+        cudaFree(d_unit_dirs);
+        cudaFree(d_stage_base);
         // cudaFree synchronises the device, so no in-flight kernel still reads these
         cudaFree(d_info);
         cudaFree(d_csum);
@@ -437,6 +448,59 @@ eucalc_status get_plan(const Complex *cx, const int32_t *dirs, int64_t D, cudaSt
     }
     g_plans.push_back(e);
     out = e;
+    return EUCALC_OK;
+}
+
+// Units of the K2 unit path for a direction plan: the directions of each (pair,
+// side) group, largest R first, packed greedily into units of at most
+// k2_unit_max() directions whose 128-padded R sum fits k2_unit_words(); units
+// with more directions first. Staging slot of direction d: sum of R over d' < d.
+eucalc_status plan_units(PlanEntry &pe) {
+    std::lock_guard<std::mutex> lk(pe.unit_mu);
+    if (pe.units_built) return EUCALC_OK;
+    const DirPlan &p = pe.p;
+    const int64_t D = (int64_t)p.info.size();
+    std::vector<int32_t> idx(D);
+    std::iota(idx.begin(), idx.end(), 0);
+    auto key = [&](int32_t d) { return p.info[d].q * 2 + p.info[d].swap; };
+    std::stable_sort(idx.begin(), idx.end(), [&](int32_t x, int32_t y) {
+        if (key(x) != key(y)) return key(x) < key(y);
+        return p.info[x].R > p.info[y].R;
+    });
+    std::vector<int4> units;
+    std::vector<int32_t> dirs_out;
+    const int gmax = k2_unit_max(), words = k2_unit_words();
+    for (int64_t i = 0; i < D;) {
+        int4 u{(int)dirs_out.size(), 0, p.info[idx[i]].q, p.info[idx[i]].swap};
+        int64_t off = 0;
+        while (i < D && u.y < gmax && key(idx[i]) == u.z * 2 + u.w) {
+            const int64_t rp = (p.info[idx[i]].R + 127) / 128 * 128;
+            if (u.y > 0 && off + rp > words) break;
+            off += rp;
+            dirs_out.push_back(idx[i]);
+            ++u.y;
+            ++i;
+        }
+        units.push_back(u);
+    }
+    std::stable_sort(units.begin(), units.end(), [](const int4 &x, const int4 &y) { return x.y > y.y; });
+    std::vector<int64_t> base(D);
+    int64_t acc = 0;
+    for (int64_t d = 0; d < D; ++d) {
+        base[d] = acc;
+        acc += p.info[d].R;
+    }
+    if (!units.empty()) {
+        CK(cudaMalloc(&pe.d_units, sizeof(int4) * units.size()));
+        CK(cudaMalloc(&pe.d_unit_dirs, sizeof(int32_t) * dirs_out.size()));
+        CK(cudaMalloc(&pe.d_stage_base, sizeof(int64_t) * D));
+        CK(cudaMemcpy(pe.d_units, units.data(), sizeof(int4) * units.size(), cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(pe.d_unit_dirs, dirs_out.data(), sizeof(int32_t) * dirs_out.size(), cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(pe.d_stage_base, base.data(), sizeof(int64_t) * D, cudaMemcpyHostToDevice));
+    }
+    pe.nunits = (int64_t)units.size();
+    pe.stage_img = acc;
+    pe.units_built = true;
     return EUCALC_OK;
 }
 
@@ -1246,8 +1310,39 @@ eucalc_status transforms_impl(const eucalc_critical *ccr, const int32_t *dirs, i
             a.chk_mask = ((0xffffu << (k + 1)) & 0xffffu) * 0x10001u;
         }
         tr.mark("memset+table+args");
+        // block regime, unit path: several directions per pass over a list, every
+        // segment staged (fixed slot of R_d entries per stream) — needs byte-aligned
+        // coordinates, 8-byte records, single-window split fallback, checked packing
+        bool unit = false;
+        {
+            const char *ev = getenv("EUCALC_K2_UNIT");
+            const bool want = !(ev && ev[0] == '0');
+            if (want && !cr->wide && p.dp == 3 && k2_block_regime(a) && a.max_rec < 16384 &&
+                !a.no_chk && p.R_max <= k2_split_window()) {
+                s = plan_units(*pe);
+                if (s != EUCALC_OK) {
+                    free_scratch();
+                    return s;
+                }
+                const size_t sb = 6 * (size_t)cx->batch * (size_t)pe->stage_img * esz;
+                if (pe->nunits > 0 && sb <= (size_t(4) << 30)) {
+                    a.stage = dalloc(sb);
+                    if (a.stage) {
+                        a.units = pe->d_units;
+                        a.nunits = pe->nunits;
+                        a.unit_dirs = pe->d_unit_dirs;
+                        a.stage_base = pe->d_stage_base;
+                        a.stage_img = pe->stage_img;
+                        a.stage_cap = cx->batch * pe->stage_img;
+                        unit = true;
+                    } else {
+                        cudaGetLastError();
+                    }
+                }
+            }
+        }
         int64_t scap = 0;
-        const size_t sbytes = k2_stage_bytes(a, num_sms(), &scap);
+        const size_t sbytes = unit ? 0 : k2_stage_bytes(a, num_sms(), &scap);
         if (sbytes) {
             a.stage = dalloc(sbytes);
             a.stage_cap = a.stage ? scap : 0;

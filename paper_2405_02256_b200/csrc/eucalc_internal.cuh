@@ -183,7 +183,13 @@ struct K2Args {
     bool no_chk;                // block regime: never use checked packed bins (EUCALC_K2_NO_CHK, tests)
     unsigned chk_bias, chk_mask;  // checked packed bins: fields in [-2^k, 2^k), k = 14 (EUCALC_K2_CHK_BITS, tests)
     void *stage;                // block regime: per-CTA output staging (k2_stage_bytes), or NULL
-    int64_t stage_cap;          // entries per staged array per CTA
+    int64_t stage_cap;          // entries per staged array per CTA (unit path: per image batch, all segments)
+    // unit path (k2_unit): several directions per pass over a list, or units == NULL
+    const int4 *units;          // [nunits] {first index into unit_dirs, G, pair q, swap}, one image's units
+    int64_t nunits;
+    const int32_t *unit_dirs;   // direction ids of the units
+    const int64_t *stage_base;  // [D] staging slot of direction d within an image (prefix of R)
+    int64_t stage_img;          // staging entries per image (sum of R)
     // fused HT (NEXT f2): kbar table (fp64) over u in [ht_U0, ...), or NULL
     const double *ht_tab;
     int64_t ht_U0, L;
@@ -194,6 +200,12 @@ struct K2Args {
     void *ht_out;               // [batch][D]
 };
 cudaError_t launch_k2(const K2Args &a, cudaStream_t s, int num_sms);
+// unit path geometry: packed histogram words per CTA, directions per unit, split window
+int k2_unit_words();
+int k2_unit_max();
+int k2_split_window();
+// the block regime (one CTA per segment / unit) is taken for these arguments
+bool k2_block_regime(const K2Args &a);
 // Block regime only: bytes of per-CTA output staging that let each segment fill
 // its histogram once (0 = warp regime, or staging too large: two fills).
 size_t k2_stage_bytes(const K2Args &a, int num_sms, int64_t *cap);

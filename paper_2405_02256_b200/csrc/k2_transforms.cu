@@ -1410,6 +1410,290 @@ __global__ void __launch_bounds__(kBlockThreads, 1) k2_block(K2Args a, long long
     }
 }
 
+// ----------------------------------------------------------------------------- unit kernel
+// Block regime with several directions per pass over a list ("units"): the
+// directions of one image that read the same pair list from the same side
+// (same orthant, Lemma 3) are grouped into units of G <= kUnitMax whose
+// packed histograms fit shared memory together (sum of their 128-padded R).
+// A CTA streams the list ONCE per unit and adds every record into the G
+// histograms (one dp4a + one shared atomic per record and direction), so the
+// record loads, the weight-word extraction and the loop overhead are shared by
+// G directions. Each histogram is then emitted (the paper's cumulative sums,
+// P:126-128) into the segment's fixed staging slot (capacity R_d entries per
+// stream), its counts go to cnt_c/cnt_o; k2_scan turns the counts into the CSR
+// offsets and k2_unit_copy moves the staged entries there. Units are taken by
+// ticket in any order (no look-back between segments).
+// Packed bins are checked exactly as in k2_block (Hist::add_chk) unless a bound
+// proves them for every direction of the unit; a flagged unit is redone one
+// direction at a time with split bins (block_segment_staged, one window).
+constexpr int kUnitMax = 4;
+constexpr int kUnitWords = (int)(kBlockSmem / 4);  // packed words of shared histogram per CTA
+
+__device__ __forceinline__ void red_smem(unsigned addr, unsigned v) {
+    asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(addr), "r"(v));
+}
+__device__ __forceinline__ unsigned atom_smem(unsigned addr, unsigned v) {
+    unsigned old;
+    asm volatile("atom.shared.add.u32 %0, [%1], %2;" : "=r"(old) : "r"(addr), "r"(v));
+    return old;
+}
+
+// Per-unit parameters of the fill: per direction the packed int8 direction, -hlo
+// and the shared byte address of its histogram.
+struct UnitParams {
+    int xs8[kUnitMax], nhlo[kUnitMax];
+    unsigned sb[kUnitMax];
+};
+
+// Adds records threadIdx.x + k * kBlockThreads of `list` into the G packed
+// histograms: per record one weight word, per record and direction one dp4a
+// (height - hlo), the bank swizzle and one shared atomic (checked: the returned
+// word biased and OR-ed into `bad`). The parameters are copied to registers once.
+template <bool CHK, bool SWAP, int G>
+__device__ __forceinline__ unsigned unit_fill(const uint2 *list, int n, const UnitParams &pp, unsigned bias) {
+    constexpr int U = 4;
+    constexpr int step = kBlockThreads;
+    int xs8[G], nhlo[G];
+    unsigned sb[G];
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+        xs8[g] = pp.xs8[g];
+        nhlo[g] = pp.nhlo[g];
+        sb[g] = pp.sb[g];
+    }
+    unsigned bad = 0;
+    auto one = [&](const uint2 r) {
+        const unsigned w = packed_word<SWAP>(r.y);
+#pragma unroll
+        for (int g = 0; g < G; ++g) {
+            int h;
+            asm("dp4a.u32.s32 %0, %1, %2, %3;" : "=r"(h) : "r"(r.x), "r"(xs8[g]), "r"(nhlo[g]));
+            const unsigned addr = sb[g] + ((unsigned)swz(h) << 2);
+            if constexpr (CHK) bad |= atom_smem(addr, w) + w + bias;
+            else red_smem(addr, w);
+        }
+    };
+    int i = threadIdx.x;
+    for (; i + (U - 1) * step < n; i += U * step) {
+        uint2 r[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) r[u] = __ldg(list + i + u * step);
+#pragma unroll
+        for (int u = 0; u < U; ++u) one(r[u]);
+    }
+    for (; i < n; i += step) one(__ldg(list + i));
+    return bad;
+}
+
+template <bool CHK, bool SWAP>
+__device__ __noinline__ unsigned unit_fill_any(const uint2 *list, int n, int G, UnitParams pp, unsigned bias) {
+    switch (G) {
+    case 1: return unit_fill<CHK, SWAP, 1>(list, n, pp, bias);
+    case 2: return unit_fill<CHK, SWAP, 2>(list, n, pp, bias);
+    case 3: return unit_fill<CHK, SWAP, 3>(list, n, pp, bias);
+    default: return unit_fill<CHK, SWAP, 4>(list, n, pp, bias);
+    }
+}
+
+// Emits one packed histogram (R bins at hist, single window) of segment s into
+// its staging slot `base` (arrays at stride cap); counts -> sh.cnt, HT written.
+template <typename OutT>
+__device__ __noinline__ void unit_emit(const K2Args &a, const OutPtrs<OutT> &outp, unsigned *hist, int R,
+                                          long long s, const DirInfo &di, BlockShared &sh, OutT *base,
+                                          long long cap) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    Hist<true, true> hs;
+    hs.c = hist;
+    hs.j = hist;
+    OutPtrs<OutT> scr = outp;
+    scr.eh = base;
+    scr.ev = base + cap;
+    scr.cv = base + 2 * cap;
+    scr.ch = base + 3 * cap;
+    scr.oh = base + 4 * cap;
+    scr.ov = base + 5 * cap;
+    scr.ect = outp.ect || outp.cls;  // staged heights serve both (T_c = T)
+    scr.alias = true;
+    const int per = ((R + kBlockWarps - 1) / kBlockWarps + kGroup - 1) / kGroup * kGroup;
+    const int b0 = min(R, warp * per), b1 = min(R, b0 + per);
+    int c = 0, o = 0, sc = 0, sj = 0;
+    for (int bb = b0; bb < b1; bb += kGroup) {
+        int wc[4], wj[4];
+        hs.load4(bb + 4 * lane, wc, wj, false);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            c += wc[q] != 0;
+            o += wj[q] != 0;
+            sc += wc[q];
+            sj += wj[q];
+        }
+    }
+    c = warp_sum(c);
+    o = warp_sum(o);
+    sc = warp_sum(sc);
+    sj = warp_sum(sj);
+    if (lane == 0) {
+        sh.wsum[warp][0] = c;
+        sh.wsum[warp][1] = o;
+        sh.wsum[warp][2] = sc;
+        sh.wsum[warp][3] = sj;
+    }
+    __syncthreads();
+    int pc = 0, po = 0, er = 0, rr = 0, tc = 0, to = 0;
+    for (int k = 0; k < kBlockWarps; ++k) {
+        if (k < warp) {
+            pc += sh.wsum[k][0];
+            po += sh.wsum[k][1];
+            er += sh.wsum[k][2];
+            rr += sh.wsum[k][3];
+        }
+        tc += sh.wsum[k][0];
+        to += sh.wsum[k][1];
+    }
+    double ht = 0.0;
+    const long long ht_off = outp.tab ? ht_tab_off(a, di) : 0;
+    for (int bb = b0; bb < b1; bb += kGroup) emit_group<kModeAny>(scr, hs, bb, di.hlo, er, rr, pc, po, ht, ht_off);
+    if (outp.tab) {  // fused HT: warp partials, then a fixed-order sum over warps
+        for (int k = 16; k; k >>= 1) ht += __shfl_xor_sync(0xffffffffu, ht, k);
+        if (lane == 0) sh.ht[warp] = ht;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        if (outp.tab) {
+            double t = 0.0;
+            for (int k = 0; k < kBlockWarps; ++k) t += sh.ht[k];
+            ht_write(a, s, t);
+        }
+        a.cnt_c[s] = tc;
+        a.cnt_o[s] = to;
+    }
+}
+
+template <typename OutT>
+__device__ __noinline__ void unit_split_segment(const K2Args &a, const OutPtrs<OutT> &outp, unsigned *hist,
+                                                int split_win, long long s, long long b, long long d,
+                                                BlockShared &sh, OutT *base) {
+    block_segment_staged<false, 3, Rec16, OutT>(a, outp, hist, split_win, s, b, d, sh, 0u, base);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        a.cnt_c[s] = sh.cnt[0];
+        a.cnt_o[s] = sh.cnt[1];
+    }
+}
+
+template <typename OutT>
+__global__ void __launch_bounds__(kBlockThreads, 1) k2_unit(K2Args a, int split_win) {
+    extern __shared__ __align__(16) unsigned hist[];
+    __shared__ BlockShared sh;
+    const OutPtrs<OutT> outp(a);
+    OutT *stage = reinterpret_cast<OutT *>(a.stage);
+    const unsigned hist_sa = (unsigned)__cvta_generic_to_shared(hist);
+    for (int i = threadIdx.x; i < kUnitWords; i += kBlockThreads) hist[i] = 0;
+    const long long total = a.nunits * a.batch;
+    while (true) {
+        __syncthreads();
+        if (threadIdx.x == 0) sh.seg = (long long)atomicAdd(a.ticket, 1u);
+        __syncthreads();
+        const long long t = sh.seg;
+        if (t >= total) break;
+        const long long b = t % a.batch;   // images interleaved: equal units of all images run together
+        const int4 un = a.units[t / a.batch];  // {first index into unit_dirs, G, q, swap}
+        const int G = un.y;
+        UnitParams pp;
+        int base[kUnitMax];
+        bool proven = true;
+        int off = 0;
+#pragma unroll
+        for (int g = 0; g < kUnitMax; ++g) {
+            pp.xs8[g] = 0;
+            pp.nhlo[g] = 0;
+            base[g] = 0;
+            if (g < G) {
+                const DirInfo &di = a.dirs[a.unit_dirs[un.x + g]];
+                pp.xs8[g] = di.xs8;
+                pp.nhlo[g] = -di.hlo;
+                base[g] = off;
+                off += (di.R + kGroup - 1) / kGroup * kGroup;
+                proven = proven && min((long long)di.line * a.max_rec, (long long)a.max_abs_sum) < 32768;
+            }
+            pp.sb[g] = hist_sa + 4u * (unsigned)base[g];
+        }
+        const uint2 *list = reinterpret_cast<const uint2 *>(a.rec) + (b * a.Q + un.z) * a.vcap;
+        const int n = a.count[b * a.Q + un.z];
+        unsigned bad;
+        if (proven) bad = un.w ? unit_fill_any<false, true>(list, n, G, pp, 0u) : unit_fill_any<false, false>(list, n, G, pp, 0u);
+        else bad = un.w ? unit_fill_any<true, true>(list, n, G, pp, a.chk_bias) : unit_fill_any<true, false>(list, n, G, pp, a.chk_bias);
+        if (__syncthreads_or(proven ? 0u : (bad & a.chk_mask))) {
+            // a packed bin left the checked range: redo each direction with split bins
+            if (threadIdx.x == 0) atomicAdd(a.ticket + 3, (unsigned)G);  // eucalc_k2_restarts: per segment
+            for (int i = threadIdx.x; i < kUnitWords; i += kBlockThreads) hist[i] = 0;
+            __syncthreads();
+            for (int g = 0; g < G; ++g) {
+                const long long d = a.unit_dirs[un.x + g], s = b * a.D + d;
+                unit_split_segment<OutT>(a, outp, hist, split_win, s, b, d, sh,
+                                         stage + b * a.stage_img + a.stage_base[d]);
+            }
+            continue;
+        }
+        for (int g = 0; g < G; ++g) {
+            const long long d = a.unit_dirs[un.x + g], s = b * a.D + d;
+            const DirInfo di = a.dirs[d];
+            unit_emit<OutT>(a, outp, hist + base[g], di.R, s, di, sh, stage + b * a.stage_img + a.stage_base[d],
+                            a.stage_cap);
+        }
+    }
+}
+
+// Staged entries of every segment -> the CSR (one CTA per segment, grid-stride).
+template <typename OutT>
+__global__ void __launch_bounds__(256) k2_unit_copy(K2Args a) {
+    const OutPtrs<OutT> outp(a);
+    const OutT *stage = reinterpret_cast<const OutT *>(a.stage);
+    const long long S = a.batch * a.D, cap = a.stage_cap;
+    for (long long s = blockIdx.x; s < S; s += gridDim.x) {
+        const long long b = s / a.D, d = s - b * a.D;
+        const OutT *bs = stage + b * a.stage_img + a.stage_base[d];
+        const int nc = a.cnt_c[s], no = a.cnt_o[s];
+        const long long ec = a.do_ect ? a.ect.off[s] : a.do_cls ? a.cls.off[s] : 0;
+        const long long eo = a.do_ord ? a.ord.off[s] : 0;
+        if (outp.ect || outp.cls) {
+            for (int i = threadIdx.x; i < nc; i += blockDim.x) {
+                const OutT h = bs[i], v = bs[cap + i], c = bs[2 * cap + i];
+                if (outp.ect) {
+                    outp.eh[ec + i] = h;
+                    outp.ev[ec + i] = v;
+                }
+                if (outp.cls) {
+                    if (!outp.alias) outp.ch[ec + i] = h;
+                    outp.cv[ec + i] = c;
+                }
+            }
+        }
+        if (outp.ord) {
+            for (int i = threadIdx.x; i < no; i += blockDim.x) {
+                outp.oh[eo + i] = bs[4 * cap + i];
+                outp.ov[eo + i] = bs[5 * cap + i];
+            }
+        }
+    }
+}
+
+template <typename OutT>
+cudaError_t launch_unit_t(const K2Args &a, cudaStream_t s, int num_sms) {
+    auto kern = k2_unit<OutT>;
+    cudaError_t e = prepare_kernel((const void *)kern, kBlockThreads, kBlockSmem, nullptr);
+    if (e != cudaSuccess) return e;
+    const long long total = a.nunits * a.batch, S = a.batch * a.D;
+    if (total == 0) return cudaSuccess;
+    const int split_win = (int)(kBlockSmem / 8) / kGroup * kGroup;
+    kern<<<(unsigned)std::min<long long>(total, num_sms), kBlockThreads, kBlockSmem, s>>>(a, split_win);
+    const long long ntiles = (S + 1 + kScanTile - 1) / kScanTile;
+    k2_scan<<<(unsigned)ntiles, kScanThreads, 0, s>>>(a, a.cnt_c, a.cnt_o, S, a.flags);
+    k2_unit_copy<OutT><<<(unsigned)std::min<long long>(S, 8LL * num_sms), 256, 0, s>>>(a);
+    count_launch(3);
+    return cudaGetLastError();
+}
+
 template <typename RecT, typename OutT, bool PACK>
 cudaError_t launch_t(const K2Args &a, cudaStream_t s, int num_sms) {
     const long long nseg = a.batch * a.D;
@@ -1501,7 +1785,25 @@ size_t k2_stage_bytes(const K2Args &a, int num_sms, int64_t *cap) {
 }
 
 cudaError_t launch_k2(const K2Args &a, cudaStream_t s, int num_sms) {
+    if (a.units) {
+        switch (a.elem_bytes) {
+        case 2: return launch_unit_t<int16_t>(a, s, num_sms);
+        case 4: return launch_unit_t<int32_t>(a, s, num_sms);
+        default: return launch_unit_t<int64_t>(a, s, num_sms);
+        }
+    }
     return a.wide ? launch_o<Rec32>(a, s, num_sms) : launch_o<Rec16>(a, s, num_sms);
+}
+
+int k2_unit_words() { return kUnitWords; }
+int k2_unit_max() { return kUnitMax; }
+int k2_split_window() { return (int)(kBlockSmem / 8) / kGroup * kGroup; }
+bool k2_block_regime(const K2Args &a) {
+    const int words = a.pack16 ? 1 : 2;
+    const int rcap = (a.R_max + kGroup - 1) / kGroup * kGroup;
+    const size_t per_warp = (size_t)rcap * 4 * words;
+    const int warps = (int)std::min<size_t>(8, (200 * 1024) / per_warp);
+    return !(warps >= 2 && a.max_count <= 32768);
 }
 
 }  // namespace eucalc

@@ -170,12 +170,17 @@ def test_block_regime_3d_culled_windows():
 
 
 @pytest.mark.parametrize("env", [{}, {"EUCALC_K2_CHK_BITS": "1"}, {"EUCALC_K2_CHK_BITS": "6"},
-                                 {"EUCALC_K2_NO_CHK": "1"}], ids=["checked", "restart", "partial", "split"])
+                                 {"EUCALC_K2_NO_CHK": "1"}, {"EUCALC_K2_UNIT": "0"},
+                                 {"EUCALC_K2_UNIT": "0", "EUCALC_K2_CHK_BITS": "1"}],
+                         ids=["checked", "restart", "partial", "split", "per-segment", "per-segment-restart"])
 def test_block_regime_checked_packed_bins(env, monkeypatch):
     """Block regime with packed 16+16 bins whose exactness no bound proves: every
     add is checked and a flagged segment restarts with split bins. The test hooks
     narrow the checked range (bits 1: every segment restarts; bits 6: some do) or
-    disable the packed path; all must give the oracle's exact representations."""
+    disable the packed path; all must give the oracle's exact representations. 3-D
+    lists go through the unit path (several directions per pass over a list, a
+    flagged unit redoes each of its directions with split bins) unless
+    EUCALC_K2_UNIT=0 selects one CTA per segment."""
     for k, v in env.items():
         monkeypatch.setenv(k, v)
     eu.k2_restarts(reset=True)
