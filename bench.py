@@ -455,6 +455,13 @@ def record_transforms(name, eu, torch, args, dist, flush, clk, steps, warmup, ht
     kb = k2_bytes(cr, dirs, r, ht=ht is not None)
     achieved = kb / (k2_ms / 1e3) / 1e9
     npair = int(cr.list_lengths()[:, pair_index(dirs)].sum())
+    _, mhz, _ = peaks()
+    clk_mhz = (clk.summary(name).get("sm_mhz") or mhz)
+    # K2 adds every record of a segment's list into the segment's histogram with one
+    # shared atomic (packed bins): npair / 32 warp atomics per step
+    warp_atoms = npair / 32.0
+    rate = warp_atoms / (k2_ms / 1e3) / SMS / (clk_mhz * 1e6)
+    apeak, asrc = atomics_peak()
     rec = {
         "value": value, "unit": UNIT, "ms_per_step": dev_ms / steps, "steps": steps, "warmup": warmup,
         "workload": DESCR[name], "images": B, "directions": D,
@@ -463,7 +470,13 @@ def record_transforms(name, eu, torch, args, dist, flush, clk, steps, warmup, ht
         "critical_points_per_s": npair / (k2_ms / 1e3),
         "roofline": {"bound": "hbm", "kernel": "K2 (k2_transforms launches of the step)", "achieved": achieved,
                      "peak": hbm, "unit": "GB/s", "frac": achieved / hbm, "traffic": None,
-                     "peak_source": psrc, "algorithmic_bytes_per_launch": kb, "launch_ms": k2_ms},
+                     "peak_source": psrc, "algorithmic_bytes_per_launch": kb, "launch_ms": k2_ms,
+                     "smem_atomics": {"warp_atomics_per_launch": warp_atoms,
+                                      "achieved_per_clk_per_sm": rate, "peak_per_clk_per_sm": apeak,
+                                      "frac": (rate / apeak) if apeak else None, "clock_mhz": clk_mhz,
+                                      "peak_source": asrc,
+                                      "note": "list bytes re-read per direction mostly hit L2 (SURVEY 8(d)): "
+                                              "the fill is bound by shared-memory atomics, not HBM"}},
         "gpu_launches": int(launches),
         "clocks": clk.summary(name),
         "elem_bytes": int(r["ect"]["value"].element_size()),
@@ -471,6 +484,22 @@ def record_transforms(name, eu, torch, args, dist, flush, clk, steps, warmup, ht
     if "zero_fixed" in w:
         rec["zero_fixed_directions"] = w["zero_fixed"]
     return rec, w, (cx, cr, r, dirs)
+
+
+def atomics_peak():
+    """Shared-memory atomic throughput measured on a B200 by tools/ubench/atoms.cu
+    (profiles/r2/s7/atoms_ubench.jsonl): warp ATOMS instructions per clock per SM for
+    pseudo-random addresses with the result used and OR-ed (K2's checked packed add)."""
+    p = os.path.join(ROOT, "profiles", "r2", "s7", "atoms_ubench.jsonl")
+    if os.path.exists(p):
+        for line in open(p):
+            try:
+                d = json.loads(line)
+            except ValueError:
+                continue
+            if d.get("mode", "").startswith("random, checked"):
+                return float(d["warp_atoms_per_clk_per_sm"]), "measured (tools/ubench/atoms.cu, " + p[len(ROOT) + 1:] + ")"
+    return None, None
 
 
 def traffic_for(name):

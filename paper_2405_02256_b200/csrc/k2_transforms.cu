@@ -1644,12 +1644,15 @@ __global__ void __launch_bounds__(kBlockThreads, 1) k2_unit(K2Args a, int split_
     }
 }
 
-// Staged entries of every segment -> the CSR (one CTA per segment, grid-stride).
+// Staged entries of every segment -> the CSR (one CTA per segment, grid-stride;
+// four elements per array in flight per thread before their stores).
 template <typename OutT>
-__global__ void __launch_bounds__(256) k2_unit_copy(K2Args a) {
+__global__ void __launch_bounds__(512) k2_unit_copy(K2Args a) {
+    constexpr int U = 4;
     const OutPtrs<OutT> outp(a);
     const OutT *stage = reinterpret_cast<const OutT *>(a.stage);
     const long long S = a.batch * a.D, cap = a.stage_cap;
+    const int T = blockDim.x;
     for (long long s = blockIdx.x; s < S; s += gridDim.x) {
         const long long b = s / a.D, d = s - b * a.D;
         const OutT *bs = stage + b * a.stage_img + a.stage_base[d];
@@ -1657,22 +1660,52 @@ __global__ void __launch_bounds__(256) k2_unit_copy(K2Args a) {
         const long long ec = a.do_ect ? a.ect.off[s] : a.do_cls ? a.cls.off[s] : 0;
         const long long eo = a.do_ord ? a.ord.off[s] : 0;
         if (outp.ect || outp.cls) {
-            for (int i = threadIdx.x; i < nc; i += blockDim.x) {
-                const OutT h = bs[i], v = bs[cap + i], c = bs[2 * cap + i];
-                if (outp.ect) {
-                    outp.eh[ec + i] = h;
-                    outp.ev[ec + i] = v;
+            for (int i0 = threadIdx.x; i0 < nc; i0 += U * T) {
+                OutT h[U], v[U], c[U];
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const int i = i0 + u * T;
+                    if (i < nc) {
+                        h[u] = bs[i];
+                        v[u] = bs[cap + i];
+                        c[u] = bs[2 * cap + i];
+                    }
                 }
-                if (outp.cls) {
-                    if (!outp.alias) outp.ch[ec + i] = h;
-                    outp.cv[ec + i] = c;
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const int i = i0 + u * T;
+                    if (i < nc) {
+                        if (outp.ect) {
+                            outp.eh[ec + i] = h[u];
+                            outp.ev[ec + i] = v[u];
+                        }
+                        if (outp.cls) {
+                            if (!outp.alias) outp.ch[ec + i] = h[u];
+                            outp.cv[ec + i] = c[u];
+                        }
+                    }
                 }
             }
         }
         if (outp.ord) {
-            for (int i = threadIdx.x; i < no; i += blockDim.x) {
-                outp.oh[eo + i] = bs[4 * cap + i];
-                outp.ov[eo + i] = bs[5 * cap + i];
+            for (int i0 = threadIdx.x; i0 < no; i0 += U * T) {
+                OutT h[U], v[U];
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const int i = i0 + u * T;
+                    if (i < no) {
+                        h[u] = bs[4 * cap + i];
+                        v[u] = bs[5 * cap + i];
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const int i = i0 + u * T;
+                    if (i < no) {
+                        outp.oh[eo + i] = h[u];
+                        outp.ov[eo + i] = v[u];
+                    }
+                }
             }
         }
     }
@@ -1689,7 +1722,7 @@ cudaError_t launch_unit_t(const K2Args &a, cudaStream_t s, int num_sms) {
     kern<<<(unsigned)std::min<long long>(total, num_sms), kBlockThreads, kBlockSmem, s>>>(a, split_win);
     const long long ntiles = (S + 1 + kScanTile - 1) / kScanTile;
     k2_scan<<<(unsigned)ntiles, kScanThreads, 0, s>>>(a, a.cnt_c, a.cnt_o, S, a.flags);
-    k2_unit_copy<OutT><<<(unsigned)std::min<long long>(S, 8LL * num_sms), 256, 0, s>>>(a);
+    k2_unit_copy<OutT><<<(unsigned)std::min<long long>(S, 4LL * num_sms), 512, 0, s>>>(a);
     count_launch(3);
     return cudaGetLastError();
 }
