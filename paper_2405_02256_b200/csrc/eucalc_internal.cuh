@@ -109,6 +109,7 @@ struct K1Args {
     int TX, TY, TZ, tiles_x, tiles_y, tiles_z;
     int W;              // warps (pencils) per tile: 8 in 3-D (one per row), 1 in 2-D
     int walk;           // 3-D: planes walked per CTA (k1_walk)
+    bool stats_in_copy; // the |Delta^-| statistics are taken by k1_copy (two-vertex 3-D pencils)
     int sh[kMaxN];
     void *rec;
     bool wide;

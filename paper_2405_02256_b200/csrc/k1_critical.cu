@@ -786,7 +786,7 @@ __device__ __forceinline__ void st_rec_w(Rec16 *p, uint32_t c, uint32_t w, bool 
 // k1_pencil<3, VERTEX, uint8_t, Rec16, kEmit>, tiles 64 x 8 x 8, a.walk planes per
 // CTA). Region order: walk step, lane, column (x0 before x0 + 1).
 template <bool AL>
-__global__ void __launch_bounds__(kThreads, 2) k1_pencil_v8(K1Args a) {
+__global__ void __launch_bounds__(kThreads, 3) k1_pencil_v8(K1Args a) {
     constexpr int Q = 4, TZ = 8;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int MX = a.M[2], MY = a.M[1], MZ = a.M[0];
@@ -806,16 +806,10 @@ __global__ void __launch_bounds__(kThreads, 2) k1_pencil_v8(K1Args a) {
     const uint8_t *img = reinterpret_cast<const uint8_t *>(a.img) + b * a.npix;
     Rec16 *out = reinterpret_cast<Rec16 *>(a.direct ? a.rec : a.scratch);
     const long long lcap = a.direct ? a.vcap : a.scap;
-    int run[Q], abs_acc[Q];
-    uint32_t ssum[Q], smax[Q];
+    int run[Q];
     Rec16 *dst[Q];
 #pragma unroll
-    for (int q = 0; q < Q; ++q) {
-        run[q] = 0;
-        abs_acc[q] = 0;
-        ssum[q] = 0;
-        smax[q] = 0;
-    }
+    for (int q = 0; q < Q; ++q) run[q] = 0;
     auto slot = [&](int w) -> long long {
         const int tt = ((tz0 + (w - w0) / TZ) * a.tiles_y + ty_t) * a.tiles_x + tx;
         return (long long)tt * 8 + warp;
@@ -840,11 +834,7 @@ __global__ void __launch_bounds__(kThreads, 2) k1_pencil_v8(K1Args a) {
             }
         }
 #pragma unroll
-        for (int q = 0; q < Q; ++q) {
-            run[q] = 0;
-            abs_acc[q] += (int)(ssum[q] & 0xffffu) + (int)(ssum[q] >> 16);  // <= 8 steps x 2040 per half
-            ssum[q] = 0;
-        }
+        for (int q = 0; q < Q; ++q) run[q] = 0;
     };
     v8::Cursor<AL> cur;
     v8::State sa, sb;
@@ -854,19 +844,15 @@ __global__ void __launch_bounds__(kThreads, 2) k1_pencil_v8(K1Args a) {
     uint32_t coord = ((uint32_t)x0 << a.sh[2]) | ((uint32_t)y << a.sh[1]) | ((uint32_t)w0 << a.sh[0]);
     const uint32_t cw = 1u << a.sh[0];
     const unsigned lt = (1u << lane) - 1;
+    // the |Delta^-| statistics of the lists are taken by k1_copy (it reads every record)
     auto emit = [&](const uint32_t (&dm)[8]) {
-        uint32_t ab[8];
-#pragma unroll
-        for (int e = 0; e < 8; ++e) ab[e] = __vmaxu2(dm[e], v8::K4 - dm[e]);  // |Delta^-| + 1024 per half
 #pragma unroll
         for (int q = 0; q < Q; ++q) {
-            const uint32_t s = ab[q] + ab[q ^ 7] - v8::K4;  // |a| + |b| per half
-            ssum[q] += s;
-            smax[q] = __vmaxu2(smax[q], s);
             const uint32_t r0 = __vadd2(__byte_perm(dm[q], dm[q ^ 7], 0x5410), v8::kUnbias);  // x0: a | b << 16
             const uint32_t r1 = __vadd2(__byte_perm(dm[q], dm[q ^ 7], 0x7632), v8::kUnbias);  // x0 + 1
             const bool k0 = r0 != 0, k1 = r1 != 0;
             const unsigned b0 = __ballot_sync(0xffffffffu, k0), b1 = __ballot_sync(0xffffffffu, k1);
+            if ((b0 | b1) == 0) continue;  // nothing kept by the warp (most steps of binary images)
             const int p0 = run[q] + __popc(b0 & lt) + __popc(b1 & lt);
             v8::st_rec_w(dst[q] + p0, coord, r0, k0);
             v8::st_rec_w(dst[q] + p0 + (int)k0, coord + cstep, r1, k1);
@@ -898,15 +884,6 @@ __global__ void __launch_bounds__(kThreads, 2) k1_pencil_v8(K1Args a) {
         emit(dm);
     }
     flush(w1 - 1);
-#pragma unroll
-    for (int q = 0; q < Q; ++q) {
-        int v = abs_acc[q];
-        for (int d = 16; d; d >>= 1) v += __shfl_xor_sync(0xffffffffu, v, d);
-        if (lane == 0 && v) atomicAdd((unsigned long long *)&a.abs_sum[b * Q + q], (unsigned long long)(long long)v);
-        int mr = max((int)(smax[q] & 0xffffu), (int)(smax[q] >> 16));
-        for (int d = 16; d; d >>= 1) mr = max(mr, __shfl_xor_sync(0xffffffffu, mr, d));
-        if (lane == 0 && mr) atomicMax((unsigned long long *)&a.max_rec[b * Q + q], (unsigned long long)mr);
-    }
 }
 
 // Exclusive scan of each list's (tile, warp) counts, in place -> offsets; the
@@ -1014,6 +991,8 @@ __global__ void __launch_bounds__(kThreads) k1_copy(K1Args a, long long cpl) {
     const int base = s_off[0], T = s_off[nr] - base;
     const RecT *src = reinterpret_cast<const RecT *>(a.scratch) + L * a.scap + r0 * a.cap_r;
     RecT *dst = reinterpret_cast<RecT *>(a.rec) + L * a.vcap + base;
+    long long ssum = 0;
+    int smax = 0;
 #pragma unroll 4
     for (int d = threadIdx.x; d < T; d += kThreads) {
         const int x = base + d;
@@ -1023,7 +1002,34 @@ __global__ void __launch_bounds__(kThreads) k1_copy(K1Args a, long long cpl) {
             if (s_off[mid] <= x) lo = mid;
             else hi = mid - 1;
         }
-        dst[d] = src[(long long)lo * a.cap_r + (x - s_off[lo])];
+        const RecT r = src[(long long)lo * a.cap_r + (x - s_off[lo])];
+        dst[d] = r;
+        if (a.stats_in_copy) {
+            const int v = abs((int)r.a) + abs((int)r.b);
+            ssum += v;
+            smax = max(smax, v);
+        }
+    }
+    if (a.stats_in_copy) {  // |Delta^-| statistics of the list (order-independent integer reductions)
+        __shared__ long long s_sum[kWarps];
+        __shared__ int s_max[kWarps];
+        for (int k = 16; k; k >>= 1) {
+            ssum += __shfl_xor_sync(0xffffffffu, ssum, k);
+            smax = max(smax, __shfl_xor_sync(0xffffffffu, smax, k));
+        }
+        if ((threadIdx.x & 31) == 0) {
+            s_sum[threadIdx.x >> 5] = ssum;
+            s_max[threadIdx.x >> 5] = smax;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {  // one atomic per CTA and statistic
+            for (int w = 1; w < kWarps; ++w) {
+                ssum += s_sum[w];
+                smax = max(smax, s_max[w]);
+            }
+            if (ssum) atomicAdd((unsigned long long *)&a.abs_sum[L], (unsigned long long)ssum);
+            if (smax) atomicMax((unsigned long long *)&a.max_rec[L], (unsigned long long)smax);
+        }
     }
 }
 
@@ -1090,7 +1096,11 @@ cudaError_t launch_d(const K1Args &a, cudaStream_t s, int mode) {
 }
 cudaError_t launch_any(const K1Args &a_in, cudaStream_t s, int mode) {
     if (use_v8(a_in)) {
-        if (mode == kEmit) return launch_v8(a_in, s);
+        if (mode == kEmit) {
+            K1Args a = a_in;
+            a.stats_in_copy = true;
+            return launch_v8(a, s);
+        }
     }
     K1Args a = a_in;
     if (a.ndim == 3 && a.TX != 32) {  // the scalar kernel's statistics pass over 32-wide column blocks
