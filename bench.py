@@ -11,7 +11,8 @@ Sub-records in the same JSON line ("configs"), each timed the same way with its
 own oracle cpu_baseline sample from the same run:
   config1   32x32 u8 TOP, 32 directions: ECT + Radon (latency, us per step)
   config2   1024 x 28x28 blob images + binary variant, 256 directions: ECT + Radon
-            + fused HT (kappa = sin, fp64) — round 1's headline workload
+  config2_fused_ht  the same + the histogram-fused HT (kappa = sin, fp64; NEXT f2)
+            — round 1's headline workload
   config3   2048^2 int16 GRF, 4096 directions: ECT + Radon
   config5   16 x 128^3 volumes, 10^4 directions: HT with exp(-t^2/2) and
             cos(2 pi t/64) in fp64 and fp32 (BJ:11): terms/s, GFLOP/s, LSU and FP32
@@ -230,7 +231,7 @@ def workload(name, rank=0):
         dirs, nfix = synth.fibonacci_directions(1024, 32.0)
         return dict(images=np.stack([gray, synth.median_binarize(gray)]), dirs=dirs, construction="vertex",
                     variants="gray + binary (v > median)", zero_fixed=nfix)
-    if name == "config2":
+    if name in ("config2", "config2_fused_ht"):
         gray = synth.blob_images(C2_IMAGES, 28, synth.IMAGE_SEED[2] + sh)
         return dict(images=np.concatenate([gray, synth.binarize(gray, 128)]),
                     dirs=synth.random_directions(256, 2, 16, synth.DIR_SEED[2]), construction="vertex",
@@ -259,7 +260,9 @@ DESCR = {
                "as one batch, vertex construction, 1024 integer-rounded Fibonacci directions (x32); exact ECT + Radon "
                "(all three streams) per image-direction",
     "config2": "BASELINE.json configs[1]: 1024 x 28x28 u8 Gaussian-blob images + binary variant (>=128), vertex "
-               "construction, 256 integer directions in [-16,16]^2; ECT + Radon + HT (kappa=sin, fp64, fused into K2)",
+               "construction, 256 integer directions in [-16,16]^2; ECT + Radon for every image",
+    "config2_fused_ht": "BASELINE.json configs[1] as config2, plus the HT (kappa=sin, fp64) from K2's merged "
+                        "histogram (NEXT f2, eucalc_transforms_ht)",
     "config3": "BASELINE.json configs[2]: 2048^2 int16 k^-3 Gaussian random field (256 levels), vertex construction, "
                "4096 integer directions in [-64,64]^2; exact ECT + Radon",
     "config1": "BASELINE.json configs[0]: 32x32 u8 uniform, top construction, 32 directions in [-8,8]^2; ECT + Radon",
@@ -381,12 +384,13 @@ def cpu_baseline(name, w, n_dirs):
     rng = np.random.default_rng(1)
     dirs = w["dirs"]
     images = w["images"]
-    if name == "config2":
+    if name in ("config2", "config2_fused_ht"):
         n_img = n_dirs  # images per variant
         imgs = np.concatenate([images[:n_img], images[C2_IMAGES:C2_IMAGES + n_img]])
-        units, secs, tg, td = oracle_transforms_sample(imgs, dirs, "vertex", list(range(len(dirs))),
-                                                       ht=(HT_KERNEL_C2, 1.0))
-        sample = f"first {n_img} gray + {n_img} binary images x all {len(dirs)} directions (ECT+Radon + HT quadrature)"
+        ht = (HT_KERNEL_C2, 1.0) if name == "config2_fused_ht" else None
+        units, secs, tg, td = oracle_transforms_sample(imgs, dirs, "vertex", list(range(len(dirs))), ht=ht)
+        sample = (f"first {n_img} gray + {n_img} binary images x all {len(dirs)} directions (ECT+Radon"
+                  + (" + HT quadrature)" if ht else ")"))
     else:
         dsel = sorted(rng.choice(len(dirs), min(n_dirs, len(dirs)), replace=False).tolist())
         units, secs, tg, td = oracle_transforms_sample(images, dirs, w["construction"], dsel)
@@ -591,7 +595,8 @@ def gpu_arm(args):
     subs = {}
     if dist.world == 1 and not args.headline_only:
         sub_steps = max(3, min(args.steps, 10))
-        for name, ht in (("config2", (HT_KERNEL_C2, 1.0, "f64")), ("config3", None), ("config1", None)):
+        for name, ht in (("config2", None), ("config2_fused_ht", (HT_KERNEL_C2, 1.0, "f64")), ("config3", None),
+                         ("config1", None)):
             if name not in args.sub:
                 continue
             rec, wsub, _ = record_transforms(name, eu, torch, args, dist, flush, clk,
@@ -602,7 +607,8 @@ def gpu_arm(args):
             t, s = traffic_for(name)
             rec["roofline"]["traffic"], rec["roofline"]["traffic_source"] = t, s
             if not args.no_cpu_baseline:
-                rec["cpu_baseline"] = cpu_baseline(name, wsub, {"config2": 96, "config3": 192, "config1": 32}[name])
+                rec["cpu_baseline"] = cpu_baseline(name, wsub, {"config2": 96, "config2_fused_ht": 64, "config3": 192,
+                                                                "config1": 32}[name])
             subs[name] = rec
             torch.cuda.empty_cache()
         if "config5" in args.sub:
@@ -734,7 +740,7 @@ def main(argv=None):
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--shard", default="images", choices=["images", "directions"])
-    ap.add_argument("--sub", default="config1,config2,config3,config5",
+    ap.add_argument("--sub", default="config1,config2,config2_fused_ht,config3,config5",
                     help="sub-records to add at N=1 (comma list)")
     ap.add_argument("--headline-only", action="store_true")
     ap.add_argument("--ref-sample", type=int, default=4, help="directions per volume per --impl reference step")

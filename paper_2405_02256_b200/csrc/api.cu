@@ -504,6 +504,14 @@ eucalc_status plan_units(PlanEntry &pe) {
     return EUCALC_OK;
 }
 
+// Writes `gen` to a host-mapped word after everything before it on the stream
+// (the read-back copies): the host polls that word with plain loads instead of
+// cudaEventSynchronize, whose wake-up took ~60 us on the GPU boxes' VM.
+__global__ void k1_signal(volatile unsigned *flag, unsigned gen) {
+    __threadfence_system();
+    *flag = gen;
+}
+
 eucalc_status sync_counts(Critical *cr, cudaStream_t st) {
     std::lock_guard<std::mutex> lk(cr->mu);
     if (cr->have_host) return EUCALC_OK;
@@ -515,7 +523,22 @@ eucalc_status sync_counts(Critical *cr, cudaStream_t st) {
     cr->h_stats = new (std::nothrow) int64_t[ns];
     if (!cr->h_count || !cr->h_stats) return fail(EUCALC_E_NOMEM, "host alloc");
     // the read-back was enqueued right after K1 into pinned memory: wait for it only
-    CK(cudaEventSynchronize(cr->k1_done));
+    // (poll the signal word; the event still decides on errors and when no word was set up)
+    bool landed = false;
+    if (cr->pinned_flag_off) {
+        const volatile unsigned *f = (const volatile unsigned *)((unsigned char *)cr->pinned + cr->pinned_flag_off);
+        for (uint64_t n = 1;; ++n) {
+            if (*f == 1u) {
+                landed = true;
+                break;
+            }
+            if ((n & 4095) == 0) {
+                const cudaError_t q = cudaEventQuery(cr->k1_done);
+                if (q != cudaErrorNotReady) break;
+            }
+        }
+    }
+    if (!landed) CK(cudaEventSynchronize(cr->k1_done));
     const int32_t *c = (const int32_t *)cr->pinned;
     memcpy(cr->h_stats, (const unsigned char *)cr->pinned + cr->pinned_stats_off, sizeof(int64_t) * ns);
     cr->max_count = 0;
@@ -948,15 +971,30 @@ eucalc_status eucalc_critical_points(const eucalc_complex *cx, void *stream, euc
         // asynchronous read-back of the list lengths and |Delta^-| statistics into
         // pinned memory; sync_counts() later waits on this event only
         cr->pinned_stats_off = ((sizeof(int32_t) * nlist + 15) / 16) * 16;
-        const size_t need = cr->pinned_stats_off + sizeof(int64_t) * nstats;
+        const size_t flag_off = ((cr->pinned_stats_off + sizeof(int64_t) * nstats + 15) / 16) * 16;
+        const size_t need = flag_off + 16;
         cr->pinned = pinned_get(need, &cr->pinned_bytes);
         if (e == cudaSuccess && !cr->pinned) e = cudaErrorMemoryAllocation;
+        unsigned *dflag = nullptr;
+        if (e == cudaSuccess) {
+            *(volatile unsigned *)((unsigned char *)cr->pinned + flag_off) = 0u;
+            if (cudaHostGetDevicePointer((void **)&dflag, (unsigned char *)cr->pinned + flag_off, 0) != cudaSuccess) {
+                cudaGetLastError();
+                dflag = nullptr;
+            }
+        }
         if (e == cudaSuccess) e = cudaEventCreateWithFlags(&cr->k1_done, cudaEventDisableTiming);
         if (e == cudaSuccess)
             e = cudaMemcpyAsync(cr->pinned, cr->d_count, sizeof(int32_t) * nlist, cudaMemcpyDeviceToHost, st);
         if (e == cudaSuccess)
             e = cudaMemcpyAsync((unsigned char *)cr->pinned + cr->pinned_stats_off, cr->d_stats,
                                 sizeof(int64_t) * nstats, cudaMemcpyDeviceToHost, st);
+        if (e == cudaSuccess && dflag) {
+            k1_signal<<<1, 1, 0, st>>>(dflag, 1u);
+            count_launch();
+            e = cudaGetLastError();
+            if (e == cudaSuccess) cr->pinned_flag_off = flag_off;
+        }
         if (e == cudaSuccess) e = cudaEventRecord(cr->k1_done, st);
     }
     if (cnt) cudaFreeAsync(cnt, st);
@@ -1154,12 +1192,34 @@ eucalc_status transforms_impl(const eucalc_critical *ccr, const int32_t *dirs, i
                                     stream);
         }
     }
-    int64_t bnd = 0;
-    s = bounds(cr, p, st, bnd);
+    // Output bound: the tight one (sum over (image, direction) of min(list length,
+    // R), O(batch * Q * log D) on the host, ~60 us at config 2's 2048 images) only
+    // when the no-K1 upper bound (sum of min(vertices, R), O(D)) is not already
+    // covered by every capacity, or host outputs need scratch sized by it.
+    s = sync_counts(cr, st);
     if (s != EUCALC_OK) return s;
-    tr.mark("bounds(k1 wait)");
-    if (required_out) *required_out = bnd;
+    tr.mark("k1 wait");
     eucalc_steps *outs[3] = {ect, ordinary, classical};
+    bool host_out = false;
+    for (eucalc_steps *o : outs)
+        if (o && o->value && !is_device_ptr(o->value)) host_out = true;
+    int64_t bnd = 0;
+    {
+        int64_t ub = 0;
+        for (const DirInfo &di : p.info) ub += std::min<int64_t>(cx->nvert, di.R);
+        ub *= cx->batch;
+        bool covered = !host_out && ub < (int64_t(1) << 31);
+        for (eucalc_steps *o : outs)
+            if (o && o->capacity < ub) covered = false;
+        if (covered) {
+            bnd = ub;
+        } else {
+            s = bounds(cr, p, st, bnd);
+            if (s != EUCALC_OK) return s;
+        }
+    }
+    tr.mark("bound");
+    if (required_out) *required_out = bnd;
     int eb = 0;
     for (eucalc_steps *o : outs) {
         if (!o) continue;
@@ -1186,10 +1246,7 @@ eucalc_status transforms_impl(const eucalc_critical *ccr, const int32_t *dirs, i
         return fail(EUCALC_E_RANGE, "more than 2^31 - 2^24 (image, direction) segments in one call");
     const bool cls_alias = classical && ect && (classical->height == ect->height || !classical->height);
     if (classical && !classical->height && !ect) return fail(EUCALC_E_ARG, "classical height is NULL");
-    // host outputs -> device scratch
-    bool host_out = false;
-    for (eucalc_steps *o : outs)
-        if (o && !is_device_ptr(o->value)) host_out = true;
+    // host outputs -> device scratch (sized by the tight bound)
     const size_t esz = (size_t)eb;
     std::vector<void *> scratch;
     auto dalloc = [&](size_t bytes) -> void * {

@@ -94,6 +94,7 @@ struct Critical {
     bool have_orthant_counts = false;  // N^-, N^ord computed (eucalc_critical_counts)
     void *pinned = nullptr;         // pinned host copy: int32 counts, then int64 stats
     size_t pinned_bytes = 0, pinned_stats_off = 0;
+    size_t pinned_flag_off = 0;     // signal word (k1_signal) polled by sync_counts, 0 = none
 };
 
 // Pinned host memory pool (power-of-two size classes, reused; never unpinned).

@@ -41,7 +41,7 @@ def main():
     reps = int(sys.argv[2]) if len(sys.argv) > 2 else 5
     w = bench.workload(name, 0)
     imgs = torch.from_numpy(np.ascontiguousarray(w["images"])).cuda()
-    ht = (bench.HT_KERNEL_C2, 1.0, "f64") if name == "config2" else None
+    ht = (bench.HT_KERNEL_C2, 1.0, "f64") if name == "config2_fused_ht" else None
     for _ in range(3):
         bench.transforms_step(eu, imgs, w["dirs"], w["construction"], ht)
     torch.cuda.synchronize()

@@ -34,7 +34,7 @@ def main():
         for _ in range(iters):
             eu.hybrid(cr, w["dirs"], kern, param, prec, algorithm=alg)
     else:
-        ht = (bench.HT_KERNEL_C2, 1.0, "f64") if name == "config2" else None
+        ht = (bench.HT_KERNEL_C2, 1.0, "f64") if name == "config2_fused_ht" else None
         for _ in range(iters):
             bench.transforms_step(eu, imgs, w["dirs"], w["construction"], ht)
     torch.cuda.synchronize()
