@@ -15,7 +15,9 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libeucalc.so")
+# EUCALC_LIB=checked loads libeucalc_checked.so (device bounds checks compiled in;
+# tests only): the same kernels, every EU_DCHECK traps on an out-of-range index
+LIB_PATH = os.path.join(_HERE, "libeucalc_checked.so" if os.environ.get("EUCALC_LIB") == "checked" else "libeucalc.so")
 
 OK, E_ARG, E_NOMEM, E_CUDA, E_NONGENERIC, E_CAPACITY, E_RANGE, E_STATE = range(8)
 DTYPES = {np.dtype(np.uint8): 0, np.dtype(np.int16): 1, np.dtype(np.int32): 2}

@@ -11,6 +11,7 @@ from concurrent.futures import ThreadPoolExecutor
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libeucalc.so")
+LIB_CHECKED = os.path.join(HERE, "libeucalc_checked.so")  # device bounds checks (EU_DCHECK), tests only
 INCLUDE = os.path.join(os.path.dirname(HERE), "include")
 OBJ = os.path.join(HERE, "build")
 
@@ -24,10 +25,10 @@ def sources():
     return sorted(glob.glob(os.path.join(CSRC, "*.cu")))
 
 
-def needs_build() -> bool:
-    if not os.path.exists(LIB):
+def needs_build(lib=LIB) -> bool:
+    if not os.path.exists(lib):
         return True
-    t = os.path.getmtime(LIB)
+    t = os.path.getmtime(lib)
     deps = sources() + glob.glob(os.path.join(CSRC, "*.cuh")) + [os.path.join(INCLUDE, "eucalc.h")]
     return any(os.path.getmtime(p) > t for p in deps)
 
@@ -36,20 +37,26 @@ def _nvcc():
     return os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not needs_build():
-        return LIB
-    os.makedirs(OBJ, exist_ok=True)
+def build(force: bool = False, verbose: bool = False, checked: bool = False) -> str:
+    """Compile libeucalc.so (or, checked=True, libeucalc_checked.so with the device
+    bounds checks of EU_DCHECK compiled in; objects in build/checked)."""
+    lib = LIB_CHECKED if checked else LIB
+    obj_dir = os.path.join(OBJ, "checked") if checked else OBJ
+    extra = ["-DEUCALC_DEVICE_CHECKS"] if checked else []
+    if not force and not needs_build(lib):
+        return lib
+    os.makedirs(obj_dir, exist_ok=True)
 
     headers = glob.glob(os.path.join(CSRC, "*.cuh")) + [os.path.join(INCLUDE, "eucalc.h")]
 
     def compile_one(src):
-        obj = os.path.join(OBJ, os.path.basename(src) + ".o")
+        obj = os.path.join(obj_dir, os.path.basename(src) + ".o")
         if not force and os.path.exists(obj):  # object newer than its source and every header: reuse
             t = os.path.getmtime(obj)
             if all(os.path.getmtime(p) < t for p in [src, *headers]):
                 return obj, subprocess.CompletedProcess([], 0, "", "")
-        r = subprocess.run([_nvcc(), *NVCC_FLAGS, "-I", INCLUDE, "-c", "-o", obj, src], capture_output=True, text=True)
+        r = subprocess.run([_nvcc(), *NVCC_FLAGS, *extra, "-I", INCLUDE, "-c", "-o", obj, src], capture_output=True,
+                           text=True)
         return obj, r
 
     with ThreadPoolExecutor(len(sources())) as ex:
@@ -59,16 +66,17 @@ def build(force: bool = False, verbose: bool = False) -> str:
         logs.append(r.stdout + r.stderr)
         if r.returncode != 0:
             raise RuntimeError("nvcc failed:\n" + r.stdout + r.stderr)
-    r = subprocess.run([_nvcc(), "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-o", LIB + ".tmp",
+    r = subprocess.run([_nvcc(), "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-o", lib + ".tmp",
                         *[o for o, _ in results]], capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError("link failed:\n" + r.stdout + r.stderr)
     if verbose:
         print("\n".join(logs))
-    os.replace(LIB + ".tmp", LIB)
-    return LIB
+    os.replace(lib + ".tmp", lib)
+    return lib
 
 
 if __name__ == "__main__":
-    build(force=True, verbose=True)
-    print(LIB)
+    import sys
+
+    print(build(force=True, verbose=True, checked="--checked" in sys.argv))

@@ -1350,6 +1350,10 @@ eucalc_status transforms_impl(const eucalc_critical *ccr, const int32_t *dirs, i
         a.ect = dev[0];
         a.ord = dev[1];
         a.cls = dev[2];
+        a.out_cap = INT64_MAX;  // device checks: the smallest capacity of the requested outputs
+        for (int i = 0; i < 3; ++i)
+            if (outs[i]) a.out_cap = std::min<int64_t>(a.out_cap, host_out ? std::max<int64_t>(bnd, 1) : outs[i]->capacity);
+        if (getenv("EUCALC_DCHECK_INJECT")) a.out_cap = 1;  // test hook: the checked library must trap
         a.flags = flags;
         a.ticket = ticket;
         a.cnt_c = cnts;

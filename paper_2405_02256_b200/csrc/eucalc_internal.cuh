@@ -11,6 +11,24 @@
 
 #include "../../include/eucalc.h"
 
+// Device-side bounds checks (the stand-in for compute-sanitizer memcheck, which
+// the GPU pool does not allow): built into libeucalc_checked.so only
+// (_build.build(checked=True), -DEUCALC_DEVICE_CHECKS); a failed check prints
+// the file and line and traps, so the launch (and the test) fails with E_CUDA.
+#ifdef EUCALC_DEVICE_CHECKS
+#include <cstdio>
+#define EU_DCHECK(cond)                                                                        \
+    do {                                                                                       \
+        if (!(cond)) {                                                                         \
+            printf("EU_DCHECK failed: %s:%d: %s (block %d thread %d)\n", __FILE__, __LINE__, #cond, \
+                   (int)blockIdx.x, (int)threadIdx.x);                                         \
+            __trap();                                                                          \
+        }                                                                                      \
+    } while (0)
+#else
+#define EU_DCHECK(cond) ((void)0)
+#endif
+
 namespace eucalc {
 
 constexpr int kMaxN = 3;
@@ -200,6 +218,7 @@ struct K2Args {
     double ht_scale;            // HT = ht_scale * sum_h H_J(h) f(u(h))
     int ht_prec;
     void *ht_out;               // [batch][D]
+    int64_t out_cap;            // entries every requested output array holds (device checks)
 };
 cudaError_t launch_k2(const K2Args &a, cudaStream_t s, int num_sms);
 // unit path geometry: packed histogram words per CTA, directions per unit, split window

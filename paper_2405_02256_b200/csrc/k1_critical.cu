@@ -562,6 +562,7 @@ __global__ void __launch_bounds__(kThreads, 3) k1_pencil(K1Args a) {
                 const int da = dm[q], db = dm[q ^ FULL];
                 const bool keep = (da | db) != 0;
                 const unsigned bal = __ballot_sync(0xffffffffu, keep);
+                EU_DCHECK(!keep || run[q] + __popc(bal & ((1u << lane) - 1)) < (a.direct ? (int)a.vcap : a.cap_r));
                 st_rec_if(dst[q] + run[q] + __popc(bal & ((1u << lane) - 1)), coord, da, db, keep);
                 const int s = abs(da) + abs(db);
                 abs_sum[q] += s;
@@ -854,6 +855,7 @@ __global__ void __launch_bounds__(kThreads, 3) k1_pencil_v8(K1Args a) {
             const unsigned b0 = __ballot_sync(0xffffffffu, k0), b1 = __ballot_sync(0xffffffffu, k1);
             if ((b0 | b1) == 0) continue;  // nothing kept by the warp (most steps of binary images)
             const int p0 = run[q] + __popc(b0 & lt) + __popc(b1 & lt);
+            EU_DCHECK(p0 + (int)k0 + (int)k1 <= a.cap_r || (a.direct && p0 + 2 <= a.vcap));
             v8::st_rec_w(dst[q] + p0, coord, r0, k0);
             v8::st_rec_w(dst[q] + p0 + (int)k0, coord + cstep, r1, k1);
             run[q] += __popc(b0) + __popc(b1);
@@ -1002,6 +1004,7 @@ __global__ void __launch_bounds__(kThreads) k1_copy(K1Args a, long long cpl) {
             if (s_off[mid] <= x) lo = mid;
             else hi = mid - 1;
         }
+        EU_DCHECK(x - s_off[lo] >= 0 && x - s_off[lo] < a.cap_r && base + d < a.vcap);
         const RecT r = src[(long long)lo * a.cap_r + (x - s_off[lo])];
         dst[d] = r;
         if (a.stats_in_copy) {

@@ -285,7 +285,10 @@ __global__ void __launch_bounds__(kThreads) k3t(K3Args a) {
                     r[3] = make_int2(p1.z, p1.w);
                 }
 #pragma unroll
-                for (int u = 0; u < 4; ++u) k[u] = tab[table_index<DP>((uint32_t)r[u].x, di.xs8, off)];
+                for (int u = 0; u < 4; ++u) {
+                    EU_DCHECK((unsigned)table_index<DP>((uint32_t)r[u].x, di.xs8, off) < (unsigned)half);
+                    k[u] = tab[table_index<DP>((uint32_t)r[u].x, di.xs8, off)];
+                }
 #pragma unroll
                 for (int u = 0; u < 4; ++u) {
                     if (u & 1) add(acc1, cmp1, r[u], k[u]);
@@ -294,6 +297,7 @@ __global__ void __launch_bounds__(kThreads) k3t(K3Args a) {
             }
             for (; i < cnt; ++i) {
                 const S r0 = srec[i];
+                EU_DCHECK((unsigned)table_index<DP>((uint32_t)r0.x, di.xs8, off) < (unsigned)half);
                 add(acc0, cmp0, r0, tab[table_index<DP>((uint32_t)r0.x, di.xs8, off)]);
             }
         }

@@ -11,7 +11,7 @@ timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --lo
 echo "launches rc=$?"
 python tools/ncu_summary.py launches $OUT/launches.csv > $OUT/launches.txt 2>&1; head -20 $OUT/launches.txt
 M=dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum
-for c in config4 config2 config3; do
+for c in config4 config2 config2_fused_ht config3; do
   python tools/run_config.py $c 2 > $OUT/plain_$c.log 2>&1 && \
   timeout 900 ncu --metrics $M --clock-control none --csv --log-file $OUT/traffic_$c.csv python tools/run_config.py $c 2 > $OUT/ncu_traffic_$c.log 2>&1
   echo "traffic $c rc=$?"
@@ -24,10 +24,10 @@ for kp in "gauss f32" "gauss f64" "cos f32" "cos f64"; do
   echo "k3t $1 $2 rc=$?"
 done
 python tools/run_config.py config4 2 > $OUT/plain_c4b.log 2>&1 && \
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:k2_block -s 1 -c 1 -o $OUT/k2block_c4 python tools/run_config.py config4 2 > $OUT/ncu_full_c4.log 2>&1
-echo "full k2_block rc=$?"
-python tools/ncu_summary.py full $OUT/k2block_c4.ncu-rep > $OUT/k2block_c4.full.txt 2>&1
-python tools/ncu_source.py $OUT/k2block_c4.ncu-rep 30 > $OUT/k2block_c4.source.txt 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:k2_unit -s 2 -c 1 -o $OUT/k2unit_c4 python tools/run_config.py config4 2 > $OUT/ncu_full_c4.log 2>&1
+echo "full k2_unit rc=$?"
+python tools/ncu_summary.py full $OUT/k2unit_c4.ncu-rep > $OUT/k2unit_c4.full.txt 2>&1
+python tools/ncu_source.py $OUT/k2unit_c4.ncu-rep 30 > $OUT/k2unit_c4.source.txt 2>&1
 python tools/run_config.py config5 1 cos f32 > $OUT/plain_c5full.log 2>&1 && \
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:k3t -c 1 -o $OUT/k3t_c5 python tools/run_config.py config5 1 cos f32 > $OUT/ncu_full_c5.log 2>&1
 echo "full k3t rc=$?"
@@ -35,3 +35,4 @@ python tools/ncu_summary.py full $OUT/k3t_c5.ncu-rep > $OUT/k3t_c5.full.txt 2>&1
 python tools/ncu_source.py $OUT/k3t_c5.ncu-rep 30 > $OUT/k3t_c5.source.txt 2>&1
 rm -f $OUT/*.ncu-rep
 du -sh $OUT
+python tools/ncu_records.py $OUT $OUT/records > $OUT/records.log 2>&1; cat $OUT/records.log | head -30
