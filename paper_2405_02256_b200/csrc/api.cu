@@ -1157,6 +1157,175 @@ struct HtReq {
 
 eucalc_status transforms_impl(const eucalc_critical *ccr, const int32_t *dirs, int64_t D, eucalc_steps *ect,
                               eucalc_steps *ordinary, eucalc_steps *classical, const HtReq *ht, int64_t *required_out,
+                              void *stream);
+
+// The library's device-to-host copy stream of the current device (non-blocking).
+cudaStream_t copy_stream() {
+    static std::mutex mu;
+    static cudaStream_t s[64] = {};
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return nullptr;
+    std::lock_guard<std::mutex> lk(mu);
+    if (!s[dev] && cudaStreamCreateWithFlags(&s[dev], cudaStreamNonBlocking) != cudaSuccess) {
+        cudaGetLastError();
+        s[dev] = nullptr;
+    }
+    return s[dev];
+}
+
+// Host outputs of a batch of >= 2 images, in image chunks: the transforms of
+// every chunk are enqueued on `st` into device scratch (a view of the critical
+// handle restricted to the chunk's images, its own CSR), and each chunk's
+// results are copied back on the copy stream while the next chunks compute;
+// offsets are shifted to the global CSR on the host. Capacities and ranges were
+// checked for the whole call by the caller.
+eucalc_status transforms_host_chunked(eucalc_critical *cr, const int32_t *dirs, int64_t D, eucalc_steps *const outs[3],
+                                      bool cls_alias, int eb, const HtReq *ht, int64_t nch, cudaStream_t st) {
+    const Complex *cx = cr->cx;
+    const int64_t B = cx->batch;
+    const size_t esz = (size_t)eb, rsz = cr->wide ? sizeof(Rec32) : sizeof(Rec16);
+    const size_t ht_osz = ht && ht->precision == EUCALC_F32 ? 4 : 8;
+    cudaStream_t cs = copy_stream();
+    if (!cs) return fail(EUCALC_E_CUDA, "copy stream");
+    std::shared_ptr<PlanEntry> pe;
+    eucalc_status s = get_plan(cx, dirs, D, st, pe);
+    if (s != EUCALC_OK) return s;
+    struct Chunk {
+        eucalc_complex vcx;
+        eucalc_critical vcr;
+        int64_t b0 = 0, nb = 0;
+        StepsOut dv[3] = {};
+        void *dht = nullptr;
+        cudaEvent_t ev = nullptr;
+        std::vector<void *> mem;
+    };
+    std::vector<std::unique_ptr<Chunk>> chunks;
+    auto release = [&]() {
+        for (auto &c : chunks) {
+            for (void *q : c->mem) cudaFreeAsync(q, cs);
+            if (c->ev) cudaEventDestroy(c->ev);
+        }
+    };
+    cudaError_t e = cudaSuccess;
+    for (int64_t c = 0; c < nch && s == EUCALC_OK && e == cudaSuccess; ++c) {
+        auto ch = std::make_unique<Chunk>();
+        ch->b0 = B * c / nch;
+        ch->nb = B * (c + 1) / nch - ch->b0;
+        Complex &v = ch->vcx;
+        v.ndim = cx->ndim;
+        v.dtype = cx->dtype;
+        v.construction = cx->construction;
+        v.batch = ch->nb;
+        std::copy(cx->m, cx->m + kMaxN, v.m);
+        std::copy(cx->M, cx->M + kMaxN, v.M);
+        v.npix = cx->npix;
+        v.nvert = cx->nvert;
+        v.d_img = (unsigned char *)cx->d_img + ch->b0 * cx->npix * (cx->dtype == EUCALC_U8 ? 1 : cx->dtype == EUCALC_I16 ? 2 : 4);
+        v.max_abs_w = cx->max_abs_w;
+        std::copy(cx->sh, cx->sh + kMaxN, v.sh);
+        std::copy(cx->msk, cx->msk + kMaxN, v.msk);
+        v.aligned = cx->aligned;
+        v.L = cx->L;
+        std::copy(cx->scale, cx->scale + kMaxN, v.scale);
+        v.owner_stream = st;
+        Critical &r = ch->vcr;
+        r.cx = &ch->vcx;
+        r.Q = cr->Q;
+        r.wide = cr->wide;
+        r.vcap = cr->vcap;
+        r.d_rec = (unsigned char *)cr->d_rec + (size_t)(ch->b0 * cr->Q) * (size_t)cr->vcap * rsz;
+        r.d_count = cr->d_count + ch->b0 * cr->Q;
+        r.d_tile_off = cr->d_tile_off + ch->b0 * cr->Q * (int64_t)(cr->ntiles + 1);
+        r.TX = cr->TX;
+        r.TY = cr->TY;
+        r.TZ = cr->TZ;
+        r.tiles_x = cr->tiles_x;
+        r.tiles_y = cr->tiles_y;
+        r.tiles_z = cr->tiles_z;
+        r.ntiles = cr->ntiles;
+        r.have_host = true;
+        r.h_count = cr->h_count + ch->b0 * cr->Q;
+        r.max_count = cr->max_count;
+        r.max_abs_sum = cr->max_abs_sum;
+        r.max_rec = cr->max_rec;
+        r.owner_stream = st;
+        int64_t bnd = 0;
+        s = bounds(&ch->vcr, pe->p, st, bnd);
+        if (s != EUCALC_OK) break;
+        const int64_t Sc = ch->nb * D;
+        auto dalloc = [&](size_t bytes) -> void * {
+            void *q = nullptr;
+            if (cudaMallocAsync(&q, std::max<size_t>(bytes, 1), st) != cudaSuccess) return nullptr;
+            ch->mem.push_back(q);
+            return q;
+        };
+        eucalc_steps ds[3] = {};
+        eucalc_steps *dsp[3] = {nullptr, nullptr, nullptr};
+        for (int i = 0; i < 3 && e == cudaSuccess; ++i) {
+            if (!outs[i]) continue;
+            ch->dv[i].off = (int64_t *)dalloc(sizeof(int64_t) * (Sc + 1));
+            ch->dv[i].v = dalloc(esz * std::max<int64_t>(bnd, 1));
+            ch->dv[i].h = (i == 2 && cls_alias) ? ch->dv[0].h : dalloc(esz * std::max<int64_t>(bnd, 1));
+            if (!ch->dv[i].off || !ch->dv[i].v || !ch->dv[i].h) e = cudaErrorMemoryAllocation;
+            ds[i] = eucalc_steps{ch->dv[i].off, ch->dv[i].h, ch->dv[i].v, std::max<int64_t>(bnd, 1), eb, 0};
+            dsp[i] = &ds[i];
+        }
+        HtReq hc{};
+        if (ht && e == cudaSuccess) {
+            hc = *ht;
+            ch->dht = dalloc(ht_osz * std::max<int64_t>(Sc, 1));
+            hc.out = ch->dht;
+            if (!ch->dht) e = cudaErrorMemoryAllocation;
+        }
+        if (e != cudaSuccess) break;
+        s = transforms_impl(&ch->vcr, dirs, D, dsp[0], dsp[1], dsp[2], ht ? &hc : nullptr, nullptr, st);
+        if (s != EUCALC_OK) break;
+        e = cudaEventCreateWithFlags(&ch->ev, cudaEventDisableTiming);
+        if (e == cudaSuccess) e = cudaEventRecord(ch->ev, st);
+        chunks.push_back(std::move(ch));
+    }
+    if (s != EUCALC_OK || e != cudaSuccess) {
+        cudaStreamSynchronize(st);
+        release();
+        cudaStreamSynchronize(cs);
+        return s != EUCALC_OK ? s : cuda_fail(e, "chunked transforms");
+    }
+    // copy back chunk by chunk (each after its own event) while later chunks compute
+    int64_t base[3] = {0, 0, 0};
+    for (auto &ch : chunks) {
+        const int64_t Sc = ch->nb * D, s0 = ch->b0 * D;
+        if (e == cudaSuccess) e = cudaStreamWaitEvent(cs, ch->ev, 0);
+        for (int i = 0; i < 3 && e == cudaSuccess; ++i)
+            if (outs[i]) e = cudaMemcpyAsync(outs[i]->offsets + s0, ch->dv[i].off, sizeof(int64_t) * (Sc + 1),
+                                             cudaMemcpyDeviceToHost, cs);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(cs);
+        for (int i = 0; i < 3 && e == cudaSuccess; ++i) {
+            eucalc_steps *o = outs[i];
+            if (!o) continue;
+            const int64_t n = o->offsets[s0 + Sc];
+            if (n > 0) {
+                e = cudaMemcpyAsync((unsigned char *)o->value + (size_t)base[i] * esz, ch->dv[i].v, esz * (size_t)n,
+                                    cudaMemcpyDeviceToHost, cs);
+                if (e == cudaSuccess && o->height && !(i == 2 && cls_alias))
+                    e = cudaMemcpyAsync((unsigned char *)o->height + (size_t)base[i] * esz, ch->dv[i].h,
+                                        esz * (size_t)n, cudaMemcpyDeviceToHost, cs);
+            }
+            for (int64_t k = 0; k <= Sc; ++k) o->offsets[s0 + k] += base[i];
+            base[i] += n;
+        }
+        if (e == cudaSuccess && ht)
+            e = cudaMemcpyAsync((unsigned char *)ht->out + (size_t)s0 * ht_osz, ch->dht, ht_osz * (size_t)Sc,
+                                cudaMemcpyDeviceToHost, cs);
+    }
+    release();
+    const cudaError_t e2 = cudaStreamSynchronize(cs);
+    if (e == cudaSuccess) e = e2;
+    if (e != cudaSuccess) return cuda_fail(e, "chunked transforms copy-back");
+    return EUCALC_OK;
+}
+
+eucalc_status transforms_impl(const eucalc_critical *ccr, const int32_t *dirs, int64_t D, eucalc_steps *ect,
+                              eucalc_steps *ordinary, eucalc_steps *classical, const HtReq *ht, int64_t *required_out,
                               void *stream) {
     HostTrace tr("transforms");
     if (!ccr) return fail(EUCALC_E_STATE, "NULL handle");
@@ -1246,6 +1415,18 @@ eucalc_status transforms_impl(const eucalc_critical *ccr, const int32_t *dirs, i
         return fail(EUCALC_E_RANGE, "more than 2^31 - 2^24 (image, direction) segments in one call");
     const bool cls_alias = classical && ect && (classical->height == ect->height || !classical->height);
     if (classical && !classical->height && !ect) return fail(EUCALC_E_ARG, "classical height is NULL");
+    // host outputs of several images: chunked, copy-back overlapped with the next chunks
+    if (host_out && cx->batch >= 2) {
+        const char *ev = getenv("EUCALC_HOST_CHUNKS");
+        const int64_t nch = std::min<int64_t>(cx->batch, ev ? std::max(1, atoi(ev)) : 4);
+        if (nch >= 2) {
+            bool all_host = true;  // every output on the host (mixed placements take the plain path)
+            for (eucalc_steps *o : outs)
+                if (o && is_device_ptr(o->value)) all_host = false;
+            if (ht && is_device_ptr(ht->out)) all_host = false;
+            if (all_host) return transforms_host_chunked(cr, dirs, D, outs, cls_alias, eb, ht, nch, st);
+        }
+    }
     // host outputs -> device scratch (sized by the tight bound)
     const size_t esz = (size_t)eb;
     std::vector<void *> scratch;

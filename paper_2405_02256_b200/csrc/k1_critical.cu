@@ -973,10 +973,8 @@ __global__ void __launch_bounds__(kThreads) k1_scan(K1Args a, long long chunks_p
 
 // The records of every (tile, warp) region, from its fixed-capacity scratch
 // region to its scanned position. A CTA owns kCopyRegions consecutive regions of
-// a list, whose destinations form one contiguous range: thread t copies
-// destination records t, t + 256, ... and finds each one's region by binary search
-// over the regions' offsets in shared memory (coalesced stores, mostly coalesced
-// loads, no per-region latency chain).
+// a list; each warp copies whole regions (lanes over the region's records, four
+// records in flight per lane): coalesced loads and stores, no per-record search.
 constexpr int kCopyRegions = 32;
 
 template <typename RecT>
@@ -990,27 +988,39 @@ __global__ void __launch_bounds__(kThreads) k1_copy(K1Args a, long long cpl) {
     for (int i = threadIdx.x; i < nr; i += kThreads) s_off[i] = off[i];
     if (threadIdx.x == 0) s_off[nr] = r0 + nr < nreg ? off[nr] : a.count[L];
     __syncthreads();
-    const int base = s_off[0], T = s_off[nr] - base;
-    const RecT *src = reinterpret_cast<const RecT *>(a.scratch) + L * a.scap + r0 * a.cap_r;
-    RecT *dst = reinterpret_cast<RecT *>(a.rec) + L * a.vcap + base;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const RecT *src0 = reinterpret_cast<const RecT *>(a.scratch) + L * a.scap + r0 * a.cap_r;
+    RecT *dst0 = reinterpret_cast<RecT *>(a.rec) + L * a.vcap;
     long long ssum = 0;
     int smax = 0;
-#pragma unroll 4
-    for (int d = threadIdx.x; d < T; d += kThreads) {
-        const int x = base + d;
-        int lo = 0, hi = nr - 1;  // last region r with s_off[r] <= x
-        while (lo < hi) {
-            const int mid = (lo + hi + 1) >> 1;
-            if (s_off[mid] <= x) lo = mid;
-            else hi = mid - 1;
-        }
-        EU_DCHECK(x - s_off[lo] >= 0 && x - s_off[lo] < a.cap_r && base + d < a.vcap);
-        const RecT r = src[(long long)lo * a.cap_r + (x - s_off[lo])];
-        dst[d] = r;
+    auto stat = [&](const RecT &r) {
         if (a.stats_in_copy) {
             const int v = abs((int)r.a) + abs((int)r.b);
             ssum += v;
             smax = max(smax, v);
+        }
+    };
+    constexpr int U = 4;
+    for (int r = warp; r < nr; r += kWarps) {
+        const int c = s_off[r + 1] - s_off[r];
+        EU_DCHECK(c >= 0 && c <= a.cap_r && s_off[r] + c <= a.vcap);
+        const RecT *src = src0 + (long long)r * a.cap_r;
+        RecT *dst = dst0 + s_off[r];
+        int i = lane;
+        for (; i + (U - 1) * 32 < c; i += U * 32) {
+            RecT v[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) v[u] = src[i + u * 32];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                dst[i + u * 32] = v[u];
+                stat(v[u]);
+            }
+        }
+        for (; i < c; i += 32) {
+            const RecT v = src[i];
+            dst[i] = v;
+            stat(v);
         }
     }
     if (a.stats_in_copy) {  // |Delta^-| statistics of the list (order-independent integer reductions)
@@ -1020,9 +1030,9 @@ __global__ void __launch_bounds__(kThreads) k1_copy(K1Args a, long long cpl) {
             ssum += __shfl_xor_sync(0xffffffffu, ssum, k);
             smax = max(smax, __shfl_xor_sync(0xffffffffu, smax, k));
         }
-        if ((threadIdx.x & 31) == 0) {
-            s_sum[threadIdx.x >> 5] = ssum;
-            s_max[threadIdx.x >> 5] = smax;
+        if (lane == 0) {
+            s_sum[warp] = ssum;
+            s_max[warp] = smax;
         }
         __syncthreads();
         if (threadIdx.x == 0) {  // one atomic per CTA and statistic

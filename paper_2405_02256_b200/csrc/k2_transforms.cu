@@ -139,7 +139,9 @@ template <bool PACK, bool SWZ = false>
 struct Hist {
     unsigned *c;
     unsigned *j;
+    int nb = 0x7fffffff;  // bins the arrays hold (device checks)
     __device__ __forceinline__ void add(int bin, int wc, int wj) const {
+        EU_DCHECK(bin >= 0 && bin < nb);
         const int w = SWZ ? swz(bin) : bin;
         if (PACK) {
             // a kept record has Delta^-(eps) != 0 or Delta^-(-eps) != 0, so (wc, wj) != (0, 0)
@@ -161,6 +163,7 @@ struct Hist {
     // Returns the biased new word; the caller ORs these and tests the OR against
     // the mask once ((x & m) | (y & m) = (x | y) & m).
     __device__ __forceinline__ unsigned add_chk(int bin, int wc, int wj, unsigned bias) const {
+        EU_DCHECK(bin >= 0 && bin < nb);
         const int w = SWZ ? swz(bin) : bin;
         const unsigned v = (unsigned)(wj * 65536 + wc);
         const unsigned old = atomicAdd(c + w, v);
@@ -299,10 +302,11 @@ struct OutPtrs {
     OutT *eh, *ev, *oh, *ov, *ch, *cv;
     const double *tab;  // fused HT (NEXT f2): kbar table over u = 2H - L*csum, or NULL
     bool ect, ord, cls, alias;
+    long long cap;      // entries each array holds (device checks); staging views set their own
     __device__ explicit OutPtrs(const K2Args &a)
         : eh((OutT *)a.ect.h), ev((OutT *)a.ect.v), oh((OutT *)a.ord.h), ov((OutT *)a.ord.v),
           ch((OutT *)a.cls.h), cv((OutT *)a.cls.v), tab(a.ht_tab), ect(a.do_ect), ord(a.do_ord), cls(a.do_cls),
-          alias(a.cls_alias) {}
+          alias(a.cls_alias), cap(a.out_cap) {}
 };
 
 // Fused HT (NEXT row f2): the merged histogram already holds, per lattice
@@ -324,6 +328,7 @@ __device__ __forceinline__ long long ht_tab_off(const K2Args &a, const DirInfo &
 
 template <int MODE, typename OutT>
 __device__ __forceinline__ void put_c(const OutPtrs<OutT> &o, int p, int h, int e, int cv) {
+    EU_DCHECK(p >= 0 && p < o.cap);
     const bool ect = MODE == kModeAny ? o.ect : (MODE & kEct);
     const bool cls = MODE == kModeAny ? o.cls : (MODE & kCls);
     const bool alias = MODE == kModeAny ? o.alias : (MODE & kAlias);
@@ -338,6 +343,7 @@ __device__ __forceinline__ void put_c(const OutPtrs<OutT> &o, int p, int h, int 
 }
 template <int MODE, typename OutT>
 __device__ __forceinline__ void put_o(const OutPtrs<OutT> &o, int p, int h, int r) {
+    EU_DCHECK(p >= 0 && p < o.cap);
     const bool ord = MODE == kModeAny ? o.ord : (MODE & kOrd);
     if (ord) {
         o.oh[p] = (OutT)h;
@@ -365,6 +371,7 @@ __device__ __forceinline__ void st_if(OutT *p, int v, bool pred) {
 }
 template <int MODE, typename OutT>
 __device__ __forceinline__ void put_c_if(const OutPtrs<OutT> &o, int p, int h, int e, int cv, bool pred) {
+    EU_DCHECK(!pred || (p >= 0 && p < o.cap));
     const bool ect = MODE == kModeAny ? o.ect : (MODE & kEct);
     const bool cls = MODE == kModeAny ? o.cls : (MODE & kCls);
     const bool alias = MODE == kModeAny ? o.alias : (MODE & kAlias);
@@ -379,6 +386,7 @@ __device__ __forceinline__ void put_c_if(const OutPtrs<OutT> &o, int p, int h, i
 }
 template <int MODE, typename OutT>
 __device__ __forceinline__ void put_o_if(const OutPtrs<OutT> &o, int p, int h, int r, bool pred) {
+    EU_DCHECK(!pred || (p >= 0 && p < o.cap));
     const bool ord = MODE == kModeAny ? o.ord : (MODE & kOrd);
     if (ord) {
         st_if(o.oh + p, h, pred);
@@ -555,6 +563,7 @@ __device__ __forceinline__ void fill_loop(const K2Args &a, const Hist<PACK> &hs,
         decode<DP>(r0, di, a, bin0, wc0, wj0);
         decode<DP>(r1, di, a, bin1, wc1, wj1);
         if constexpr (PACK && std::is_same<RecT, Rec16>::value) {
+            EU_DCHECK(bin0 >= 0 && bin0 < hs.nb && bin1 >= 0 && bin1 < hs.nb);
             atomicAdd(hs.c + bin0, packed_word<SWAP>(reinterpret_cast<const uint2 &>(r0).y));
             atomicAdd(hs.c + bin1, packed_word<SWAP>(reinterpret_cast<const uint2 &>(r1).y));
         } else {
@@ -568,8 +577,10 @@ __device__ __forceinline__ void fill_loop(const K2Args &a, const Hist<PACK> &hs,
         const RecT r = list[i];
         int bin, wc, wj;
         decode<DP>(r, di, a, bin, wc, wj);
-        if constexpr (PACK && std::is_same<RecT, Rec16>::value)
+        if constexpr (PACK && std::is_same<RecT, Rec16>::value) {
+            EU_DCHECK(bin >= 0 && bin < hs.nb);
             atomicAdd(hs.c + bin, packed_word<SWAP>(reinterpret_cast<const uint2 &>(r).y));
+        }
         else
             hs.add(bin, wc, wj);
         lo = min(lo, bin);
@@ -687,6 +698,7 @@ __device__ __forceinline__ Hist<PACK> warp_hist(unsigned *smem, int rcap) {
     Hist<PACK> hs;
     hs.c = smem + (size_t)warp * rcap * words;
     hs.j = hs.c + rcap;
+    hs.nb = rcap;
     for (int i = threadIdx.x; i < (int)(blockDim.x / 32) * rcap * words; i += blockDim.x) smem[i] = 0;
     __syncthreads();
     return hs;
@@ -1040,6 +1052,7 @@ __device__ __forceinline__ bool block_segment(const K2Args &a, const OutPtrs<Out
     Hist<PACK, true> hs;
     hs.c = hist;
     hs.j = hist + win;
+    hs.nb = win;
     const RecT *recs = reinterpret_cast<const RecT *>(a.rec);
     const DirInfo di = a.dirs[d];
     const RecT *list = recs + (b * a.Q + di.q) * a.vcap;
@@ -1159,10 +1172,10 @@ __device__ __forceinline__ bool block_segment(const K2Args &a, const OutPtrs<Out
 // segment's entries go to the staging buffer `base` at segment-local positions;
 // its counts end in sh.cnt (nc, no) and its HT (if fused) is written. Nothing is
 // published. Returns false when a checked packed fill flagged (rerun split).
-template <bool PACK, int DP, typename RecT, typename OutT>
+template <bool PACK, int DP, typename RecT, typename OutT, typename SH = BlockShared>
 __device__ __forceinline__ bool block_segment_staged(const K2Args &a, const OutPtrs<OutT> &outp, unsigned *hist,
                                                      int win, long long s, long long b, long long d,
-                                                     BlockShared &sh, unsigned chk_mask, OutT *base) {
+                                                     SH &sh, unsigned chk_mask, OutT *base) {
     constexpr bool CHK = PACK;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     unsigned bad = 0;
@@ -1200,6 +1213,8 @@ __device__ __forceinline__ bool block_segment_staged(const K2Args &a, const OutP
     scr.ov = base + 5 * a.stage_cap;
     scr.ect = outp.ect || outp.cls;  // staged heights serve both (T_c = T)
     scr.alias = true;
+    scr.cap = a.units ? di.R : a.stage_cap;  // unit path: the segment's slot; else the CTA's buffer
+    hs.nb = win;
     int pc_carry = 0, po_carry = 0, e_carry = 0, r_carry = 0;
     double ht = 0.0;
     const long long ht_off = outp.tab ? ht_tab_off(a, di) : 0;
@@ -1276,6 +1291,7 @@ __device__ __forceinline__ void copy_out(const OutPtrs<OutT> &outp, const OutT *
                                          long long eo, int nc, int no) {
     const OutT *eh = base, *ev = base + cap, *cv = base + 2 * cap, *ch = base + 3 * cap, *oh = base + 4 * cap,
                *ov = base + 5 * cap;
+    EU_DCHECK(nc <= cap && no <= cap && ec + nc <= outp.cap && eo + no <= outp.cap);
     constexpr int U = 4;
     if (outp.ect || outp.cls) {
         for (int i0 = threadIdx.x; i0 < nc; i0 += U * kBlockThreads) {
@@ -1427,7 +1443,17 @@ __global__ void __launch_bounds__(kBlockThreads, 1) k2_block(K2Args a, long long
 // proves them for every direction of the unit; a flagged unit is redone one
 // direction at a time with split bins (block_segment_staged, one window).
 constexpr int kUnitMax = 4;
-constexpr int kUnitWords = (int)(kBlockSmem / 4);  // packed words of shared histogram per CTA
+// the unit kernel's shared state (no culled-tile list: its segments are single-window)
+struct UnitShared {
+    long long seg;
+    int cnt[2];
+    int wsum[kBlockWarps][4];
+    double ht[kBlockWarps];
+    int hit[1];
+    int nhit;
+};
+constexpr size_t kUnitSmem = 222 * 1024;                // dynamic: 227 KB per CTA minus UnitShared
+constexpr int kUnitWords = (int)(kUnitSmem / 4);  // packed words of shared histogram per CTA
 
 __device__ __forceinline__ void red_smem(unsigned addr, unsigned v) {
     asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(addr), "r"(v));
@@ -1443,6 +1469,7 @@ __device__ __forceinline__ unsigned atom_smem(unsigned addr, unsigned v) {
 struct UnitParams {
     int xs8[kUnitMax], nhlo[kUnitMax];
     unsigned sb[kUnitMax];
+    int nb[kUnitMax];  // R of each direction (device checks)
 };
 
 // Adds records threadIdx.x + k * kBlockThreads of `list` into the G packed
@@ -1468,6 +1495,7 @@ __device__ __forceinline__ unsigned unit_fill(const uint2 *list, int n, const Un
         for (int g = 0; g < G; ++g) {
             int h;
             asm("dp4a.u32.s32 %0, %1, %2, %3;" : "=r"(h) : "r"(r.x), "r"(xs8[g]), "r"(nhlo[g]));
+            EU_DCHECK(h >= 0 && h < pp.nb[g]);
             const unsigned addr = sb[g] + ((unsigned)swz(h) << 2);
             if constexpr (CHK) bad |= atom_smem(addr, w) + w + bias;
             else red_smem(addr, w);
@@ -1499,13 +1527,15 @@ __device__ __noinline__ unsigned unit_fill_any(const uint2 *list, int n, int G, 
 // its staging slot `base` (arrays at stride cap); counts -> sh.cnt, HT written.
 template <typename OutT>
 __device__ __noinline__ void unit_emit(const K2Args &a, const OutPtrs<OutT> &outp, unsigned *hist, int R,
-                                          long long s, const DirInfo &di, BlockShared &sh, OutT *base,
+                                          long long s, const DirInfo &di, UnitShared &sh, OutT *base,
                                           long long cap) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     Hist<true, true> hs;
     hs.c = hist;
     hs.j = hist;
+    hs.nb = R;
     OutPtrs<OutT> scr = outp;
+    scr.cap = R;  // the segment's staging slot
     scr.eh = base;
     scr.ev = base + cap;
     scr.cv = base + 2 * cap;
@@ -1572,8 +1602,8 @@ __device__ __noinline__ void unit_emit(const K2Args &a, const OutPtrs<OutT> &out
 template <typename OutT>
 __device__ __noinline__ void unit_split_segment(const K2Args &a, const OutPtrs<OutT> &outp, unsigned *hist,
                                                 int split_win, long long s, long long b, long long d,
-                                                BlockShared &sh, OutT *base) {
-    block_segment_staged<false, 3, Rec16, OutT>(a, outp, hist, split_win, s, b, d, sh, 0u, base);
+                                                UnitShared &sh, OutT *base) {
+    block_segment_staged<false, 3, Rec16, OutT, UnitShared>(a, outp, hist, split_win, s, b, d, sh, 0u, base);
     __syncthreads();
     if (threadIdx.x == 0) {
         a.cnt_c[s] = sh.cnt[0];
@@ -1584,7 +1614,7 @@ __device__ __noinline__ void unit_split_segment(const K2Args &a, const OutPtrs<O
 template <typename OutT>
 __global__ void __launch_bounds__(kBlockThreads, 1) k2_unit(K2Args a, int split_win) {
     extern __shared__ __align__(16) unsigned hist[];
-    __shared__ BlockShared sh;
+    __shared__ UnitShared sh;
     const OutPtrs<OutT> outp(a);
     OutT *stage = reinterpret_cast<OutT *>(a.stage);
     const unsigned hist_sa = (unsigned)__cvta_generic_to_shared(hist);
@@ -1607,11 +1637,13 @@ __global__ void __launch_bounds__(kBlockThreads, 1) k2_unit(K2Args a, int split_
         for (int g = 0; g < kUnitMax; ++g) {
             pp.xs8[g] = 0;
             pp.nhlo[g] = 0;
+            pp.nb[g] = 0;
             base[g] = 0;
             if (g < G) {
                 const DirInfo &di = a.dirs[a.unit_dirs[un.x + g]];
                 pp.xs8[g] = di.xs8;
                 pp.nhlo[g] = -di.hlo;
+                pp.nb[g] = di.R;
                 base[g] = off;
                 off += (di.R + kGroup - 1) / kGroup * kGroup;
                 proven = proven && min((long long)di.line * a.max_rec, (long long)a.max_abs_sum) < 32768;
@@ -1659,6 +1691,7 @@ __global__ void __launch_bounds__(512) k2_unit_copy(K2Args a) {
         const int nc = a.cnt_c[s], no = a.cnt_o[s];
         const long long ec = a.do_ect ? a.ect.off[s] : a.do_cls ? a.cls.off[s] : 0;
         const long long eo = a.do_ord ? a.ord.off[s] : 0;
+        EU_DCHECK(nc <= a.dirs[d].R && no <= a.dirs[d].R && ec + nc <= outp.cap && eo + no <= outp.cap);
         if (outp.ect || outp.cls) {
             for (int i0 = threadIdx.x; i0 < nc; i0 += U * T) {
                 OutT h[U], v[U], c[U];
@@ -1714,12 +1747,12 @@ __global__ void __launch_bounds__(512) k2_unit_copy(K2Args a) {
 template <typename OutT>
 cudaError_t launch_unit_t(const K2Args &a, cudaStream_t s, int num_sms) {
     auto kern = k2_unit<OutT>;
-    cudaError_t e = prepare_kernel((const void *)kern, kBlockThreads, kBlockSmem, nullptr);
+    cudaError_t e = prepare_kernel((const void *)kern, kBlockThreads, kUnitSmem, nullptr);
     if (e != cudaSuccess) return e;
     const long long total = a.nunits * a.batch, S = a.batch * a.D;
     if (total == 0) return cudaSuccess;
     const int split_win = (int)(kBlockSmem / 8) / kGroup * kGroup;
-    kern<<<(unsigned)std::min<long long>(total, num_sms), kBlockThreads, kBlockSmem, s>>>(a, split_win);
+    kern<<<(unsigned)std::min<long long>(total, num_sms), kBlockThreads, kUnitSmem, s>>>(a, split_win);
     const long long ntiles = (S + 1 + kScanTile - 1) / kScanTile;
     k2_scan<<<(unsigned)ntiles, kScanThreads, 0, s>>>(a, a.cnt_c, a.cnt_o, S, a.flags);
     k2_unit_copy<OutT><<<(unsigned)std::min<long long>(S, 4LL * num_sms), 512, 0, s>>>(a);

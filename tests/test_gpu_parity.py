@@ -243,19 +243,36 @@ def test_output_widths_and_shared_heights():
     assert r["ect"]["value"].element_size() == 4
 
 
-def test_host_buffers_match_device():
-    images = synth.blob_images(8, 28, 2)
-    dirs = synth.random_directions(16, 2, 16, 4)
+@pytest.mark.parametrize("chunks", ["1", "3", None], ids=["plain", "3-chunks", "default-chunks"])
+def test_host_buffers_match_device(chunks, monkeypatch):
+    """Host outputs (copied back chunk by chunk of images while the next chunks
+    compute, offsets shifted on the host; EUCALC_HOST_CHUNKS=1: one pass) equal
+    the device outputs, with and without shared classical heights and the fused HT,
+    in 2-D (warp regime) and 3-D (unit path)."""
+    if chunks:
+        monkeypatch.setenv("EUCALC_HOST_CHUNKS", chunks)
+    vol = synth.smooth_volume(40, 93)
+    cases = [(synth.blob_images(8, 28, 2), synth.random_directions(16, 2, 16, 4)),
+             (np.stack([vol, (vol > np.median(vol)).astype(np.uint8), vol[::-1].copy()]),
+              synth.random_directions(9, 3, 20, 6))]
+    for images, dirs in cases:
+        cx = eu.build_complex(images, "vertex")
+        cr = eu.critical_points(cx)
+        S = images.shape[0] * len(dirs)
+        for share in (False, True):
+            dev = eu.transforms(cr, dirs, device="cuda", share_heights=share, ht=("gauss", 1.0, "f64"))
+            host = eu.transforms(cr, dirs, device="cpu", share_heights=share, ht=("gauss", 1.0, "f64"))
+            np.testing.assert_array_equal(dev.pop("ht").cpu().numpy(), host.pop("ht").numpy())
+            dev = {k: to_np(v) for k, v in dev.items()}
+            host = {k: to_np(v) for k, v in host.items()}
+            for k in dev:
+                n = dev[k]["offsets"][S]
+                np.testing.assert_array_equal(dev[k]["offsets"], host[k]["offsets"])
+                np.testing.assert_array_equal(dev[k]["value"][:n], host[k]["value"][:n])
+                np.testing.assert_array_equal(dev[k]["height"][:n], host[k]["height"][:n])
+    images, dirs = cases[0]
     cx = eu.build_complex(images, "vertex")
     cr = eu.critical_points(cx)
-    dev = {k: to_np(v) for k, v in eu.transforms(cr, dirs, device="cuda").items()}
-    host = {k: to_np(v) for k, v in eu.transforms(cr, dirs, device="cpu").items()}
-    S = images.shape[0] * len(dirs)
-    for k in dev:
-        n = dev[k]["offsets"][S]
-        np.testing.assert_array_equal(dev[k]["offsets"], host[k]["offsets"])
-        np.testing.assert_array_equal(dev[k]["value"][:n], host[k]["value"][:n])
-        np.testing.assert_array_equal(dev[k]["height"][:n], host[k]["height"][:n])
     hd = eu.hybrid(cr, dirs, "gauss", 1.0, "f64", device="cuda").cpu().numpy()
     hh = eu.hybrid(cr, dirs, "gauss", 1.0, "f64", device="cpu").numpy()
     np.testing.assert_array_equal(hd, hh)
