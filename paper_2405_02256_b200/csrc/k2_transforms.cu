@@ -961,6 +961,92 @@ __device__ __forceinline__ void tile_bins(const K2Args &a, const DirInfo &di, in
     bmax = hmax - di.hlo;
 }
 
+__device__ __forceinline__ void red_smem(unsigned addr, unsigned v) {
+    asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(addr), "r"(v));
+}
+__device__ __forceinline__ unsigned atom_smem(unsigned addr, unsigned v) {
+    unsigned old;
+    asm volatile("atom.shared.add.u32 %0, [%1], %2;" : "=r"(old) : "r"(addr), "r"(v));
+    return old;
+}
+
+// Span fill (8-byte records, packed swizzled bins, byte-aligned coordinates): the
+// list ranges ("runs") to stream are cut into chunks of kSpanChunk records, dealt
+// round-robin to the warps; a lane keeps eight 8-byte loads in flight, and a record
+// costs one weight word (packed_word), one dp2a/dp4a (bin relative to the window),
+// the window test (CHECK), the bank swizzle and one shared atomic (CHK: checked, the
+// returned word biased and OR-ed into the result). Runs come from shared tables
+// (s_rb/s_re = record range, s_cpre = exclusive chunk prefix, nruns + 1 entries),
+// or, nruns == 0, the single run [0, n).
+constexpr int kSpanTiles = 2048;  // tiles whose hit mask and run tables fit BlockShared::hit
+constexpr int kSpanChunk = 512;   // records per warp work item
+
+template <int DP, bool CHK, bool SWAP, bool CHECK>
+__device__ __noinline__ unsigned span_fill(const uint2 *list, const int *s_rb, const int *s_re, const int *s_cpre,
+                                           int nruns, int n, int xs8, int nhlo, unsigned wbins, unsigned sb,
+                                           unsigned bias) {
+    constexpr int U = 8;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    unsigned bad = 0;
+    auto one = [&](const uint2 r) {
+        const unsigned w = packed_word<SWAP>(r.y);
+        int h;
+        if (DP == 2) asm("dp2a.lo.u32.s32 %0, %1, %2, %3;" : "=r"(h) : "r"(r.x), "r"(xs8), "r"(nhlo));
+        else asm("dp4a.u32.s32 %0, %1, %2, %3;" : "=r"(h) : "r"(r.x), "r"(xs8), "r"(nhlo));
+        EU_DCHECK(CHECK || (unsigned)h < wbins);
+        if (!CHECK || (unsigned)h < wbins) {
+            const unsigned addr = sb + ((unsigned)swz(h) << 2);
+            if constexpr (CHK) bad |= atom_smem(addr, w) + w + bias;
+            else red_smem(addr, w);
+        }
+    };
+    const bool single = nruns == 0;
+    const int total = single ? (n + kSpanChunk - 1) / kSpanChunk : s_cpre[nruns];
+    int r = 0;
+    for (int k = warp; k < total; k += kBlockWarps) {
+        int b, e;
+        if (single) {
+            b = k * kSpanChunk;
+            e = min(b + kSpanChunk, n);
+        } else {
+            while (k >= s_cpre[r + 1]) ++r;
+            b = s_rb[r] + (k - s_cpre[r]) * kSpanChunk;
+            e = min(b + kSpanChunk, s_re[r]);
+        }
+        for (int i = b + lane; i < e; i += U * 32) {
+            uint2 v[U];
+            if (i + (U - 1) * 32 < e) {
+#pragma unroll
+                for (int u = 0; u < U; ++u) v[u] = __ldg(list + i + u * 32);
+#pragma unroll
+                for (int u = 0; u < U; ++u) one(v[u]);
+            } else {
+#pragma unroll
+                for (int u = 0; u < U; ++u)
+                    if (i + u * 32 < e) v[u] = __ldg(list + i + u * 32);
+#pragma unroll
+                for (int u = 0; u < U; ++u)
+                    if (i + u * 32 < e) one(v[u]);
+            }
+        }
+    }
+    return bad;
+}
+
+template <int DP, bool CHK>
+__device__ __forceinline__ unsigned span_fill_any(const uint2 *list, const int *s_rb, const int *s_re,
+                                                  const int *s_cpre, int nruns, int n, const DirInfo &di, int lo,
+                                                  int wbins, unsigned sb, unsigned bias) {
+    const int nhlo = -(di.hlo + lo);
+    const bool whole = lo == 0 && wbins >= di.R;
+    if (di.swap) {
+        if (whole) return span_fill<DP, CHK, true, false>(list, s_rb, s_re, s_cpre, nruns, n, di.xs8, nhlo, wbins, sb, bias);
+        return span_fill<DP, CHK, true, true>(list, s_rb, s_re, s_cpre, nruns, n, di.xs8, nhlo, wbins, sb, bias);
+    }
+    if (whole) return span_fill<DP, CHK, false, false>(list, s_rb, s_re, s_cpre, nruns, n, di.xs8, nhlo, wbins, sb, bias);
+    return span_fill<DP, CHK, false, true>(list, s_rb, s_re, s_cpre, nruns, n, di.xs8, nhlo, wbins, sb, bias);
+}
+
 // One height window of a segment: every record whose bin is in [lo, lo+wbins).
 // A single window takes the whole list; several windows cull K1 tiles by their
 // height band, so each record is streamed about once over all windows instead
@@ -972,6 +1058,71 @@ __device__ void fill_window(const K2Args &a, const RecT *list, const int32_t *to
                             int lo, int wbins, bool cull, const Hist<PACK, SWZ> &hs, int *s_hit, int *s_nhit,
                             unsigned &bad, bool chk) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if constexpr (PACK && SWZ && std::is_same<RecT, Rec16>::value && (DP == 2 || DP == 3)) {
+        if (!cull || a.ntiles <= kSpanTiles) {
+            // span path: maximal runs of consecutive hit tiles are contiguous list ranges
+            // (tile t's records are list[toff[t], toff[t+1])), streamed in warp chunks
+            const uint2 *l2 = reinterpret_cast<const uint2 *>(list);
+            const unsigned sb = (unsigned)__cvta_generic_to_shared(hs.c);
+            int *s_mask = s_hit, *s_rb = s_hit + kSpanTiles / 32, *s_re = s_rb + kSpanTiles / 2 + 1,
+                *s_cpre = s_re + kSpanTiles / 2 + 1;
+            int nruns = 0;
+            if (cull) {
+                const int nw = (a.ntiles + 31) >> 5;
+                if (threadIdx.x == 0) *s_nhit = 0;
+                for (int t = threadIdx.x; t < nw * 32; t += kBlockThreads) {
+                    bool hit = false;
+                    if (t < a.ntiles) {
+                        int bmin, bmax;
+                        tile_bins(a, di, t, bmin, bmax);
+                        hit = bmax >= lo && bmin < lo + wbins;
+                    }
+                    const unsigned m = __ballot_sync(0xffffffffu, hit);
+                    if (lane == 0) s_mask[t >> 5] = (int)m;
+                }
+                __syncthreads();
+                for (int t = threadIdx.x; t < a.ntiles; t += kBlockThreads) {
+                    const unsigned m = (unsigned)s_mask[t >> 5];
+                    bool start = (m >> (t & 31)) & 1u;
+                    if (start && t > 0) start = !(((unsigned)s_mask[(t - 1) >> 5] >> ((t - 1) & 31)) & 1u);
+                    if (start) {
+                        int w = t >> 5;
+                        unsigned z = ~m & (0xffffffffu << (t & 31));  // first tile after t that is not hit
+                        while (!z && ++w < nw) z = ~(unsigned)s_mask[w];
+                        const int e = z ? min((w << 5) + __ffs(z) - 1, a.ntiles) : a.ntiles;
+                        const int rb = toff[t], re = toff[e];
+                        if (re > rb) {
+                            const int k = atomicAdd(s_nhit, 1);
+                            s_rb[k] = rb;
+                            s_re[k] = re;
+                        }
+                    }
+                }
+                __syncthreads();
+                nruns = *s_nhit;
+                if (warp == 0) {
+                    int run = 0;
+                    for (int base = 0; base < nruns; base += 32) {
+                        const int c = base + lane < nruns
+                                          ? (s_re[base + lane] - s_rb[base + lane] + kSpanChunk - 1) / kSpanChunk : 0;
+                        int inc = c;
+                        for (int k = 1; k < 32; k <<= 1) {
+                            const int y = __shfl_up_sync(0xffffffffu, inc, k);
+                            if (lane >= k) inc += y;
+                        }
+                        if (base + lane < nruns) s_cpre[base + lane] = run + inc - c;
+                        run += __shfl_sync(0xffffffffu, inc, 31);
+                    }
+                    if (lane == 0) s_cpre[nruns] = run;
+                }
+                __syncthreads();
+                if (nruns == 0) return;
+            }
+            if (CHK && chk) bad |= span_fill_any<DP, true>(l2, s_rb, s_re, s_cpre, nruns, n, di, lo, wbins, sb, a.chk_bias);
+            else span_fill_any<DP, false>(l2, s_rb, s_re, s_cpre, nruns, n, di, lo, wbins, sb, 0u);
+            return;
+        }
+    }
     if (!cull) {
         fill_range<8, DP, CHK>(a, list, 0, n, di, lo, wbins, hs, threadIdx.x, kBlockThreads, bad, chk);
         return;
@@ -1455,14 +1606,6 @@ struct UnitShared {
 constexpr size_t kUnitSmem = 222 * 1024;                // dynamic: 227 KB per CTA minus UnitShared
 constexpr int kUnitWords = (int)(kUnitSmem / 4);  // packed words of shared histogram per CTA
 
-__device__ __forceinline__ void red_smem(unsigned addr, unsigned v) {
-    asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(addr), "r"(v));
-}
-__device__ __forceinline__ unsigned atom_smem(unsigned addr, unsigned v) {
-    unsigned old;
-    asm volatile("atom.shared.add.u32 %0, [%1], %2;" : "=r"(old) : "r"(addr), "r"(v));
-    return old;
-}
 
 // Per-unit parameters of the fill: per direction the packed int8 direction, -hlo
 // and the shared byte address of its histogram.

@@ -330,6 +330,40 @@ def test_ect_equals_digital_topology_layer_cake():
                 assert evaluate_ect(r["T"], r["E"], h) == want
 
 
+def test_top_ect_equals_digital_topology_of_closed_complements():
+    """TOP construction: a lower cell takes the min of its top cofaces, so for
+    weights in {0..3} the layer {phi >= k} is the complement of Cl(B_k), the closed
+    subcomplex spanned by the pixels below k, and with S_t the closed subcomplex of cells
+    whose vertices all have height <= t,
+        ECT(xi, t) = sum_k chi(S_t minus Cl(B_k)) = sum_k [chi(S_t) - chi(S_t & Cl(B_k))].
+    Both terms are Euler characteristics of CLOSED cubical complexes, computed here by
+    connected-component labelling (b0 - b1) of their cells drawn on the doubled grid
+    (a cell is a point; faces are 4-neighbours; a unit square of mutually incident cells
+    is filled: the cubical subdivision, same homotopy type) - no (-1)^dim sum, no min."""
+    rng = np.random.default_rng(57)
+    for k in range(20):
+        m0, m1 = (int(x) for x in rng.integers(1, 6, size=2))
+        img = rng.integers(0, 4, size=(m0, m1))
+        g = oracle.Grid(img, "top")
+        # doubled grid of the (m0+1) x (m1+1) vertex lattice; pixel r is the cell (2 r0 + 1, 2 r1 + 1)
+        u0, u1 = np.meshgrid(np.arange(2 * m0 + 1), np.arange(2 * m1 + 1), indexing="ij")
+        for xi in synth.random_directions(2, 2, 5, 900 + k):
+            r = g.transforms(xi)
+            xs = g.xs(xi)
+            lo, hi = g.height_range(xi)
+            # highest vertex of every cell: vertices floor(u/2), ceil(u/2) per axis
+            hmax = sum(np.maximum(int(xs[i]) * (u // 2), int(xs[i]) * ((u + 1) // 2)) for i, u in enumerate((u0, u1)))
+            for h in range(lo - 1, hi + 1):
+                S = hmax <= h
+                want = 0
+                for lev in range(1, 4):
+                    cl = np.zeros(S.shape, dtype=bool)
+                    for r0, r1 in zip(*np.nonzero(img < lev)):
+                        cl[2 * r0:2 * r0 + 3, 2 * r1:2 * r1 + 3] = True  # the pixel and all its faces
+                    want += digital_euler_2d(S) - digital_euler_2d(S & cl)
+                assert evaluate_ect(r["T"], r["E"], h) == want, (img, xi, h)
+
+
 def test_radon_equals_slice_geometry():
     """Radon(xi, t) = chi(phi_{xi=t}): for binary vertex-construction images the
     slice of the subcomplex K by the line {xi = t} is a disjoint union of points and
