@@ -17,7 +17,10 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 # EUCALC_LIB=checked loads libeucalc_checked.so (device bounds checks compiled in;
 # tests only): the same kernels, every EU_DCHECK traps on an out-of-range index
-LIB_PATH = os.path.join(_HERE, "libeucalc_checked.so" if os.environ.get("EUCALC_LIB") == "checked" else "libeucalc.so")
+# EUCALC_LIB=dev loads libeucalc_dev.so (development builds: K2 instantiated for 8-byte
+# records and 32-bit outputs only, anything else returns an error)
+LIB_PATH = os.path.join(_HERE, {"checked": "libeucalc_checked.so", "dev": "libeucalc_dev.so"}.get(
+    os.environ.get("EUCALC_LIB", ""), "libeucalc.so"))
 
 OK, E_ARG, E_NOMEM, E_CUDA, E_NONGENERIC, E_CAPACITY, E_RANGE, E_STATE = range(8)
 DTYPES = {np.dtype(np.uint8): 0, np.dtype(np.int16): 1, np.dtype(np.int32): 2}

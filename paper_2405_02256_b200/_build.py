@@ -12,6 +12,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libeucalc.so")
 LIB_CHECKED = os.path.join(HERE, "libeucalc_checked.so")  # device bounds checks (EU_DCHECK), tests only
+LIB_DEV = os.path.join(HERE, "libeucalc_dev.so")  # development: K2 for 8-byte records / 32-bit outputs only (fast compile)
 INCLUDE = os.path.join(os.path.dirname(HERE), "include")
 OBJ = os.path.join(HERE, "build")
 
@@ -37,12 +38,14 @@ def _nvcc():
     return os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
 
-def build(force: bool = False, verbose: bool = False, checked: bool = False) -> str:
+def build(force: bool = False, verbose: bool = False, checked: bool = False, dev: bool = False) -> str:
     """Compile libeucalc.so (or, checked=True, libeucalc_checked.so with the device
     bounds checks of EU_DCHECK compiled in; objects in build/checked)."""
-    lib = LIB_CHECKED if checked else LIB
-    obj_dir = os.path.join(OBJ, "checked") if checked else OBJ
-    extra = ["-DEUCALC_DEVICE_CHECKS"] if checked else []
+    lib = LIB_CHECKED if checked else LIB_DEV if dev else LIB
+    obj_dir = os.path.join(OBJ, "checked") if checked else os.path.join(OBJ, "dev") if dev else OBJ
+    extra = ["-DEUCALC_DEVICE_CHECKS"] if checked else ["-DEUCALC_DEV_FAST"] if dev else []
+    if dev:  # experiment switches for development builds, e.g. EUCALC_DEV_DEFS="-DEXP_X=1"
+        extra += os.environ.get("EUCALC_DEV_DEFS", "").split()
     if not force and not needs_build(lib):
         return lib
     os.makedirs(obj_dir, exist_ok=True)
@@ -79,4 +82,5 @@ def build(force: bool = False, verbose: bool = False, checked: bool = False) -> 
 if __name__ == "__main__":
     import sys
 
-    print(build(force=True, verbose=True, checked="--checked" in sys.argv))
+    print(build(force="--no-force" not in sys.argv, verbose=True, checked="--checked" in sys.argv,
+                dev="--dev" in sys.argv))

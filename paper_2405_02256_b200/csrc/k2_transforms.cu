@@ -333,12 +333,12 @@ __device__ __forceinline__ void put_c(const OutPtrs<OutT> &o, int p, int h, int 
     const bool cls = MODE == kModeAny ? o.cls : (MODE & kCls);
     const bool alias = MODE == kModeAny ? o.alias : (MODE & kAlias);
     if (ect) {
-        o.eh[p] = (OutT)h;
-        o.ev[p] = (OutT)e;
+        __stcs(o.eh + p, (OutT)h);
+        __stcs(o.ev + p, (OutT)e);
     }
     if (cls) {
-        if (!alias) o.ch[p] = (OutT)h;
-        o.cv[p] = (OutT)cv;
+        if (!alias) __stcs(o.ch + p, (OutT)h);
+        __stcs(o.cv + p, (OutT)cv);
     }
 }
 template <int MODE, typename OutT>
@@ -346,8 +346,8 @@ __device__ __forceinline__ void put_o(const OutPtrs<OutT> &o, int p, int h, int 
     EU_DCHECK(p >= 0 && p < o.cap);
     const bool ord = MODE == kModeAny ? o.ord : (MODE & kOrd);
     if (ord) {
-        o.oh[p] = (OutT)h;
-        o.ov[p] = (OutT)r;
+        __stcs(o.oh + p, (OutT)h);
+        __stcs(o.ov + p, (OutT)r);
     }
 }
 
@@ -468,6 +468,11 @@ __device__ __forceinline__ void emit_group16(const OutPtrs<OutT> &o, const Hist<
     r_run = (pend + 0x8000) >> 16;
 }
 
+template <int MODE, typename OutT>
+__device__ __forceinline__ void emit_words(const OutPtrs<OutT> &o, const int (&wc)[4], const int (&wj)[4], int base,
+                                           int h0, int &e_run, int &r_run, int &pc, int &po, double &ht,
+                                           long long tab_off);
+
 template <int MODE, typename OutT, bool PACK, bool SWZ>
 __device__ __forceinline__ void emit_group(const OutPtrs<OutT> &o, const Hist<PACK, SWZ> &hs, int base, int h0,
                                            int &e_run, int &r_run, int &pc, int &po, double &ht,
@@ -479,6 +484,15 @@ __device__ __forceinline__ void emit_group(const OutPtrs<OutT> &o, const Hist<PA
     const int lane = threadIdx.x & 31;
     int wc[4], wj[4];
     hs.load4(base + 4 * lane, wc, wj, true);
+    emit_words<MODE>(o, wc, wj, base, h0, e_run, r_run, pc, po, ht, tab_off);
+}
+
+// The emission of one 128-bin group given the lane's four bins (sum Delta^-, sum J).
+template <int MODE, typename OutT>
+__device__ __forceinline__ void emit_words(const OutPtrs<OutT> &o, const int (&wc)[4], const int (&wj)[4], int base,
+                                           int h0, int &e_run, int &r_run, int &pc, int &po, double &ht,
+                                           long long tab_off) {
+    const int lane = threadIdx.x & 31;
     int lc = 0, lo = 0, sc = 0, sj = 0;
 #pragma unroll
     for (int s = 0; s < 4; ++s) {
@@ -981,24 +995,36 @@ __device__ __forceinline__ unsigned atom_smem(unsigned addr, unsigned v) {
 constexpr int kSpanTiles = 2048;  // tiles whose hit mask and run tables fit BlockShared::hit
 constexpr int kSpanChunk = 512;   // records per warp work item
 
-template <int DP, bool CHK, bool SWAP, bool CHECK>
-__device__ __noinline__ unsigned span_fill(const uint2 *list, const int *s_rb, const int *s_re, const int *s_cpre,
-                                           int nruns, int n, int xs8, int nhlo, unsigned wbins, unsigned sb,
-                                           unsigned bias) {
+template <int DP, bool CHK>
+__device__ __forceinline__ unsigned span_fill(const uint2 *list, const int *s_rb, const int *s_re, const int *s_cpre,
+                                              int nruns, int n, const DirInfo &di, int lo, int wb, unsigned sb,
+                                              unsigned bias, int nb, int nmax) {
     constexpr int U = 8;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int xs8 = di.xs8, nhlo = -(di.hlo + lo);
+    // the window test also serves a window that covers the whole range (always true);
+    // the antipodal side swaps the record's two 16-bit weights before packed_word
+    const unsigned wbins = (unsigned)wb, sel = di.swap ? 0x1032u : 0x3210u;
+    __shared__ unsigned span_dummy[32];
+    // shared addresses and the byte selector as opaque registers (else the compiler
+    // rematerialises them from the CTA's shared window per record)
+    unsigned dummy = (unsigned)__cvta_generic_to_shared(span_dummy) + 4u * lane, sbr = sb, selr = sel;
+    asm volatile("mov.u32 %0, %0;" : "+r"(dummy));
+    asm volatile("mov.u32 %0, %0;" : "+r"(sbr));
+    asm volatile("mov.u32 %0, %0;" : "+r"(selr));
     unsigned bad = 0;
     auto one = [&](const uint2 r) {
-        const unsigned w = packed_word<SWAP>(r.y);
+        const unsigned w = packed_word<false>(__byte_perm(r.y, 0u, selr));
         int h;
         if (DP == 2) asm("dp2a.lo.u32.s32 %0, %1, %2, %3;" : "=r"(h) : "r"(r.x), "r"(xs8), "r"(nhlo));
         else asm("dp4a.u32.s32 %0, %1, %2, %3;" : "=r"(h) : "r"(r.x), "r"(xs8), "r"(nhlo));
-        EU_DCHECK(CHECK || (unsigned)h < wbins);
-        if (!CHECK || (unsigned)h < wbins) {
-            const unsigned addr = sb + ((unsigned)swz(h) << 2);
-            if constexpr (CHK) bad |= atom_smem(addr, w) + w + bias;
-            else red_smem(addr, w);
-        }
+        // no branch: a record outside the window adds 0 to the lane's own dummy word
+        // (its biased word has no flag bit: bias + 0 + 0)
+        const bool in = (unsigned)h < wbins;
+        const unsigned addr = in ? sbr + ((unsigned)swz(h) << 2) : dummy;
+        const unsigned wv = in ? w : 0u;
+        if constexpr (CHK) bad |= atom_smem(addr, wv) + wv + bias;
+        else red_smem(addr, wv);
     };
     const bool single = nruns == 0;
     const int total = single ? (n + kSpanChunk - 1) / kSpanChunk : s_cpre[nruns];
@@ -1013,6 +1039,7 @@ __device__ __noinline__ unsigned span_fill(const uint2 *list, const int *s_rb, c
             b = s_rb[r] + (k - s_cpre[r]) * kSpanChunk;
             e = min(b + kSpanChunk, s_re[r]);
         }
+        EU_DCHECK(b >= 0 && b <= e && e <= nmax && wb <= nb);
         for (int i = b + lane; i < e; i += U * 32) {
             uint2 v[U];
             if (i + (U - 1) * 32 < e) {
@@ -1031,20 +1058,6 @@ __device__ __noinline__ unsigned span_fill(const uint2 *list, const int *s_rb, c
         }
     }
     return bad;
-}
-
-template <int DP, bool CHK>
-__device__ __forceinline__ unsigned span_fill_any(const uint2 *list, const int *s_rb, const int *s_re,
-                                                  const int *s_cpre, int nruns, int n, const DirInfo &di, int lo,
-                                                  int wbins, unsigned sb, unsigned bias) {
-    const int nhlo = -(di.hlo + lo);
-    const bool whole = lo == 0 && wbins >= di.R;
-    if (di.swap) {
-        if (whole) return span_fill<DP, CHK, true, false>(list, s_rb, s_re, s_cpre, nruns, n, di.xs8, nhlo, wbins, sb, bias);
-        return span_fill<DP, CHK, true, true>(list, s_rb, s_re, s_cpre, nruns, n, di.xs8, nhlo, wbins, sb, bias);
-    }
-    if (whole) return span_fill<DP, CHK, false, false>(list, s_rb, s_re, s_cpre, nruns, n, di.xs8, nhlo, wbins, sb, bias);
-    return span_fill<DP, CHK, false, true>(list, s_rb, s_re, s_cpre, nruns, n, di.xs8, nhlo, wbins, sb, bias);
 }
 
 // One height window of a segment: every record whose bin is in [lo, lo+wbins).
@@ -1093,6 +1106,7 @@ __device__ void fill_window(const K2Args &a, const RecT *list, const int32_t *to
                         const int rb = toff[t], re = toff[e];
                         if (re > rb) {
                             const int k = atomicAdd(s_nhit, 1);
+                            EU_DCHECK(k <= kSpanTiles / 2);
                             s_rb[k] = rb;
                             s_re[k] = re;
                         }
@@ -1118,8 +1132,8 @@ __device__ void fill_window(const K2Args &a, const RecT *list, const int32_t *to
                 __syncthreads();
                 if (nruns == 0) return;
             }
-            if (CHK && chk) bad |= span_fill_any<DP, true>(l2, s_rb, s_re, s_cpre, nruns, n, di, lo, wbins, sb, a.chk_bias);
-            else span_fill_any<DP, false>(l2, s_rb, s_re, s_cpre, nruns, n, di, lo, wbins, sb, 0u);
+            if (CHK && chk) bad |= span_fill<DP, true>(l2, s_rb, s_re, s_cpre, nruns, n, di, lo, wbins, sb, a.chk_bias, hs.nb, n);
+            else span_fill<DP, false>(l2, s_rb, s_re, s_cpre, nruns, n, di, lo, wbins, sb, 0u, hs.nb, n);
             return;
         }
     }
@@ -1451,9 +1465,9 @@ __device__ __forceinline__ void copy_out(const OutPtrs<OutT> &outp, const OutT *
             for (int u = 0; u < U; ++u) {
                 const int i = i0 + u * kBlockThreads;
                 if (i < nc) {
-                    h[u] = eh[i];
-                    v[u] = ev[i];
-                    c[u] = cv[i];
+                    h[u] = __ldcs(eh + i);
+                    v[u] = __ldcs(ev + i);
+                    c[u] = __ldcs(cv + i);
                 }
             }
 #pragma unroll
@@ -1461,12 +1475,12 @@ __device__ __forceinline__ void copy_out(const OutPtrs<OutT> &outp, const OutT *
                 const int i = i0 + u * kBlockThreads;
                 if (i < nc) {
                     if (outp.ect) {
-                        outp.eh[ec + i] = h[u];
-                        outp.ev[ec + i] = v[u];
+                        __stcs(outp.eh + ec + i, h[u]);
+                        __stcs(outp.ev + ec + i, v[u]);
                     }
                     if (outp.cls) {
-                        if (!outp.alias) outp.ch[ec + i] = h[u];
-                        outp.cv[ec + i] = c[u];
+                        if (!outp.alias) __stcs(outp.ch + ec + i, h[u]);
+                        __stcs(outp.cv + ec + i, c[u]);
                     }
                 }
             }
@@ -1479,16 +1493,16 @@ __device__ __forceinline__ void copy_out(const OutPtrs<OutT> &outp, const OutT *
             for (int u = 0; u < U; ++u) {
                 const int i = i0 + u * kBlockThreads;
                 if (i < no) {
-                    h[u] = oh[i];
-                    v[u] = ov[i];
+                    h[u] = __ldcs(oh + i);
+                    v[u] = __ldcs(ov + i);
                 }
             }
 #pragma unroll
             for (int u = 0; u < U; ++u) {
                 const int i = i0 + u * kBlockThreads;
                 if (i < no) {
-                    outp.oh[eo + i] = h[u];
-                    outp.ov[eo + i] = v[u];
+                    __stcs(outp.oh + eo + i, h[u]);
+                    __stcs(outp.ov + eo + i, v[u]);
                 }
             }
         }
@@ -1960,11 +1974,15 @@ cudaError_t launch_p(const K2Args &a, cudaStream_t s, int num_sms) {
 }
 template <typename RecT>
 cudaError_t launch_o(const K2Args &a, cudaStream_t s, int num_sms) {
+#ifdef EUCALC_DEV_FAST  // development builds (libeucalc_dev.so): only 32-bit outputs are instantiated
+    return a.elem_bytes == 4 ? launch_p<RecT, int32_t>(a, s, num_sms) : cudaErrorNotSupported;
+#else
     switch (a.elem_bytes) {
     case 2: return launch_p<RecT, int16_t>(a, s, num_sms);
     case 4: return launch_p<RecT, int32_t>(a, s, num_sms);
     default: return launch_p<RecT, int64_t>(a, s, num_sms);
     }
+#endif
 }
 
 }  // namespace
@@ -1994,6 +2012,10 @@ size_t k2_stage_bytes(const K2Args &a, int num_sms, int64_t *cap) {
 }
 
 cudaError_t launch_k2(const K2Args &a, cudaStream_t s, int num_sms) {
+#ifdef EUCALC_DEV_FAST
+    if (a.units) return a.elem_bytes == 4 ? launch_unit_t<int32_t>(a, s, num_sms) : cudaErrorNotSupported;
+    return a.wide ? cudaErrorNotSupported : launch_o<Rec16>(a, s, num_sms);
+#else
     if (a.units) {
         switch (a.elem_bytes) {
         case 2: return launch_unit_t<int16_t>(a, s, num_sms);
@@ -2002,6 +2024,7 @@ cudaError_t launch_k2(const K2Args &a, cudaStream_t s, int num_sms) {
         }
     }
     return a.wide ? launch_o<Rec32>(a, s, num_sms) : launch_o<Rec16>(a, s, num_sms);
+#endif
 }
 
 int k2_unit_words() { return kUnitWords; }

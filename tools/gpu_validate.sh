@@ -1,4 +1,4 @@
-# Session-8 validation: ubenches, whole GPU suite, smoke, full bench. bash tools/gpu_s8.sh TAG
+# Validation run (under gpurun): ubenches, whole GPU suite, smoke, full bench. bash tools/gpu_validate.sh TAG
 TAG=${1:-s8}; OUT=gpurun_out/$TAG; mkdir -p $OUT
 python -c "import __graft_entry__ as g; g.build()" > $OUT/build.log 2>&1 || { echo BUILD FAILED; tail -20 $OUT/build.log; exit 1; }
 ./tools/ubench/dsmem_atoms > $OUT/dsmem_atoms.jsonl 2>&1; cat $OUT/dsmem_atoms.jsonl
