@@ -1001,26 +1001,35 @@ __global__ void __launch_bounds__(kThreads) k1_copy(K1Args a, long long cpl) {
         }
     };
     constexpr int U = 4;
-    for (int r = warp; r < nr; r += kWarps) {
-        const int c = s_off[r + 1] - s_off[r];
-        EU_DCHECK(c >= 0 && c <= a.cap_r && s_off[r] + c <= a.vcap);
-        const RecT *src = src0 + (long long)r * a.cap_r;
-        RecT *dst = dst0 + s_off[r];
-        int i = lane;
-        for (; i + (U - 1) * 32 < c; i += U * 32) {
-            RecT v[U];
-#pragma unroll
-            for (int u = 0; u < U; ++u) v[u] = src[i + u * 32];
+    // Two regions per warp step, all loads of a step issued before its stores and the
+    // ragged ends predicated: a region holds ~100 records of a gray volume and ~15 of a
+    // binary one, so a scalar tail loop would serialise load -> store round trips.
+    for (int r = warp; r < nr; r += 2 * kWarps) {
+        const int r2 = r + kWarps;
+        const int c1 = s_off[r + 1] - s_off[r], c2 = r2 < nr ? s_off[r2 + 1] - s_off[r2] : 0;
+        EU_DCHECK(c1 >= 0 && c1 <= a.cap_r && s_off[r] + c1 <= a.vcap);
+        EU_DCHECK(c2 >= 0 && c2 <= a.cap_r && (r2 >= nr || s_off[r2] + c2 <= a.vcap));
+        const RecT *src1 = src0 + (long long)r * a.cap_r, *src2 = src0 + (long long)r2 * a.cap_r;
+        RecT *dst1 = dst0 + s_off[r], *dst2 = dst0 + (r2 < nr ? s_off[r2] : 0);
+        const int cm = max(c1, c2);
+        for (int i = lane; i < cm; i += U * 32) {
+            RecT v1[U], v2[U];
 #pragma unroll
             for (int u = 0; u < U; ++u) {
-                dst[i + u * 32] = v[u];
-                stat(v[u]);
+                if (i + u * 32 < c1) v1[u] = src1[i + u * 32];
+                if (i + u * 32 < c2) v2[u] = src2[i + u * 32];
             }
-        }
-        for (; i < c; i += 32) {
-            const RecT v = src[i];
-            dst[i] = v;
-            stat(v);
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                if (i + u * 32 < c1) {
+                    dst1[i + u * 32] = v1[u];
+                    stat(v1[u]);
+                }
+                if (i + u * 32 < c2) {
+                    dst2[i + u * 32] = v2[u];
+                    stat(v2[u]);
+                }
+            }
         }
     }
     if (a.stats_in_copy) {  // |Delta^-| statistics of the list (order-independent integer reductions)
