@@ -161,6 +161,23 @@ def test_block_regime_multiwindow():
     check_fused_ht(img, dirs, "vertex", cr, "cos", 7.5, "f64", pairs=[(0, 0), (0, 6), (0, 7)])
 
 
+def test_block_regime_span_runs_and_tile_fallback():
+    """Multi-window 2-D segments: the span fill streams maximal runs of consecutive hit
+    tiles (a tall narrow image: runs cross tile rows; small windows forced by large
+    directions), and images with more than 2048 K1 tiles take the per-tile culled path;
+    8- and 4-byte outputs."""
+    # 3073 x 97 vertices: L = 3072, xs = (xi_0, 32 xi_1), 4 x 49 tiles
+    tall = np.ascontiguousarray(np.tile(synth.grf_image(256, 11), (13, 1))[:3073, :97])[None]
+    dirs = np.array([[20, -3], [-33, 2], [18, 3], [-1, -1], [64, 1], [127, -3]], np.int32)
+    for eb in (8, 4):
+        _, _, res = run_gpu(tall, dirs, "vertex", elem_bytes=eb)
+        check_transforms(tall, dirs, "vertex", res)
+    big = np.ascontiguousarray(np.tile(synth.grf_image(528, 12), (4, 4)))[None]  # 2112 x 2112: 66 x 33 tiles
+    d2 = np.array([[40, -37], [-3, 2]], np.int32)
+    _, _, res = run_gpu(big, d2, "vertex", elem_bytes=4)
+    check_transforms(big, d2, "vertex", res)
+
+
 def test_block_regime_3d_culled_windows():
     """3-D, several K1 tiles (16x16x8 boxes) and height windows -> tile culling."""
     vol = synth.smooth_volume(40, 77)[None]
