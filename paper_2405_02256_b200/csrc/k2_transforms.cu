@@ -302,7 +302,6 @@ struct OutPtrs {
     OutT *eh, *ev, *oh, *ov, *ch, *cv;
     const double *tab;  // fused HT (NEXT f2): kbar table over u = 2H - L*csum, or NULL
     bool ect, ord, cls, alias;
-    int *wbuf = nullptr;  // block regime, 4-byte outputs: the warp's 128-word shared buffer for coalesced stores
     long long cap;      // entries each array holds (device checks); staging views set their own
     __device__ explicit OutPtrs(const K2Args &a)
         : eh((OutT *)a.ect.h), ev((OutT *)a.ect.v), oh((OutT *)a.ord.h), ov((OutT *)a.ord.v),
@@ -509,55 +508,6 @@ __device__ __forceinline__ void emit_words(const OutPtrs<OutT> &o, const int (&w
     int p_c = pc + (ec & 0xffff), p_o = po + (ec >> 16);
     int e = e_run + (isc - sc), r = r_run + (isj - sj);
     const int hb = h0 + base + 4 * lane;
-    if constexpr (sizeof(OutT) == 4 && MODE == kModeAny) {
-        if (o.wbuf) {
-            // Coalesced emission: a lane's entries sit at scattered positions (stride ~2
-            // entries between lanes), so direct stores touch ~4x the sectors they fill.
-            // Each array's entries of the group are compacted in the warp's shared buffer
-            // and written out by consecutive lanes.
-            const int tcg = __shfl_sync(0xffffffffu, ic, 31);
-            const int ncg = tcg & 0xffff, nog = tcg >> 16;
-            int ev_[4], cv_[4], ov_[4];
-#pragma unroll
-            for (int s = 0; s < 4; ++s) {
-                const int rb = r;
-                e += wc[s];
-                r += wj[s];
-                ev_[s] = e;
-                cv_[s] = rb + wc[s];
-                ov_[s] = r;
-                if (o.tab && wj[s]) ht = fma((double)wj[s], __ldg(o.tab + (long long)(hb + s) + tab_off), ht);
-            }
-            int *wb = o.wbuf;
-            const int lc0 = ec & 0xffff, lo0 = ec >> 16;
-            auto flush = [&](OutT *dst, int n, const int (&val)[4], const int (&nz)[4], int lp) {
-#pragma unroll
-                for (int s = 0; s < 4; ++s)
-                    if (nz[s]) wb[lp++] = val[s];
-                __syncwarp();
-                for (int j = lane; j < n; j += 32) __stcs(dst + j, (OutT)wb[j]);
-                __syncwarp();
-            };
-            const int hh[4] = {hb, hb + 1, hb + 2, hb + 3};
-            if (o.ect) {
-                flush(o.eh + pc, ncg, hh, wc, lc0);
-                flush(o.ev + pc, ncg, ev_, wc, lc0);
-            }
-            if (o.cls) {
-                if (!o.alias) flush(o.ch + pc, ncg, hh, wc, lc0);
-                flush(o.cv + pc, ncg, cv_, wc, lc0);
-            }
-            if (o.ord) {
-                flush(o.oh + po, nog, hh, wj, lo0);
-                flush(o.ov + po, nog, ov_, wj, lo0);
-            }
-            pc += ncg;
-            po += nog;
-            e_run += __shfl_sync(0xffffffffu, isc, 31);
-            r_run += __shfl_sync(0xffffffffu, isj, 31);
-            return;
-        }
-    }
 #pragma unroll
     for (int s = 0; s < 4; ++s) {
         const int rb = r;
@@ -1429,8 +1379,6 @@ __device__ __forceinline__ bool block_segment_staged(const K2Args &a, const OutP
     scr.ect = outp.ect || outp.cls;  // staged heights serve both (T_c = T)
     scr.alias = true;
     scr.cap = a.units ? di.R : a.stage_cap;  // unit path: the segment's slot; else the CTA's buffer
-    // the culled-tile tables are idle during emission: 128 words per warp for coalesced stores
-    if constexpr (sizeof(sh.hit) >= kBlockWarps * kGroup * sizeof(int)) scr.wbuf = sh.hit + warp * kGroup;
     hs.nb = win;
     int pc_carry = 0, po_carry = 0, e_carry = 0, r_carry = 0;
     double ht = 0.0;
