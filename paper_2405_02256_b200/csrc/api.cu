@@ -1173,27 +1173,31 @@ cudaStream_t copy_stream() {
     return s[dev];
 }
 
-// Host outputs of a batch of >= 2 images, in image chunks: the transforms of
-// every chunk are enqueued on `st` into device scratch (a view of the critical
-// handle restricted to the chunk's images, its own CSR), and each chunk's
-// results are copied back on the copy stream while the next chunks compute;
-// offsets are shifted to the global CSR on the host. Capacities and ranges were
-// checked for the whole call by the caller.
+// Host outputs in chunks of images (and, when every chunk is one image, of
+// direction ranges of that image): the transforms of every chunk are enqueued on
+// `st` into device scratch (a view of the critical handle restricted to the
+// chunk's images, the chunk's directions, its own CSR), and each chunk's results
+// are copied back on the copy stream while the next chunks compute; offsets are
+// shifted to the global CSR on the host. Capacities and ranges were checked for
+// the whole call by the caller.
 eucalc_status transforms_host_chunked(eucalc_critical *cr, const int32_t *dirs, int64_t D, eucalc_steps *const outs[3],
-                                      bool cls_alias, int eb, const HtReq *ht, int64_t nch, cudaStream_t st) {
+                                      bool cls_alias, int eb, const HtReq *ht, int64_t nch, int64_t ndch,
+                                      cudaStream_t st) {
     const Complex *cx = cr->cx;
     const int64_t B = cx->batch;
     const size_t esz = (size_t)eb, rsz = cr->wide ? sizeof(Rec32) : sizeof(Rec16);
     const size_t ht_osz = ht && ht->precision == EUCALC_F32 ? 4 : 8;
     cudaStream_t cs = copy_stream();
     if (!cs) return fail(EUCALC_E_CUDA, "copy stream");
-    std::shared_ptr<PlanEntry> pe;
-    eucalc_status s = get_plan(cx, dirs, D, st, pe);
-    if (s != EUCALC_OK) return s;
+    eucalc_status s = EUCALC_OK;
+    // single-image chunks are cut further into `ndch` direction ranges (the CSR is
+    // image-major, so (image, direction range) chunks in that order stay contiguous)
+    if (nch < B) ndch = 1;
+    ndch = std::max<int64_t>(1, std::min<int64_t>(ndch, D));
     struct Chunk {
         eucalc_complex vcx;
         eucalc_critical vcr;
-        int64_t b0 = 0, nb = 0;
+        int64_t b0 = 0, nb = 0, d0 = 0, nd = 0;
         StepsOut dv[3] = {};
         void *dht = nullptr;
         cudaEvent_t ev = nullptr;
@@ -1207,10 +1211,17 @@ eucalc_status transforms_host_chunked(eucalc_critical *cr, const int32_t *dirs, 
         }
     };
     cudaError_t e = cudaSuccess;
-    for (int64_t c = 0; c < nch && s == EUCALC_OK && e == cudaSuccess; ++c) {
+    for (int64_t cc = 0; cc < nch * ndch && s == EUCALC_OK && e == cudaSuccess; ++cc) {
+        const int64_t c = cc / ndch, dc = cc % ndch;
         auto ch = std::make_unique<Chunk>();
         ch->b0 = B * c / nch;
         ch->nb = B * (c + 1) / nch - ch->b0;
+        ch->d0 = D * dc / ndch;
+        ch->nd = D * (dc + 1) / ndch - ch->d0;
+        const int32_t *cdirs = dirs + ch->d0 * cx->ndim;
+        std::shared_ptr<PlanEntry> pe;
+        s = get_plan(cx, cdirs, ch->nd, st, pe);
+        if (s != EUCALC_OK) break;
         Complex &v = ch->vcx;
         v.ndim = cx->ndim;
         v.dtype = cx->dtype;
@@ -1252,7 +1263,7 @@ eucalc_status transforms_host_chunked(eucalc_critical *cr, const int32_t *dirs, 
         int64_t bnd = 0;
         s = bounds(&ch->vcr, pe->p, st, bnd);
         if (s != EUCALC_OK) break;
-        const int64_t Sc = ch->nb * D;
+        const int64_t Sc = ch->nb * ch->nd;
         auto dalloc = [&](size_t bytes) -> void * {
             void *q = nullptr;
             if (cudaMallocAsync(&q, std::max<size_t>(bytes, 1), st) != cudaSuccess) return nullptr;
@@ -1278,7 +1289,7 @@ eucalc_status transforms_host_chunked(eucalc_critical *cr, const int32_t *dirs, 
             if (!ch->dht) e = cudaErrorMemoryAllocation;
         }
         if (e != cudaSuccess) break;
-        s = transforms_impl(&ch->vcr, dirs, D, dsp[0], dsp[1], dsp[2], ht ? &hc : nullptr, nullptr, st);
+        s = transforms_impl(&ch->vcr, cdirs, ch->nd, dsp[0], dsp[1], dsp[2], ht ? &hc : nullptr, nullptr, st);
         if (s != EUCALC_OK) break;
         e = cudaEventCreateWithFlags(&ch->ev, cudaEventDisableTiming);
         if (e == cudaSuccess) e = cudaEventRecord(ch->ev, st);
@@ -1293,7 +1304,7 @@ eucalc_status transforms_host_chunked(eucalc_critical *cr, const int32_t *dirs, 
     // copy back chunk by chunk (each after its own event) while later chunks compute
     int64_t base[3] = {0, 0, 0};
     for (auto &ch : chunks) {
-        const int64_t Sc = ch->nb * D, s0 = ch->b0 * D;
+        const int64_t Sc = ch->nb * ch->nd, s0 = ch->b0 * D + ch->d0;
         if (e == cudaSuccess) e = cudaStreamWaitEvent(cs, ch->ev, 0);
         for (int i = 0; i < 3 && e == cudaSuccess; ++i)
             if (outs[i]) e = cudaMemcpyAsync(outs[i]->offsets + s0, ch->dv[i].off, sizeof(int64_t) * (Sc + 1),
@@ -1416,15 +1427,23 @@ eucalc_status transforms_impl(const eucalc_critical *ccr, const int32_t *dirs, i
     const bool cls_alias = classical && ect && (classical->height == ect->height || !classical->height);
     if (classical && !classical->height && !ect) return fail(EUCALC_E_ARG, "classical height is NULL");
     // host outputs of several images: chunked, copy-back overlapped with the next chunks
-    if (host_out && cx->batch >= 2) {
-        const char *ev = getenv("EUCALC_HOST_CHUNKS");
+    // (a chunk of one image is cut further into direction ranges when the call is large:
+    // more than 2^22 output entries per range, so small calls keep one launch per image)
+    if (host_out) {
+        const char *ev = getenv("EUCALC_HOST_CHUNKS"), *dv = getenv("EUCALC_HOST_DIR_CHUNKS");
         const int64_t nch = std::min<int64_t>(cx->batch, ev ? std::max(1, atoi(ev)) : 4);
-        if (nch >= 2) {
+        int64_t ndch = 1;
+        if (nch == cx->batch) {
+            const int64_t per_image = bnd / std::max<int64_t>(1, cx->batch);
+            ndch = dv ? std::max(1, atoi(dv)) : (per_image >> 22) ? 2 : 1;  // measured: 2 best (config 4), more ranges leave SMs idle
+            ndch = std::max<int64_t>(1, std::min<int64_t>(ndch, D));
+        }
+        if (nch * ndch >= 2) {
             bool all_host = true;  // every output on the host (mixed placements take the plain path)
             for (eucalc_steps *o : outs)
                 if (o && is_device_ptr(o->value)) all_host = false;
             if (ht && is_device_ptr(ht->out)) all_host = false;
-            if (all_host) return transforms_host_chunked(cr, dirs, D, outs, cls_alias, eb, ht, nch, st);
+            if (all_host) return transforms_host_chunked(cr, dirs, D, outs, cls_alias, eb, ht, nch, ndch, st);
         }
     }
     // host outputs -> device scratch (sized by the tight bound)

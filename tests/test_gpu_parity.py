@@ -260,18 +260,24 @@ def test_output_widths_and_shared_heights():
     assert r["ect"]["value"].element_size() == 4
 
 
-@pytest.mark.parametrize("chunks", ["1", "3", None], ids=["plain", "3-chunks", "default-chunks"])
-def test_host_buffers_match_device(chunks, monkeypatch):
-    """Host outputs (copied back chunk by chunk of images while the next chunks
-    compute, offsets shifted on the host; EUCALC_HOST_CHUNKS=1: one pass) equal
-    the device outputs, with and without shared classical heights and the fused HT,
-    in 2-D (warp regime) and 3-D (unit path)."""
+@pytest.mark.parametrize("chunks,dchunks", [("1", None), ("3", None), (None, None), ("8", "3"), (None, "16")],
+                         ids=["plain", "3-chunks", "default-chunks", "image-and-3-direction-chunks",
+                              "one-direction-per-chunk"])
+def test_host_buffers_match_device(chunks, dchunks, monkeypatch):
+    """Host outputs (copied back chunk by chunk of images, and of direction ranges of
+    single-image chunks, while the next chunks compute, offsets shifted on the host;
+    EUCALC_HOST_CHUNKS=1: one pass) equal the device outputs, with and without shared
+    classical heights and the fused HT, in 2-D (warp regime) and 3-D (unit path), for a
+    batch and for a single image."""
     if chunks:
         monkeypatch.setenv("EUCALC_HOST_CHUNKS", chunks)
+    if dchunks:
+        monkeypatch.setenv("EUCALC_HOST_DIR_CHUNKS", dchunks)
     vol = synth.smooth_volume(40, 93)
     cases = [(synth.blob_images(8, 28, 2), synth.random_directions(16, 2, 16, 4)),
              (np.stack([vol, (vol > np.median(vol)).astype(np.uint8), vol[::-1].copy()]),
-              synth.random_directions(9, 3, 20, 6))]
+              synth.random_directions(9, 3, 20, 6)),
+             (vol[None], synth.random_directions(11, 3, 20, 7))]
     for images, dirs in cases:
         cx = eu.build_complex(images, "vertex")
         cr = eu.critical_points(cx)
