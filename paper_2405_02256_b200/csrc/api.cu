@@ -1596,6 +1596,22 @@ eucalc_status transforms_impl(const eucalc_critical *ccr, const int32_t *dirs, i
                         a.stage_img = pe->stage_img;
                         a.stage_cap = cx->batch * pe->stage_img;
                         unit = true;
+                        // several images: all units of the heaviest image first (EUCALC_K2_IMG_ORDER=0: interleaved)
+                        const char *io = getenv("EUCALC_K2_IMG_ORDER");
+                        if (cx->batch > 1 && !(io && io[0] == '0')) {
+                            std::vector<int64_t> w(cx->batch, 0);
+                            for (int64_t b = 0; b < cx->batch; ++b)
+                                for (int q = 0; q < cr->Q; ++q) w[b] += cr->h_count[b * cr->Q + q];
+                            std::vector<int32_t> ord(cx->batch);
+                            std::iota(ord.begin(), ord.end(), 0);
+                            std::stable_sort(ord.begin(), ord.end(), [&](int32_t x, int32_t y) { return w[x] > w[y]; });
+                            int32_t *d_ord = (int32_t *)dalloc(sizeof(int32_t) * cx->batch);
+                            if (d_ord && cudaMemcpyAsync(d_ord, ord.data(), sizeof(int32_t) * cx->batch,
+                                                         cudaMemcpyHostToDevice, st) == cudaSuccess)
+                                a.img_order = d_ord;  // pageable source: staged before the call returns
+                            else
+                                cudaGetLastError();
+                        }
                     } else {
                         cudaGetLastError();
                     }

@@ -1783,8 +1783,11 @@ __global__ void __launch_bounds__(kBlockThreads, 1) k2_unit(K2Args a, int split_
         __syncthreads();
         const long long t = sh.seg;
         if (t >= total) break;
-        const long long b = t % a.batch;   // images interleaved: equal units of all images run together
-        const int4 un = a.units[t / a.batch];  // {first index into unit_dirs, G, q, swap}
+        // image-major, heaviest image first: the CTAs in flight stream the same few lists
+        // (L2) and the short units of light images fill the tail of the heavy ones;
+        // without an order, images interleaved (equal units of all images run together)
+        const long long b = a.img_order ? a.img_order[t / a.nunits] : t % a.batch;
+        const int4 un = a.units[a.img_order ? t % a.nunits : t / a.batch];  // {first index into unit_dirs, G, q, swap}
         const int G = un.y;
         UnitParams pp;
         int base[kUnitMax];
