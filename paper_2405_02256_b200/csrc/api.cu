@@ -362,9 +362,16 @@ struct PlanEntry {
     int4 *d_units = nullptr;
     int32_t *d_unit_dirs = nullptr;
     int64_t *d_stage_base = nullptr;
+    // the same directions in units balanced for a single image (plan_units_balanced)
+    bool bal_built = false;
+    int64_t bal_nunits = 0;
+    int4 *d_bal_units = nullptr;
+    int32_t *d_bal_unit_dirs = nullptr;
     ~PlanEntry() {
         cudaFree(d_units);
         cudaFree(d_unit_dirs);
+        cudaFree(d_bal_units);
+        cudaFree(d_bal_unit_dirs);
         cudaFree(d_stage_base);
         // cudaFree synchronises the device, so no in-flight kernel still reads these
         cudaFree(d_info);
@@ -469,7 +476,9 @@ eucalc_status plan_units(PlanEntry &pe) {
     });
     std::vector<int4> units;
     std::vector<int32_t> dirs_out;
-    const int gmax = k2_unit_max(), words = k2_unit_words();
+    int gmax = k2_unit_max();
+    const int words = k2_unit_words();
+    if (const char *v = getenv("EUCALC_K2_UNIT_G")) gmax = std::max(1, std::min(gmax, atoi(v)));  // measurement hook
     for (int64_t i = 0; i < D;) {
         int4 u{(int)dirs_out.size(), 0, p.info[idx[i]].q, p.info[idx[i]].swap};
         int64_t off = 0;
@@ -501,6 +510,84 @@ eucalc_status plan_units(PlanEntry &pe) {
     pe.nunits = (int64_t)units.size();
     pe.stage_img = acc;
     pe.units_built = true;
+    return EUCALC_OK;
+}
+
+// Units for ONE image on `sms` SMs. Every unit streams its whole list, so units of
+// kUnitMax directions minimise the work, but U units of equal cost on P SMs take
+// ceil(U / P) waves (config 4: 256 units on 148 SMs = 2 waves, the second 73% full).
+// Here the unit count is raised to the next multiple of P by giving the (pair, side)
+// groups with the most directions per unit one more unit each, and a group's
+// directions are spread evenly over its units (sizes differ by at most one): 296
+// units of 4 or 3 directions take one wave of each (cost of a unit ~ 0.11 + 0.22 G of
+// a 4-direction unit: 1.78 against 2.0). Only taken when it lowers that estimate;
+// with several images the light images' units fill the last wave instead (plan_units).
+// Built after plan_units (shares its staging slots). bal_nunits == 0: no gain.
+eucalc_status plan_units_balanced(PlanEntry &pe, int sms) {
+    std::lock_guard<std::mutex> lk(pe.unit_mu);
+    if (pe.bal_built) return EUCALC_OK;
+    pe.bal_built = true;
+    const DirPlan &p = pe.p;
+    const int64_t D = (int64_t)p.info.size();
+    const int gmax = k2_unit_max(), words = k2_unit_words();
+    if (pe.nunits <= sms || pe.nunits % sms == 0) return EUCALC_OK;
+    std::vector<int32_t> idx(D);
+    std::iota(idx.begin(), idx.end(), 0);
+    auto key = [&](int32_t d) { return p.info[d].q * 2 + p.info[d].swap; };
+    std::stable_sort(idx.begin(), idx.end(), [&](int32_t x, int32_t y) {
+        if (key(x) != key(y)) return key(x) < key(y);
+        return p.info[x].R > p.info[y].R;
+    });
+    struct Group { int64_t i0, n, u; };
+    std::vector<Group> groups;
+    for (int64_t i = 0; i < D;) {
+        int64_t j = i;
+        while (j < D && key(idx[j]) == key(idx[i])) ++j;
+        groups.push_back({i, j - i, (j - i + gmax - 1) / gmax});
+        i = j;
+    }
+    int64_t U = 0;
+    for (const Group &g : groups) U += g.u;
+    const int64_t target = (U + sms - 1) / sms * sms;
+    while (U < target) {  // one more unit for the group with the most directions per unit
+        Group *best = nullptr;
+        for (Group &g : groups)
+            if (g.u < g.n && (!best || g.n * best->u > best->n * g.u)) best = &g;
+        if (!best) break;
+        ++best->u;
+        ++U;
+    }
+    std::vector<int4> units;
+    std::vector<int32_t> dirs_out;
+    for (const Group &g : groups) {
+        int64_t i = g.i0;
+        for (int64_t k = 0; k < g.u; ++k) {
+            // the larger units take the directions with the smaller R (sorted by decreasing R)
+            const int64_t sz = g.n / g.u + (k >= g.u - g.n % g.u ? 1 : 0);
+            int4 u{(int)dirs_out.size(), 0, p.info[idx[g.i0]].q, p.info[idx[g.i0]].swap};
+            int64_t off = 0;
+            for (int64_t t = 0; t < sz; ++t, ++i) {
+                off += (p.info[idx[i]].R + 127) / 128 * 128;
+                dirs_out.push_back(idx[i]);
+                ++u.y;
+            }
+            if (off > words || u.y > gmax) return EUCALC_OK;  // does not fit shared memory: keep plan_units' units
+            units.push_back(u);
+        }
+    }
+    // estimated makespans (units of a kUnitMax-direction unit), heaviest units first
+    auto cost = [&](int G) { return 0.107 + 0.223 * G * 4.0 / gmax; };
+    std::stable_sort(units.begin(), units.end(), [](const int4 &x, const int4 &y) { return x.y > y.y; });
+    std::vector<double> load(sms, 0.0);
+    for (const int4 &u : units) *std::min_element(load.begin(), load.end()) += cost(u.y);
+    const double bal = *std::max_element(load.begin(), load.end());
+    const double plain = (double)((pe.nunits + sms - 1) / sms) * cost(gmax);
+    if (bal >= 0.97 * plain) return EUCALC_OK;
+    CK(cudaMalloc(&pe.d_bal_units, sizeof(int4) * units.size()));
+    CK(cudaMalloc(&pe.d_bal_unit_dirs, sizeof(int32_t) * dirs_out.size()));
+    CK(cudaMemcpy(pe.d_bal_units, units.data(), sizeof(int4) * units.size(), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(pe.d_bal_unit_dirs, dirs_out.data(), sizeof(int32_t) * dirs_out.size(), cudaMemcpyHostToDevice));
+    pe.bal_nunits = (int64_t)units.size();
     return EUCALC_OK;
 }
 
@@ -1592,6 +1679,14 @@ eucalc_status transforms_impl(const eucalc_critical *ccr, const int32_t *dirs, i
                         a.units = pe->d_units;
                         a.nunits = pe->nunits;
                         a.unit_dirs = pe->d_unit_dirs;
+                        // one image: units balanced over the SMs (EUCALC_K2_UNIT_BALANCE=0: off)
+                        const char *ub = getenv("EUCALC_K2_UNIT_BALANCE");
+                        if (cx->batch == 1 && !(ub && ub[0] == '0') &&
+                            plan_units_balanced(*pe, num_sms()) == EUCALC_OK && pe->bal_nunits > 0) {
+                            a.units = pe->d_bal_units;
+                            a.nunits = pe->bal_nunits;
+                            a.unit_dirs = pe->d_bal_unit_dirs;
+                        }
                         a.stage_base = pe->d_stage_base;
                         a.stage_img = pe->stage_img;
                         a.stage_cap = cx->batch * pe->stage_img;
