@@ -214,6 +214,36 @@ def test_block_regime_checked_packed_bins(env, monkeypatch):
     check_transforms(img, d2, "top", res)
 
 
+def same_streams(x, y):
+    for k in x:
+        np.testing.assert_array_equal(x[k]["offsets"], y[k]["offsets"])
+        n = x[k]["offsets"][-1]
+        np.testing.assert_array_equal(x[k]["height"][:n], y[k]["height"][:n])
+        np.testing.assert_array_equal(x[k]["value"][:n], y[k]["value"][:n])
+
+
+def test_unit_path_image_order_and_balanced_units(monkeypatch):
+    """3-D unit path: a batch whose images differ in list size (tickets run image-major,
+    heaviest image first, the light image listed first here) and a single image with more
+    units than SMs (units balanced over the SMs: 3 and 4 directions per unit), against the
+    oracle; and the interleaved / unbalanced plans give identical outputs."""
+    vol = synth.smooth_volume(64, 81)
+    batch = np.stack([(vol > np.median(vol)).astype(np.uint8), vol])
+    dirs, _ = synth.fibonacci_directions(40, 12.0)
+    _, _, res = run_gpu(batch, dirs, "vertex", elem_bytes=4)
+    check_transforms(batch, dirs, "vertex", res, pairs=[(b, d) for b in (0, 1) for d in (0, 7, 19, 39)])
+    monkeypatch.setenv("EUCALC_K2_IMG_ORDER", "0")
+    _, _, res0 = run_gpu(batch, dirs, "vertex", elem_bytes=4)
+    same_streams(res, res0)
+    many, _ = synth.fibonacci_directions(700, 12.0)  # 175 units of 4 > 148 SMs
+    one = vol[None]
+    _, _, resb = run_gpu(one, many, "vertex", elem_bytes=4)
+    check_transforms(one, many, "vertex", resb, pairs=[(0, d) for d in (0, 1, 350, 698, 699)])
+    monkeypatch.setenv("EUCALC_K2_UNIT_BALANCE", "0")
+    _, _, resu = run_gpu(one, many, "vertex", elem_bytes=4)
+    same_streams(resb, resu)
+
+
 def test_negative_and_int32_weights():
     rng = np.random.default_rng(3)
     images = rng.integers(-40000, 40000, size=(2, 12, 11)).astype(np.int32)
