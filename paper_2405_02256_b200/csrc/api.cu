@@ -1713,8 +1713,45 @@ eucalc_status transforms_impl(const eucalc_critical *ccr, const int32_t *dirs, i
                 }
             }
         }
+        // block regime, one CTA per segment: fixed staging slots per segment (as in the unit
+        // path) + k2_scan + k2_unit_copy instead of look-back and copy-out inside the
+        // kernel, when the slots (6 arrays x batch x sum of R) fit a memory budget
+        // (EUCALC_K2_SLOTS=0: per-CTA staging with look-back)
+        bool slots = false;
+        {
+            const char *ev = getenv("EUCALC_K2_SLOTS");
+            if (!unit && !(ev && ev[0] == '0') && k2_block_regime(a) && S >= 2 * (int64_t)num_sms()) {
+                s = plan_units(*pe);  // builds the per-direction slot offsets
+                if (s != EUCALC_OK) {
+                    free_scratch();
+                    return s;
+                }
+                const size_t sb = 6 * (size_t)cx->batch * (size_t)pe->stage_img * esz;
+                // budget: 16 GB and an eighth of the device's memory (queried once: cudaMemGetInfo
+                // costs ~1 ms per call); a failed allocation falls back to per-CTA staging
+                static size_t total_mem[64] = {};
+                int dev = 0;
+                cudaGetDevice(&dev);
+                if (dev >= 0 && dev < 64 && !total_mem[dev]) {
+                    size_t free_b = 0, total_b = 0;
+                    if (cudaMemGetInfo(&free_b, &total_b) == cudaSuccess) total_mem[dev] = total_b;
+                }
+                const size_t budget = dev >= 0 && dev < 64 ? total_mem[dev] / 8 : 0;
+                if (pe->stage_img > 0 && sb <= (size_t(16) << 30) && sb <= budget) {
+                    a.stage = dalloc(sb);
+                    if (a.stage) {
+                        a.stage_base = pe->d_stage_base;
+                        a.stage_img = pe->stage_img;
+                        a.stage_cap = cx->batch * pe->stage_img;
+                        slots = true;
+                    } else {
+                        cudaGetLastError();
+                    }
+                }
+            }
+        }
         int64_t scap = 0;
-        const size_t sbytes = unit ? 0 : k2_stage_bytes(a, num_sms(), &scap);
+        const size_t sbytes = (unit || slots) ? 0 : k2_stage_bytes(a, num_sms(), &scap);
         if (sbytes) {
             a.stage = dalloc(sbytes);
             a.stage_cap = a.stage ? scap : 0;

@@ -1378,7 +1378,7 @@ __device__ __forceinline__ bool block_segment_staged(const K2Args &a, const OutP
     scr.ov = base + 5 * a.stage_cap;
     scr.ect = outp.ect || outp.cls;  // staged heights serve both (T_c = T)
     scr.alias = true;
-    scr.cap = a.units ? di.R : a.stage_cap;  // unit path: the segment's slot; else the CTA's buffer
+    scr.cap = (a.units || a.stage_base) ? di.R : a.stage_cap;  // the segment's slot; else the CTA's buffer
     hs.nb = win;
     int pc_carry = 0, po_carry = 0, e_carry = 0, r_carry = 0;
     double ht = 0.0;
@@ -1528,6 +1528,33 @@ __global__ void __launch_bounds__(kBlockThreads, 1) k2_block(K2Args a, long long
         use_packed = proven || (a.max_rec < 16384 && !a.no_chk);
         return proven ? 0u : a.chk_mask;
     };
+    if (a.stage && a.stage_base) {
+        // Slot mode: every segment is filled once and emitted into its own fixed staging
+        // slot (R_d entries per array, as in the unit path), its counts go to cnt_c/cnt_o;
+        // k2_scan then turns the counts into the CSR offsets and k2_unit_copy moves the
+        // staged entries there at copy-kernel bandwidth - no look-back between segments
+        // and no copy-out inside this kernel's segment loop.
+        OutT *stage = reinterpret_cast<OutT *>(a.stage);
+        while (true) {
+            __syncthreads();
+            if (threadIdx.x == 0) sh.seg = (long long)atomicAdd(a.ticket, 1u);
+            __syncthreads();
+            const long long s = sh.seg;
+            if (s >= nseg) break;
+            const long long b = s / a.D, d = s % a.D;
+            OutT *slot = stage + b * a.stage_img + a.stage_base[d];
+            bool packed;
+            const unsigned m = packed_mask(d, packed);
+            if (!packed || !block_segment_staged<true, DP, RecT, OutT>(a, outp, hist, 2 * win, s, b, d, sh, m, slot))
+                block_segment_staged<false, DP, RecT, OutT>(a, outp, hist, win, s, b, d, sh, 0u, slot);
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                a.cnt_c[s] = sh.cnt[0];
+                a.cnt_o[s] = sh.cnt[1];
+            }
+        }
+        return;
+    }
     if (a.stage) {
         // Pipelined: segment s is filled and emitted into staging buffer `cur` and
         // its aggregate published; then the PREVIOUS segment of this CTA is looked
@@ -1837,10 +1864,10 @@ __global__ void __launch_bounds__(kBlockThreads, 1) k2_unit(K2Args a, int split_
 }
 
 // Staged entries of every segment -> the CSR (one CTA per segment, grid-stride;
-// four elements per array in flight per thread before their stores).
+// eight elements per array in flight per thread before their stores).
 template <typename OutT>
 __global__ void __launch_bounds__(512) k2_unit_copy(K2Args a) {
-    constexpr int U = 4;
+    constexpr int U = 8;
     const OutPtrs<OutT> outp(a);
     const OutT *stage = reinterpret_cast<const OutT *>(a.stage);
     const long long S = a.batch * a.D, cap = a.stage_cap;
@@ -1968,6 +1995,12 @@ cudaError_t launch_t(const K2Args &a, cudaStream_t s, int num_sms) {
     long long grid = std::min<long long>(nseg, num_sms);
     kern<<<(unsigned)grid, kBlockThreads, kBlockSmem, s>>>(a, nseg, win);
     count_launch();
+    if (a.stage && a.stage_base) {  // slot mode: offsets from the counts, then the staged entries to the CSR
+        const long long ntiles = (nseg + 1 + kScanTile - 1) / kScanTile;
+        k2_scan<<<(unsigned)ntiles, kScanThreads, 0, s>>>(a, a.cnt_c, a.cnt_o, nseg, a.flags);
+        k2_unit_copy<OutT><<<(unsigned)std::min<long long>(nseg, 8LL * num_sms), 512, 0, s>>>(a);
+        count_launch(2);
+    }
     return cudaGetLastError();
 }
 

@@ -188,8 +188,11 @@ def test_block_regime_3d_culled_windows():
 
 @pytest.mark.parametrize("env", [{}, {"EUCALC_K2_CHK_BITS": "1"}, {"EUCALC_K2_CHK_BITS": "6"},
                                  {"EUCALC_K2_NO_CHK": "1"}, {"EUCALC_K2_UNIT": "0"},
-                                 {"EUCALC_K2_UNIT": "0", "EUCALC_K2_CHK_BITS": "1"}],
-                         ids=["checked", "restart", "partial", "split", "per-segment", "per-segment-restart"])
+                                 {"EUCALC_K2_UNIT": "0", "EUCALC_K2_CHK_BITS": "1"},
+                                 {"EUCALC_K2_UNIT": "0", "EUCALC_K2_SLOTS": "0"},
+                                 {"EUCALC_K2_UNIT": "0", "EUCALC_K2_SLOTS": "0", "EUCALC_K2_CHK_BITS": "1"}],
+                         ids=["checked", "restart", "partial", "split", "per-segment", "per-segment-restart",
+                              "per-segment-lookback", "per-segment-lookback-restart"])
 def test_block_regime_checked_packed_bins(env, monkeypatch):
     """Block regime with packed 16+16 bins whose exactness no bound proves: every
     add is checked and a flagged segment restarts with split bins. The test hooks
@@ -212,6 +215,23 @@ def test_block_regime_checked_packed_bins(env, monkeypatch):
     d2 = np.concatenate([synth.random_directions(4, 2, 90, 6), np.array([[90, -89]], np.int32)])
     cx, cr, res = run_gpu(img, d2, "top")
     check_transforms(img, d2, "top", res)
+
+
+@pytest.mark.parametrize("restart", [False, True], ids=["packed", "restart-split"])
+def test_block_regime_slot_mode(restart, monkeypatch):
+    """Block regime with >= 2 x SMs segments: every segment staged in its own slot, offsets
+    by k2_scan, entries moved by k2_unit_copy (no look-back); against the oracle on sampled
+    segments and identical to the look-back path on all of them, also when every segment
+    restarts with split bins (two windows)."""
+    if restart:
+        monkeypatch.setenv("EUCALC_K2_CHK_BITS", "1")
+    img = np.stack([synth.grf_image(160, 21), 255 - synth.grf_image(160, 22)])
+    dirs = synth.random_directions(200, 2, 90, 23)
+    _, _, res = run_gpu(img, dirs, "vertex", elem_bytes=4)
+    check_transforms(img, dirs, "vertex", res, pairs=[(b, d) for b in (0, 1) for d in (0, 57, 199)])
+    monkeypatch.setenv("EUCALC_K2_SLOTS", "0")
+    _, _, res0 = run_gpu(img, dirs, "vertex", elem_bytes=4)
+    same_streams(res, res0)
 
 
 def same_streams(x, y):
