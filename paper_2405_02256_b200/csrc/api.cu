@@ -362,6 +362,7 @@ struct PlanEntry {
     int4 *d_units = nullptr;
     int32_t *d_unit_dirs = nullptr;
     int64_t *d_stage_base = nullptr;
+    int32_t *d_dir_by_R = nullptr;  // directions by decreasing R (slot mode's segment order)
     // the same directions in units balanced for a single image (plan_units_balanced)
     bool bal_built = false;
     int64_t bal_nunits = 0;
@@ -373,6 +374,7 @@ struct PlanEntry {
         cudaFree(d_bal_units);
         cudaFree(d_bal_unit_dirs);
         cudaFree(d_stage_base);
+        cudaFree(d_dir_by_R);
         // cudaFree synchronises the device, so no in-flight kernel still reads these
         cudaFree(d_info);
         cudaFree(d_csum);
@@ -506,6 +508,11 @@ eucalc_status plan_units(PlanEntry &pe) {
         CK(cudaMemcpy(pe.d_units, units.data(), sizeof(int4) * units.size(), cudaMemcpyHostToDevice));
         CK(cudaMemcpy(pe.d_unit_dirs, dirs_out.data(), sizeof(int32_t) * dirs_out.size(), cudaMemcpyHostToDevice));
         CK(cudaMemcpy(pe.d_stage_base, base.data(), sizeof(int64_t) * D, cudaMemcpyHostToDevice));
+        std::vector<int32_t> by_r(D);
+        std::iota(by_r.begin(), by_r.end(), 0);
+        std::stable_sort(by_r.begin(), by_r.end(), [&](int32_t x, int32_t y) { return p.info[x].R > p.info[y].R; });
+        CK(cudaMalloc(&pe.d_dir_by_R, sizeof(int32_t) * D));
+        CK(cudaMemcpy(pe.d_dir_by_R, by_r.data(), sizeof(int32_t) * D, cudaMemcpyHostToDevice));
     }
     pe.nunits = (int64_t)units.size();
     pe.stage_img = acc;
@@ -1743,6 +1750,7 @@ eucalc_status transforms_impl(const eucalc_critical *ccr, const int32_t *dirs, i
                         a.stage_base = pe->d_stage_base;
                         a.stage_img = pe->stage_img;
                         a.stage_cap = cx->batch * pe->stage_img;
+                        a.seg_order = pe->d_dir_by_R;
                         slots = true;
                     } else {
                         cudaGetLastError();

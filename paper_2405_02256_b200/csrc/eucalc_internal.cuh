@@ -211,6 +211,7 @@ struct K2Args {
     const int64_t *stage_base;  // [D] staging slot of direction d within an image (prefix of R)
     int64_t stage_img;          // staging entries per image (sum of R)
     const int32_t *img_order;   // [batch] images by decreasing list size (all units of the heaviest image first), or NULL
+    const int32_t *seg_order;   // [D] slot mode: directions by decreasing R (longest segments first), or NULL
     // fused HT (NEXT f2): kbar table (fp64) over u in [ht_U0, ...), or NULL
     const double *ht_tab;
     int64_t ht_U0, L;

@@ -1539,9 +1539,11 @@ __global__ void __launch_bounds__(kBlockThreads, 1) k2_block(K2Args a, long long
             __syncthreads();
             if (threadIdx.x == 0) sh.seg = (long long)atomicAdd(a.ticket, 1u);
             __syncthreads();
-            const long long s = sh.seg;
-            if (s >= nseg) break;
-            const long long b = s / a.D, d = s % a.D;
+            const long long t = sh.seg;
+            if (t >= nseg) break;
+            // any order is valid here: the directions with the largest height range first, so
+            // the last wave holds the shortest segments
+            const long long b = t / a.D, d = a.seg_order ? a.seg_order[t % a.D] : t % a.D, s = b * a.D + d;
             OutT *slot = stage + b * a.stage_img + a.stage_base[d];
             bool packed;
             const unsigned m = packed_mask(d, packed);
